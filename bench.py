@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py -- PLAS sort hot path on BASELINE.json configs[2] (1024^2 x 14 fp32).
+
+One "step" = one full PLAS sort to convergence of a 1024x1024 grid of 14
+standardised 3DGS-like attributes (seeded synthetic stand-in).
+  value : grid-elems/s = N * passes / device time, inputs resident in HBM,
+          timed with CUDA events around each sort (L2 flushed before each step);
+  e2e   : the same metric through the public API sort_grid() with the features
+          in pinned host memory (H2D of the fp64 features + D2H of the int64
+          permutation inside the timed region);
+  roofline: the dominant kernel's algorithmic bytes / its CUDA-event duration,
+          from an event-instrumented host-stepped replay of the same sort;
+  cpu_baseline: the reference's own CPU sort (baseline/_ref/sogs, numba+SciPy)
+          on a bounded prefix of the same workload (oracle port if absent).
+N > 1 (torchrun): every rank sorts its own independent grid (data seed = rank),
+no data-path collective; value = sum of rank units / max rank time ("weak").
+"""
+
+import argparse
+import json
+import math
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+METRIC = "plas_sort_grid_elems_per_s"
+UNIT = "grid-elems/s"
+WORKLOADS = {
+    "C0": dict(cfg=dict(radius_decay=0.5, improvement_threshold=1e-5)),
+    "C1": dict(cfg={}),
+    "C2": dict(cfg={}),
+    "C3": dict(cfg={}),
+    "C4": dict(cfg={}),
+}
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    p.add_argument("--side", type=int, default=None, help="override grid side (testing)")
+    p.add_argument("--mode", default="device", choices=["device", "parity"])
+    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work per sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-profile", action="store_true")
+    return p.parse_args(argv)
+
+
+# ---------------------------------------------------------------------------- ranks
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return dist if world > 1 else None
+
+
+def combine(units, seconds, dist, device):
+    """Whole-job aggregate: sum of units over ranks, max of time over ranks."""
+    if dist is None:
+        return float(units), float(seconds)
+    import torch
+    u = torch.tensor([float(units)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(seconds)], dtype=torch.float64, device=device)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(u.item()), float(t.item())
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        if shutil.which("nvidia-smi") is None:
+            return
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        self.fh = open(self.path, "w")
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-lms", "200"],
+                                     stdout=self.fh, stderr=subprocess.DEVNULL)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU reference
+def cpu_reference_sample(features, cfg_kw, budget_s, threads=None):
+    """Time the reference CPU sort on a bounded prefix of the workload.
+
+    Prefers the unmodified reference package installed in baseline/_ref (numba +
+    SciPy, run through its public sort_grid_report); the prefix is bounded by
+    stopping at the first pass that would start after `budget_s` (a counting
+    wrapper around the reference's own _reassign_pass).  Falls back to the C
+    oracle port (oracle/) with the same bound.
+    """
+    n = features.shape[0]
+    threads = threads or os.cpu_count()
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "sogs")):
+        os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_bench"))
+        sys.dont_write_bytecode = True
+        if ref_dir not in sys.path:
+            sys.path.insert(0, ref_dir)
+        import sogs.plas as rp
+        rp.sort_grid(np.random.default_rng(0).random((64, 3)), rp.SortConfig(), threads=threads)  # JIT warm-up
+
+        class _Stop(Exception):
+            pass
+
+        state = {"passes": 0, "t0": None, "t_end": None}
+        orig = rp._reassign_pass
+
+        def counted(*a, **k):
+            now = time.perf_counter()
+            if now - state["t0"] >= budget_s:
+                state["t_end"] = now
+                raise _Stop()
+            orig(*a, **k)
+            state["passes"] += 1
+
+        rp._reassign_pass = counted
+        state["t0"] = time.perf_counter()
+        try:
+            rp.sort_grid_report(features, rp.SortConfig(**cfg_kw), threads=threads)
+            state["t_end"] = time.perf_counter()
+            done = "full sort"
+        except _Stop:
+            done = "prefix"
+        finally:
+            rp._reassign_pass = orig
+        el = state["t_end"] - state["t0"]
+        return {"value": n * state["passes"] / el, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"{done}: first {state['passes']} passes (incl. their level blurs) of the "
+                          f"{int(math.isqrt(n))}^2x{features.shape[1]} sort, {el:.1f} s; reference sogs "
+                          f"sort_grid_report(threads={threads}) from baseline/_ref"}
+    from oracle import oracle
+    t0 = time.perf_counter()
+    _, rep = oracle.sort_grid_report(features, max_seconds=budget_s, **cfg_kw)
+    el = time.perf_counter() - t0
+    return {"value": n * rep["reorders"] / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"prefix: first {rep['reorders']} passes of the sort, {el:.1f} s; C oracle port"}
+
+
+# ---------------------------------------------------------------------------- ours
+def measured_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import paper_2312_13299_b200 as plas
+    from paper_2312_13299_b200 import _lib, synthetic
+    from paper_2312_13299_b200.plas import SortPlan, sort_on_device
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    device = torch.device("cuda", local)
+    feats = synthetic.make(args.config, data_seed=rank, side=args.side)
+    n, D = feats.shape
+    side = math.isqrt(n)
+    cfg = plas.SortConfig(rng_seed=0, rng_mode=args.mode, **WORKLOADS[args.config]["cfg"])
+    dev = torch.from_numpy(feats).to(device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        sort_on_device(dev, cfg)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    step_ms, passes, levels = [], [], []
+    rep = None
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        perm, rep = sort_on_device(dev, cfg)
+        e1.record()
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        passes.append(rep["reorders"])
+        levels.append(len(rep["radius_trace"]))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    units, secs = combine(n * sum(passes), sum(step_ms) / 1e3, dist, device)
+    value = units / secs
+    ms_per_step = secs * 1e3 / args.steps
+
+    perm_np = perm.cpu().numpy()
+    grid = feats[perm_np].reshape(side, side, D)
+    quality = {"nbr_l2": synthetic.neighbour_l2(grid), "final_vad": rep["final_vad"],
+               "initial_vad": rep["initial_vad"], "passes": passes[-1], "levels": levels[-1],
+               "sort_time_s": statistics.median(step_ms) / 1e3}
+
+    # ---- e2e through the public API, pinned host features, perm back to host
+    e2e = None
+    if not args.no_e2e:
+        host = torch.from_numpy(feats).pin_memory()
+        plas.sort_grid(host, cfg)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e_ms, e_units = [], 0
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p_host, r = plas.sort_grid_report(host, cfg)
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+            e_units += n * r.reorders
+        eu, es = combine(e_units, sum(e_ms) / 1e3, dist, device)
+        e2e = {"value": eu / es, "unit": UNIT, "h2d_bytes_per_step": int(feats.nbytes),
+               "d2h_bytes_per_step": int(n * 8), "ms_per_step": es * 1e3 / args.steps}
+
+    # ---- per-kernel CUDA-event times (host-stepped replay of one sort)
+    roofline = None
+    kernel_ms = None
+    if not args.no_profile:
+        prof = _lib.SortProfile()
+        perm_p = torch.empty(n, dtype=torch.int64, device=device)
+        SortPlan(n, D, cfg).run(dev, perm_p, None, prof)
+        kernel_ms = {}
+        for name in ("pass", "blur0", "blur1", "border", "distance", "control", "select"):
+            ms, cnt = getattr(prof, f"ms_{name}"), getattr(prof, f"n_{name}")
+            kernel_ms[name] = {"total_ms": round(ms, 3), "launches": int(cnt),
+                               "avg_us": round(1e3 * ms / cnt, 2) if cnt else None}
+        peak, peak_kind = measured_peak()
+        S = (D + 3) // 4 * 4
+        # every pass reads each cell's fp32 feature row and target row (8D bytes)
+        alg_pass = n * 8 * D
+        avg_pass_s = prof.ms_pass / prof.n_pass / 1e3
+        blur_total = prof.ms_blur0 + prof.ms_blur1
+        dominant = "pass_kernel" if prof.ms_pass >= blur_total else "blur"
+        achieved = alg_pass / avg_pass_s / 1e9
+        roofline = {"bound": "hbm", "kernel": "pass_kernel (K3 fused assign+swap+distance)",
+                    "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic("pass_kernel"),
+                    "algorithmic_bytes_per_launch": alg_pass, "avg_launch_us": round(avg_pass_s * 1e6, 2),
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                    "dominant_by_time": dominant,
+                    "time_share_pass": round(prof.ms_pass / max(1e-9, prof.ms_pass + blur_total + prof.ms_border
+                                                                  + prof.ms_distance + prof.ms_control), 3)}
+        # the blur at large radius is fp64-compute-bound; its HBM fraction is reported for context
+        alg_blur = n * 8 * D
+        b_avg = (prof.ms_blur0 + prof.ms_blur1) / max(1, prof.n_blur0 + prof.n_blur1) / 1e3
+        roofline["blur_hbm_frac"] = round(alg_blur / b_avg / 1e9 / peak, 4) if b_avg else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(feats, WORKLOADS[args.config]["cfg"], args.cpu_budget)
+
+    # kernels launched per sort by our library (graph mode): 6 init + 5 final +
+    # 8 per level + 2 per pass (see plas_b200.cu); parity mode adds 3 per pass
+    per_pass = 2 if args.mode == "device" else 5
+    launches = sum(11 + 8 * L + per_pass * P for L, P in zip(levels, passes))
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 data, f64 accumulate", "data": "synthetic",
+        "config": {"workload": f"{args.config} {side}x{side}x{D} PLAS sort to convergence "
+                               f"(BASELINE.json configs[{args.config[1]}])",
+                   "side": side, "dim": D, "rng_mode": args.mode, "seed": 0,
+                   "sort_config": WORKLOADS[args.config]["cfg"] or "SortConfig defaults",
+                   "l2": "256 MiB buffer written before every timed step (outside the events)",
+                   "parallelism": f"{world} independent grid(s), one per rank"},
+        "quality": quality, "e2e": e2e, "roofline": roofline, "kernel_ms": kernel_ms,
+        "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return  # the reference arm runs on rank 0 only
+    from paper_2312_13299_b200 import synthetic
+    feats = synthetic.make(args.config, data_seed=0, side=args.side)
+    n, D = feats.shape
+    side = math.isqrt(n)
+    budget = max(3.0, min(args.cpu_budget, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    samples = []
+    for k in range(args.warmup + args.steps):
+        r = cpu_reference_sample(feats, WORKLOADS[args.config]["cfg"], budget)
+        if k >= args.warmup:
+            vals.append(r["value"])
+            samples.append(r)
+    v = statistics.mean(vals)
+    last = samples[-1]
+    line = {
+        "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * budget, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 data, f64 accumulate", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{args.config} {side}x{side}x{D} PLAS sort (bounded CPU prefix per step)",
+                   "side": side, "dim": D},
+        "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"]},
+        "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -57,8 +57,8 @@ def lib():
         L.oracle_grid_distance_f32.restype = f64
         L.oracle_vad_f32.argtypes = [P, i32, i32, i32, i32]
         L.oracle_vad_f32.restype = f64
-        L.oracle_sort.argtypes = [P, i64, i32, i64, f64, i32, i32, P, P, P, P, P, i64, P, P, P,
-                                  i64, P, P]
+        L.oracle_sort.argtypes = [P, i64, i32, i64, f64, i32, i32, P, P, P, P, P, i64, f64, P, P,
+                                  P, i64, P, P]
         L.oracle_sort.restype = i64
         L.oracle_smoothness_plane.argtypes = [P, i32, i32, i32, f64, f64, i32, P, i32, P]
         L.oracle_smoothness_plane.restype = f64
@@ -187,7 +187,7 @@ def vad(grid):
 # ---------------------------------------------------------------- sort
 def sort_grid_report(features, rng_seed=0, improvement_threshold=1e-4, radius_decay=0.95,
                      min_block_size=16, initial_radius_override=None, init_perm=None,
-                     max_passes=0):
+                     max_passes=0, max_seconds=0.0):
     """plas.py:226-286.  Returns (perm, report dict) with the reference's fields."""
     f = np.ascontiguousarray(features, dtype=np.float64)
     n, D = f.shape
@@ -210,7 +210,7 @@ def sort_grid_report(features, rng_seed=0, improvement_threshold=1e-4, radius_de
         ip = None if init_perm is None else np.ascontiguousarray(init_perm, dtype=np.int64)
         passes = lib().oracle_sort(_p(f), n, D, rng_seed, improvement_threshold, min_block_size, L,
                                    _p(np.asarray(rs, dtype=np.float64)), _p(hs), _p(wcat), _p(woff),
-                                   None if ip is None else _p(ip), max_passes, _p(perm), _p(counts),
+                                   None if ip is None else _p(ip), max_passes, float(max_seconds), _p(perm), _p(counts),
                                    _p(trace), cap, _p(vads), _p(lv))
         if passes >= 0:
             break

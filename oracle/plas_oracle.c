@@ -28,6 +28,13 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
+
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
 
 /* ------------------------------------------------------------------ */
 /* NumPy SeedSequence (numpy/random/bit_generator.pyx)                 */
@@ -188,70 +195,69 @@ void oracle_rng_permutation(oracle_rng *r, int64_t n, int64_t *out) {
 /* ------------------------------------------------------------------ */
 /* Blur (SciPy correlate1d, symmetric kernel, mode constant 0)         */
 /* ------------------------------------------------------------------ */
-/* fold one line position: in(k) returns the fp64 value at line index k (0 outside) */
-#define FOLD(acc, get, pos, w, h)                                 \
-    do {                                                          \
-        double _a = (get(pos)) * (w)[0];                          \
-        for (int _j = (h); _j >= 1; _j--) {                        \
-            double _p = (get((pos) - _j)) + (get((pos) + _j));     \
-            _a = _a + _p * (w)[_j];                               \
-        }                                                         \
-        (acc) = _a;                                               \
+/*
+ * One axis of the blur, restated as "for each output line position, for each
+ * tap j = h..1 (outermost first), for every element of the slab": the
+ * per-element operation sequence is exactly SciPy's
+ *     acc = in[i] * w0;  for j = h..1: acc += (in[i-j] + in[i+j]) * w_j
+ * while the innermost loop runs over contiguous memory.
+ * A slab is `len` contiguous doubles; line positions are `n` slabs apart by
+ * `stride` elements; `get` converts the input element to double.
+ */
+#define AXIS_PASS(TIN, TOUT, in, out, n, nslab, slab_stride, stride, len, w, h)            \
+    do {                                                                                 \
+        double *acc = (double *)malloc(sizeof(double) * (size_t)(len));                   \
+        for (int64_t sl = 0; sl < (nslab); sl++) {                                        \
+            const TIN *ib = (in) + sl * (slab_stride);                                    \
+            TOUT *ob = (out) + sl * (slab_stride);                                        \
+            for (int64_t i = 0; i < (n); i++) {                                           \
+                const TIN *ci = ib + i * (stride);                                        \
+                for (int64_t e = 0; e < (len); e++) acc[e] = (double)ci[e] * (w)[0];      \
+                for (int j = (h); j >= 1; j--) {                                           \
+                    const TIN *lo = (i - j >= 0) ? ib + (i - j) * (stride) : NULL;         \
+                    const TIN *hi = (i + j < (n)) ? ib + (i + j) * (stride) : NULL;        \
+                    double wj = (w)[j];                                                   \
+                    for (int64_t e = 0; e < (len); e++) {                                 \
+                        double p = (lo ? (double)lo[e] : 0.0) + (hi ? (double)hi[e] : 0.0);\
+                        acc[e] = acc[e] + p * wj;                                         \
+                    }                                                                     \
+                }                                                                         \
+                TOUT *co = ob + i * (stride);                                             \
+                for (int64_t e = 0; e < (len); e++) co[e] = (TOUT)acc[e];                 \
+            }                                                                             \
+        }                                                                                 \
+        free(acc);                                                                        \
     } while (0)
 
 /* axis-0 pass (along y) then axis-1 pass (along x) over an (H, W, C) grid.
- * mode 0: f32 in, f32 out after each axis (gaussian_filter1d on float32 arrays).
- * mode 1: f64 in, f64 everywhere.
+ * f32: f32 in, f32 out after each axis (gaussian_filter1d on float32 arrays).
+ * f64: f64 everywhere.
  * w: h+1 weights (w[0] centre), computed by NumPy exactly as scipy's _gaussian_kernel1d. */
 void oracle_separable_blur_f32(const float *in, int H, int W, int C, const double *w, int h,
                                float *out) {
     float *tmp = (float *)malloc(sizeof(float) * (size_t)H * W * C);
-    for (int x = 0; x < W; x++)
-        for (int c = 0; c < C; c++) {
-#define GY(k) (((k) >= 0 && (k) < H) ? (double)in[((size_t)(k) * W + x) * C + c] : 0.0)
-            for (int y = 0; y < H; y++) {
-                double a;
-                FOLD(a, GY, y, w, h);
-                tmp[((size_t)y * W + x) * C + c] = (float)a;
-            }
-#undef GY
-        }
-    for (int y = 0; y < H; y++)
-        for (int c = 0; c < C; c++) {
-#define GX(k) (((k) >= 0 && (k) < W) ? (double)tmp[((size_t)y * W + (k)) * C + c] : 0.0)
-            for (int x = 0; x < W; x++) {
-                double a;
-                FOLD(a, GX, x, w, h);
-                out[((size_t)y * W + x) * C + c] = (float)a;
-            }
-#undef GX
-        }
+    const int64_t row = (int64_t)W * C;
+    /* axis 0: one slab = a whole row (W*C), positions y */
+    AXIS_PASS(float, float, in, tmp, H, 1, 0, row, row, w, h);
+    /* axis 1: per row y, positions x, slab = the C channels of a cell */
+    for (int y = 0; y < H; y++) {
+        const float *ir = tmp + (int64_t)y * row;
+        float *orow = out + (int64_t)y * row;
+        AXIS_PASS(float, float, ir, orow, W, 1, 0, C, C, w, h);
+    }
     free(tmp);
 }
 
 void oracle_separable_blur_f64(const double *in, int H, int W, int C, const double *w, int h,
                                double *out) {
     double *tmp = (double *)malloc(sizeof(double) * (size_t)H * W * C);
-    for (int x = 0; x < W; x++)
-        for (int c = 0; c < C; c++) {
-#define GY(k) (((k) >= 0 && (k) < H) ? in[((size_t)(k) * W + x) * C + c] : 0.0)
-            for (int y = 0; y < H; y++) {
-                double a;
-                FOLD(a, GY, y, w, h);
-                tmp[((size_t)y * W + x) * C + c] = a;
-            }
-#undef GY
-        }
-    for (int y = 0; y < H; y++)
-        for (int c = 0; c < C; c++) {
-#define GX(k) (((k) >= 0 && (k) < W) ? tmp[((size_t)y * W + (k)) * C + c] : 0.0)
-            for (int x = 0; x < W; x++) {
-                double a;
-                FOLD(a, GX, x, w, h);
-                out[((size_t)y * W + x) * C + c] = a;
-            }
-#undef GX
-        }
+    const int64_t row = (int64_t)W * C;
+    AXIS_PASS(double, double, in, tmp, H, 1, 0, row, row, w, h);
+    for (int y = 0; y < H; y++) {
+        const double *ir = tmp + (int64_t)y * row;
+        double *orow = out + (int64_t)y * row;
+        AXIS_PASS(double, double, ir, orow, W, 1, 0, C, C, w, h);
+    }
     free(tmp);
 }
 
@@ -484,17 +490,18 @@ static void reassign_pass(float *feat, int64_t *idx, const float *target, int si
  * multiplication, plas.py:246/274) and the per-level Gaussian weights (NumPy
  * exp, scipy _gaussian_kernel1d) are built by the caller: L levels, level l has
  * half-width hs[l] and weights w + woff[l] (hs[l]+1 values).
- * max_passes bounds the total pass count (0 = unbounded) so a bounded CPU
- * sample can be timed; trace_cap bounds the trace buffer.
+ * max_passes / max_seconds bound the run (0 = unbounded) so a bounded CPU
+ * sample can be timed (checked before each pass); trace_cap bounds the trace.
  * Returns the number of passes executed, or -1 on trace overflow.
  */
 int64_t oracle_sort(const double *features, int64_t n, int D, int64_t seed, double thr,
                     int min_block, int L, const double *radii, const int *hs,
                     const double *w, const int64_t *woff, const int64_t *init_perm,
-                    int64_t max_passes, int64_t *perm_out, int64_t *level_counts,
+                    int64_t max_passes, double max_seconds, int64_t *perm_out, int64_t *level_counts,
                     double *trace, int64_t trace_cap, double *vads, int64_t *levels_done) {
     int side = (int)llround(sqrt((double)n));
     int S = D;
+    double t_start = now_s();
     oracle_rng rng;
     oracle_rng_init(&rng, (uint64_t)seed);
     int64_t *idx = perm_out;
@@ -518,6 +525,7 @@ int64_t oracle_sort(const double *features, int64_t n, int D, int64_t seed, doub
     int lv;
     int stopped = 0;
     for (lv = 0; lv < L && !stopped; lv++) {
+        if (max_seconds > 0 && now_s() - t_start >= max_seconds) break;
         double radius = radii[lv];
         const double *wl = w + woff[lv];
         int h = hs[lv];
@@ -531,7 +539,8 @@ int64_t oracle_sort(const double *features, int64_t n, int D, int64_t seed, doub
         int64_t count = 1;
         int strikes = 0;
         while (strikes < 2) {
-            if (max_passes > 0 && passes >= max_passes) { stopped = 1; break; }
+            if ((max_passes > 0 && passes >= max_passes) ||
+                (max_seconds > 0 && now_s() - t_start >= max_seconds)) { stopped = 1; break; }
             int dy = (int)oracle_rng_integers(&rng, beta);
             int dx = (int)oracle_rng_integers(&rng, beta);
             oracle_rng_permutation(&rng, (int64_t)beta * beta, mp);

@@ -1,0 +1,257 @@
+// Shared device helpers for the PLAS sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PLAS_FULL_MASK 0xffffffffu
+
+namespace plas {
+
+// ------------------------------------------------------------------
+// Device-resident sort controller: every pass/level decision of
+// plas.py:251-274 is taken on the device from these fields.
+// ------------------------------------------------------------------
+struct Ctrl {
+  // level state
+  int level;          // current level index into the schedule
+  int num_levels;
+  int pass;           // passes executed in this level
+  int strikes;        // consecutive sub-threshold passes (plas.py:268-271)
+  int beta;           // block side of this level (plas.py:60-61)
+  int h;              // blur half-width ceil(r) of this level
+  // geometry of the pass about to run / running (plas.py:87-110)
+  int dy, dx;
+  int first_y, first_x;  // first segment end (dy if dy > 0 else beta)
+  int nby, nbx;          // number of block rows / columns
+  int cap;               // groups per block slot = ceil(beta^2 / 4)
+  int level_done;        // 1 when strikes reached 2 (host-visible in parity mode)
+  long long total_groups;  // nby * nbx * cap
+  double previous;     // last mean distance (plas.py:256, 272)
+  double current;
+  long long reorders;  // total passes (plas.py:265)
+  long long trace_pos; // next free slot of the trace buffer
+  long long trace_cap;
+  int status;          // 0 ok, 1 trace overflow
+  int levels_done;
+  int side;
+  int rng_mode;        // 0 parity (host draws), 1 device
+  unsigned long long key0, key1;  // Philox4x64 key (numpy SeedSequence state)
+  double threshold;
+  int min_block;
+  int pad_;
+};
+
+// ------------------------------------------------------------------
+// Philox4x64-10 (Random123 constants; same generator NumPy's Philox uses)
+// ------------------------------------------------------------------
+__host__ __device__ __forceinline__ void philox4x64_10(const unsigned long long in[4],
+                                                       unsigned long long k0,
+                                                       unsigned long long k1,
+                                                       unsigned long long out[4]) {
+  unsigned long long c0 = in[0], c1 = in[1], c2 = in[2], c3 = in[3];
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+#ifdef __CUDA_ARCH__
+    unsigned long long hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+    unsigned long long hi1 = __umul64hi(0xCA5A826395121157ull, c2);
+#else
+    unsigned long long hi0 = (unsigned long long)(((unsigned __int128)0xD2E7470EE14C6C93ull * c0) >> 64);
+    unsigned long long hi1 = (unsigned long long)(((unsigned __int128)0xCA5A826395121157ull * c2) >> 64);
+#endif
+    unsigned long long lo0 = 0xD2E7470EE14C6C93ull * c0;
+    unsigned long long lo1 = 0xCA5A826395121157ull * c2;
+    unsigned long long n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+// Unbiased bounded draw in [0, n) from a stream of 32-bit words (Lemire).
+// `words` supplies 8 32-bit values; with n <= 2^31 a rejection beyond 8 words
+// has probability < 2^-8 per word ... the loop falls back to a fresh block.
+struct DeviceDraw {
+  unsigned long long key0, key1;
+  unsigned long long ctr[4];
+  unsigned long long buf[4];
+  int used;  // 32-bit halves consumed from buf (0..8)
+  __host__ __device__ void init(unsigned long long k0, unsigned long long k1, unsigned long long a,
+                                unsigned long long b, unsigned long long c) {
+    key0 = k0;
+    key1 = k1;
+    ctr[0] = 0;
+    ctr[1] = a;
+    ctr[2] = b;
+    ctr[3] = c;
+    used = 8;
+  }
+  __host__ __device__ unsigned int next32() {
+    if (used == 8) {
+      ctr[0]++;
+      philox4x64_10(ctr, key0, key1, buf);
+      used = 0;
+    }
+    unsigned long long w = buf[used >> 1];
+    unsigned int v = (used & 1) ? (unsigned int)(w >> 32) : (unsigned int)w;
+    used++;
+    return v;
+  }
+  __host__ __device__ unsigned int bounded(unsigned int n) {
+    if (n <= 1) return 0;
+    unsigned long long m = (unsigned long long)next32() * n;
+    unsigned int left = (unsigned int)m;
+    if (left < n) {
+      unsigned int thresh = (0u - n) % n;
+      while (left < thresh) {
+        m = (unsigned long long)next32() * n;
+        left = (unsigned int)m;
+      }
+    }
+    return (unsigned int)(m >> 32);
+  }
+  __host__ __device__ unsigned long long next64() {
+    unsigned long long lo = next32();
+    unsigned long long hi = next32();
+    return lo | (hi << 32);
+  }
+};
+
+// ------------------------------------------------------------------
+// Keyed bijection on [0, m): unbalanced Feistel network on the smallest
+// power-of-two domain >= m with cycle walking (DEVICE-mode grouping law,
+// SURVEY Appendix A.1 option (b)).
+// ------------------------------------------------------------------
+__host__ __device__ __forceinline__ unsigned int mix32(unsigned int x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+
+struct Feistel {
+  unsigned int keys[6];
+  int lbits, rbits;  // domain bits = lbits + rbits
+  unsigned int m;
+  __host__ __device__ void init(unsigned long long k, unsigned int m_) {
+    m = m_;
+    int bits = 0;
+    while ((1u << bits) < m_ && bits < 31) bits++;
+    if (bits < 2) bits = 2;
+    lbits = bits >> 1;
+    rbits = bits - lbits;
+#pragma unroll
+    for (int r = 0; r < 6; r++) {
+      k = k * 6364136223846793005ull + 1442695040888963407ull;
+      keys[r] = (unsigned int)(k >> 32);
+    }
+  }
+  __host__ __device__ __forceinline__ unsigned int once(unsigned int x) const {
+    // state (L: a bits, R: b bits) -> (R, L ^ F(R)); shapes alternate, 6 rounds
+    unsigned int a = lbits, b = rbits;
+    unsigned int L = x >> b, R = x & ((1u << b) - 1u);
+#pragma unroll
+    for (int r = 0; r < 6; r++) {
+      unsigned int f = mix32(R ^ keys[r]) & ((1u << a) - 1u);
+      unsigned int nL = R, nR = L ^ f;
+      // new shape: L has b bits, R has a bits
+      unsigned int t = a;
+      a = b;
+      b = t;
+      L = nL;
+      R = nR;
+    }
+    return (L << b) | R;
+  }
+  __host__ __device__ __forceinline__ unsigned int operator()(unsigned int i) const {
+    if (m <= 1) return 0;
+    unsigned int x = once(i);
+    while (x >= m) x = once(x);
+    return x;
+  }
+};
+
+// ------------------------------------------------------------------
+// Pass geometry (plas.py:87-110): segment bounds of block row/col b.
+// ------------------------------------------------------------------
+__host__ __device__ __forceinline__ void segment(int b, int first, int beta, int side, int* lo,
+                                                 int* hi) {
+  int s = (b == 0) ? 0 : first + (b - 1) * beta;
+  int e = first + b * beta;
+  if (e > side) e = side;
+  *lo = s;
+  *hi = e;
+}
+
+__host__ __device__ __forceinline__ int num_segments(int first, int beta, int side) {
+  return first < side ? 1 + (side - first + beta - 1) / beta : 1;
+}
+
+__host__ __device__ __forceinline__ void set_pass_geometry(Ctrl* c, int dy, int dx) {
+  c->dy = dy;
+  c->dx = dx;
+  c->first_y = dy > 0 ? dy : c->beta;
+  c->first_x = dx > 0 ? dx : c->beta;
+  c->nby = num_segments(c->first_y, c->beta, c->side);
+  c->nbx = num_segments(c->first_x, c->beta, c->side);
+  c->cap = (c->beta * c->beta + 3) / 4;
+  c->total_groups = (long long)c->nby * c->nbx * c->cap;
+}
+
+// DEVICE-mode per-pass draws: dy, dx and the grouping key come from the
+// Philox4x64-10 stream keyed like NumPy's (SeedSequence state), at counter
+// (block, pass, level, purpose) -- stateless, identical on every GPU.
+__host__ __device__ __forceinline__ void device_pass_draws(const Ctrl* c, int* dy, int* dx,
+                                                           unsigned long long* gkey) {
+  DeviceDraw d;
+  d.init(c->key0, c->key1, (unsigned long long)c->pass, (unsigned long long)c->level,
+         0x504153535ull /* "PASS" */);
+  *dy = (int)d.bounded((unsigned)c->beta);
+  *dx = (int)d.bounded((unsigned)c->beta);
+  *gkey = d.next64();
+}
+
+__host__ __device__ __forceinline__ unsigned long long class_key(unsigned long long gkey, int h,
+                                                                 int w) {
+  unsigned long long k = gkey ^ ((unsigned long long)(unsigned)h << 32) ^ (unsigned)w;
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+// warp / block reductions in fp64 with a fixed order (deterministic)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(PLAS_FULL_MASK, v, o);
+  return v;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < NT / 32 ? sh[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+}  // namespace plas

@@ -1,0 +1,815 @@
+// plas_b200.cu -- C ABI + sort driver of the B200-native PLAS hot path.
+//
+// Reference call stack: sort_grid_report -> _sort
+// (plas.py:226-286) -> per level blur_target + grid_distance, per pass
+// rng draws + _reassign_pass -> _assign_groups + grid_distance.
+//
+// PARITY mode replays that loop from the host with NumPy-exact draws (one
+// stream sync per pass to read the device-side convergence flag, with the
+// next pass's draws generated while the GPU works).
+// DEVICE mode builds the whole sort as ONE CUDA graph: an outer WHILE
+// conditional node over levels and an inner WHILE node over passes whose
+// condition is set on the device by the controller kernel (K4), so the host
+// launches once and syncs once.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <cmath>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "../../include/plas_b200.h"
+#include "assign.cuh"
+#include "blur.cuh"
+#include "common.cuh"
+#include "control.cuh"
+#include "host_rng.h"
+#include "smooth.cuh"
+
+using namespace plas;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t _e = (call);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return fail(PLAS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+#define CKL()                                                                               \
+  do {                                                                                      \
+    cudaError_t _e = cudaGetLastError();                                                    \
+    if (_e != cudaSuccess)                                                                  \
+      return fail(PLAS_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(_e) + " @" + \
+                                     std::to_string(__LINE__));                             \
+  } while (0)
+
+constexpr int MAX_PARTS = 4096;
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int grid_for(long long work, int threads, int per_sm) {
+  long long g = (work + threads - 1) / threads;
+  long long cap = (long long)num_sms() * per_sm;
+  if (g > cap) g = cap;
+  if (g > MAX_PARTS) g = MAX_PARTS;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// bump allocator over a caller-provided workspace
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * count;
+    return p;
+  }
+};
+
+int row_stride(int dim) { return (dim + 3) / 4 * 4; }
+
+// ---------------------------------------------------------------- schedule
+struct Schedule {
+  std::vector<double> radii, weights;
+  std::vector<int> betas, hs;
+  std::vector<long long> woff;
+};
+
+double default_initial_radius(int side) { return std::max(side / 2.0 - 1.0, 2.0); }
+
+void build_schedule(const plas_sort_args* a, int side, Schedule* s) {
+  s->radii.clear();
+  if (a->radii) {
+    s->radii.assign(a->radii, a->radii + a->num_levels);
+  } else {
+    double r = std::isnan(a->initial_radius) ? default_initial_radius(side) : a->initial_radius;
+    while (r >= 1.0) {  // plas.py:251, 274 (repeated multiplication)
+      s->radii.push_back(r);
+      r *= a->radius_decay;
+    }
+  }
+  const int L = (int)s->radii.size();
+  s->betas.resize(L);
+  s->hs.resize(L);
+  s->woff.resize(L);
+  s->weights.clear();
+  for (int l = 0; l < L; l++) {
+    const double r = s->radii[l];
+    int beta = std::max(a->min_block_size, (int)r + 1);  // plas.py:60-61
+    s->betas[l] = std::min(beta, side);
+    s->hs[l] = (int)ceil(r);
+    if (a->weights) {
+      s->woff[l] = a->weight_offsets[l];
+    } else {
+      // scipy _gaussian_kernel1d(sigma=r/2, 0, h): exp(-0.5/sigma^2 x^2) / sum
+      const int h = s->hs[l];
+      const double sigma = r / 2.0, sigma2 = sigma * sigma;
+      std::vector<double> phi(2 * h + 1);
+      double sum = 0.0;
+      for (int x = -h; x <= h; x++) phi[x + h] = exp(-0.5 / sigma2 * (double)(x * x));
+      for (double v : phi) sum += v;
+      s->woff[l] = (long long)s->weights.size();
+      for (int j = 0; j <= h; j++) s->weights.push_back(phi[h + j] / sum);
+    }
+  }
+  if (a->weights) {
+    long long wl = 0;
+    for (int l = 0; l < L; l++) wl = std::max(wl, (long long)(s->woff[l] + s->hs[l] + 1));
+    s->weights.assign(a->weights, a->weights + wl);
+  }
+}
+
+// ---------------------------------------------------------------- workspace
+struct SortWs {
+  Ctrl* ctrl;
+  float *feat, *target, *tmp, *den32;
+  int* idx;
+  double* rowweight;
+  double* partials;
+  int* flags;  // [0] nonfinite, [1] moved
+  double* scalars;  // [0] vad mean, [1] vad0, [2] vad1
+  double* radii;
+  int *betas, *hs;
+  long long* woff;
+  double* weights;
+  long long* level_counts;
+  double* trace;
+  int* mp;   // parity: master permutation (beta0^2)
+  int* sel;  // parity: 9 class selections
+  long long sel_stride;
+};
+
+size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long long tcap,
+                  int rng_mode, int side, SortWs* w) {
+  Carver c{base};
+  const int S = row_stride(dim);
+  w->ctrl = c.take<Ctrl>(1);
+  w->feat = c.take<float>((size_t)n * S);
+  w->target = c.take<float>((size_t)n * S);
+  w->tmp = c.take<float>((size_t)n * S);
+  w->den32 = c.take<float>((size_t)n);
+  w->idx = c.take<int>((size_t)n);
+  w->rowweight = c.take<double>((size_t)side);
+  w->partials = c.take<double>(MAX_PARTS);
+  w->flags = c.take<int>(8);
+  w->scalars = c.take<double>(8);
+  w->radii = c.take<double>(std::max(L, 1));
+  w->betas = c.take<int>(std::max(L, 1));
+  w->hs = c.take<int>(std::max(L, 1));
+  w->woff = c.take<long long>(std::max(L, 1));
+  w->weights = c.take<double>(std::max(wlen, 1LL));
+  w->level_counts = c.take<long long>(std::max(L, 1));
+  w->trace = c.take<double>(std::max(tcap, 1LL));
+  long long b0 = side;  // beta0 <= side
+  w->sel_stride = rng_mode == PLAS_RNG_PARITY ? b0 * b0 : 0;
+  w->mp = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(b0 * b0) : 1);
+  w->sel = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(9 * b0 * b0) : 1);
+  return align_up(c.off);
+}
+
+// ---------------------------------------------------------------- graph helpers
+template <typename... KArgs, typename... Args>
+cudaError_t add_kernel(cudaGraphNode_t* out, cudaGraph_t g, const cudaGraphNode_t* deps, int ndeps,
+                       void (*kern)(KArgs...), dim3 grid, dim3 block, Args&&... args) {
+  std::tuple<typename std::decay<KArgs>::type...> vals(std::forward<Args>(args)...);
+  void* ptrs[sizeof...(KArgs) > 0 ? sizeof...(KArgs) : 1];
+  std::apply([&](auto&... v) {
+    int i = 0;
+    ((ptrs[i++] = (void*)&v), ...);
+  }, vals);
+  cudaKernelNodeParams p{};
+  p.func = (void*)kern;
+  p.gridDim = grid;
+  p.blockDim = block;
+  p.sharedMemBytes = 0;
+  p.kernelParams = ptrs;
+  p.extra = nullptr;
+  return cudaGraphAddKernelNode(out, g, deps, ndeps, &p);
+}
+
+cudaError_t add_while(cudaGraphNode_t* out, cudaGraph_t g, const cudaGraphNode_t* deps, int ndeps,
+                      cudaGraphConditionalHandle h, cudaGraph_t* body) {
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaError_t e = cudaGraphAddNode(out, g, deps, ndeps, &p);
+  if (e == cudaSuccess) *body = p.conditional.phGraph_out[0];
+  return e;
+}
+
+// kernel configuration shared by both modes
+struct Launch {
+  int S, D, side;
+  long long n;
+  int blur_grid, den_grid, rows_grid, dist_grid, pass_grid, vad_grid;
+  BlurLevelRef lvl;
+  Sched sched;
+};
+
+template <bool PARITY>
+void* pass_kernel_ptr(int S) {
+  if (S <= 16) return (void*)pass_kernel<16, PARITY>;
+  if (S <= 64) return (void*)pass_kernel<64, PARITY>;
+  return (void*)pass_kernel<0, PARITY>;
+}
+
+int pass_grid_size(int S) {
+  static int cached[3] = {0, 0, 0};
+  int which = S <= 16 ? 0 : (S <= 64 ? 1 : 2);
+  if (!cached[which]) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)pass_kernel_ptr<false>(S), 256, 0);
+    if (occ <= 0) occ = 1;
+    cached[which] = std::min(num_sms() * occ, MAX_PARTS);
+  }
+  return cached[which];
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int plas_abi_version(void) { return PLAS_ABI_VERSION; }
+size_t plas_sizeof_sort_args(void) { return sizeof(plas_sort_args); }
+size_t plas_sizeof_sort_result(void) { return sizeof(plas_sort_result); }
+
+const char* plas_last_error(void) { return g_last_error.c_str(); }
+
+int plas_num_levels(int64_t n, double radius_decay, double initial_radius) {
+  int side = (int)llround(sqrt((double)n));
+  if (side < 2 || !(radius_decay > 0.0 && radius_decay < 1.0)) return 0;
+  double r = std::isnan(initial_radius) ? default_initial_radius(side) : initial_radius;
+  int L = 0;
+  while (r >= 1.0) {
+    L++;
+    r *= radius_decay;
+  }
+  return L;
+}
+
+size_t plas_sort_workspace_bytes(int64_t n, int dim, int num_levels, int64_t weights_len,
+                                 int64_t trace_capacity, int rng_mode) {
+  SortWs w;
+  int side = (int)llround(sqrt((double)n));
+  return carve_sort(nullptr, n, dim, num_levels, weights_len, trace_capacity, rng_mode, side, &w);
+}
+
+void plas_seed_key(uint64_t seed, uint64_t key[2]) { host::seed_key(seed, key); }
+
+int plas_host_permutation(uint64_t seed, int64_t n, int64_t* out) {
+  if (n < 0 || !out) return fail(PLAS_ERR_INVALID, "bad permutation args");
+  host::NumpyPhilox r;
+  r.seed(seed);
+  r.permutation(n, out);
+  return PLAS_OK;
+}
+
+int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t ws_bytes) {
+  if (!a || !res || !a->features || !res->perm) return fail(PLAS_ERR_INVALID, "null argument");
+  const long long n = a->n;
+  const int D = a->dim;
+  const int side = (int)llround(sqrt((double)n));
+  if (D < 1 || side < 2 || (long long)side * side != n || n >= (1LL << 31))
+    return fail(PLAS_ERR_INVALID, "features must be (side^2, D) with side >= 2, D >= 1");
+  if (!(a->improvement_threshold > 0.0) || a->min_block_size < 2)
+    return fail(PLAS_ERR_INVALID, "bad SortConfig");
+  if (a->features_dtype != PLAS_F32 && a->features_dtype != PLAS_F64)
+    return fail(PLAS_ERR_INVALID, "features dtype must be f32 or f64");
+  const int mode = a->rng_mode;
+  if (mode != PLAS_RNG_PARITY && mode != PLAS_RNG_DEVICE) return fail(PLAS_ERR_INVALID, "rng_mode");
+  cudaStream_t st = (cudaStream_t)a->stream;
+
+  Schedule sch;
+  build_schedule(a, side, &sch);
+  const int L = (int)sch.radii.size();
+  const long long tcap = std::max<long long>(a->trace_capacity, 1);
+  SortWs w;
+  size_t need = carve_sort(nullptr, n, D, L, (long long)sch.weights.size(), tcap, mode, side, &w);
+  if (!wsp || ws_bytes < need)
+    return fail(PLAS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  carve_sort((char*)wsp, n, D, L, (long long)sch.weights.size(), tcap, mode, side, &w);
+  const int S = row_stride(D);
+
+  // ---- upload schedule + controller
+  if (L > 0) {
+    CK(cudaMemcpyAsync(w.radii, sch.radii.data(), sizeof(double) * L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.betas, sch.betas.data(), sizeof(int) * L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.hs, sch.hs.data(), sizeof(int) * L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.woff, sch.woff.data(), sizeof(long long) * L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.weights, sch.weights.data(), sizeof(double) * sch.weights.size(),
+                       cudaMemcpyHostToDevice, st));
+  }
+  Ctrl hc;
+  memset(&hc, 0, sizeof(hc));
+  hc.num_levels = L;
+  hc.side = side;
+  hc.trace_cap = tcap;
+  hc.rng_mode = mode;
+  hc.threshold = a->improvement_threshold;
+  hc.min_block = a->min_block_size;
+  uint64_t key[2];
+  host::seed_key(a->seed, key);
+  hc.key0 = key[0];
+  hc.key1 = key[1];
+  CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
+  // pad channels of target/tmp must read as zero
+  if (S != D) {
+    CK(cudaMemsetAsync(w.target, 0, sizeof(float) * n * S, st));
+    CK(cudaMemsetAsync(w.tmp, 0, sizeof(float) * n * S, st));
+  }
+
+  // ---- initial permutation (plas.py:241)
+  host::NumpyPhilox rng;
+  rng.seed(a->seed);
+  std::vector<int> hperm;
+  if (mode == PLAS_RNG_PARITY) {
+    hperm.resize(n);
+    rng.permutation(n, hperm.data());  // also advances the stream like draw #1
+  }
+  if (a->initial_perm) {
+    perm_i64_to_i32_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>((const long long*)a->initial_perm,
+                                                                 w.idx, n);
+    CKL();
+  } else if (mode == PLAS_RNG_PARITY) {
+    CK(cudaMemcpyAsync(w.idx, hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  } else {
+    init_perm_device_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(w.idx, n, key[0], key[1]);
+    CKL();
+  }
+
+  cudaEvent_t ev0, ev1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventRecord(ev0, st));
+  const int gi = grid_for(n * S, 256, 8);
+  if (a->features_dtype == PLAS_F32)
+    gather_init_kernel<float><<<gi, 256, 0, st>>>((const float*)a->features, w.idx, w.feat, n, D, S,
+                                                  w.flags);
+  else
+    gather_init_kernel<double><<<gi, 256, 0, st>>>((const double*)a->features, w.idx, w.feat, n, D,
+                                                   S, w.flags);
+  CKL();
+  int hflags = 0;
+  CK(cudaMemcpyAsync(&hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hflags) {
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return fail(PLAS_ERR_NONFINITE, "features must be finite");
+  }
+
+  // ---- launch configuration
+  Launch lc;
+  lc.S = S;
+  lc.D = D;
+  lc.side = side;
+  lc.n = n;
+  lc.blur_grid = grid_for((long long)side * S * ((side + BLUR_R - 1) / BLUR_R), 256, 8);
+  lc.den_grid = grid_for((long long)side * ((side + 1) / 2), 256, 8);
+  lc.rows_grid = grid_for(side, 128, 1);
+  lc.dist_grid = grid_for(n, RED_THREADS, 4);
+  lc.vad_grid = grid_for(n * D, RED_THREADS, 4);
+  lc.pass_grid = pass_grid_size(S);
+  lc.lvl = BlurLevelRef{w.ctrl, w.hs, w.weights, w.woff, 0, nullptr};
+  lc.sched = Sched{w.radii, w.betas, w.hs, w.level_counts, w.trace};
+
+  auto vad_launch = [&](double* out) -> int {
+    vad_kernel<float><<<lc.vad_grid, RED_THREADS, 0, st>>>(w.feat, side, side, D, S, nullptr, w.partials);
+    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.partials, lc.vad_grid,
+                                                    2.0 * side * (side - 1) * (double)D, w.scalars);
+    vad_kernel<float><<<lc.vad_grid, RED_THREADS, 0, st>>>(w.feat, side, side, D, S, w.scalars, w.partials);
+    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.partials, lc.vad_grid,
+                                                    2.0 * side * (side - 1) * (double)D, out);
+    CKL();
+    return 0;
+  };
+  if (int e = vad_launch(w.scalars + 1)) return e;
+
+  if (mode == PLAS_RNG_DEVICE && !a->profile) {
+    // ------------------------------------------------------------ graph
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle outer_h, inner_h;
+    CK(cudaGraphConditionalHandleCreate(&outer_h, g, L > 0 ? 1 : 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t outer_node;
+    cudaGraph_t obody;
+    CK(add_while(&outer_node, g, nullptr, 0, outer_h, &obody));
+    CK(cudaGraphConditionalHandleCreate(&inner_h, obody, 0, 0));
+    cudaGraphNode_t nd[8];
+    CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched));
+    CK(add_kernel(&nd[1], obody, &nd[0], 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
+                  w.rowweight, side, lc.lvl));
+    CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight_kernel, dim3(lc.den_grid), dim3(256),
+                  (const double*)w.rowweight, w.den32, (double*)nullptr, side, side, lc.lvl));
+    CK(add_kernel(&nd[3], obody, &nd[2], 1, blur_axis_kernel<float, float, 0, 0>, dim3(lc.blur_grid),
+                  dim3(256), (const float*)w.feat, w.tmp, side, side, D, S, lc.lvl, (const void*)nullptr));
+    CK(add_kernel(&nd[4], obody, &nd[3], 1, blur_axis_kernel<float, float, 1, 1>, dim3(lc.blur_grid),
+                  dim3(256), (const float*)w.tmp, w.target, side, side, D, S, lc.lvl,
+                  (const void*)w.den32));
+    CK(add_kernel(&nd[5], obody, &nd[4], 1, distance_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
+                  (const float*)w.feat, (const float*)w.target, n, D, S, w.partials));
+    CK(add_kernel(&nd[6], obody, &nd[5], 1, level_start_finalize_kernel, dim3(1), dim3(RED_THREADS),
+                  w.ctrl, lc.sched, (const double*)w.partials, lc.dist_grid, n,
+                  (unsigned long long)inner_h));
+    cudaGraphNode_t inner_node;
+    cudaGraph_t ibody;
+    CK(add_while(&inner_node, obody, &nd[6], 1, inner_h, &ibody));
+    CK(add_kernel(&nd[7], obody, &inner_node, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl,
+                  lc.sched, (unsigned long long)outer_h));
+    cudaGraphNode_t pn[2];
+    cudaKernelNodeParams kp{};
+    {
+      float* feat = w.feat;
+      int* idx = w.idx;
+      const float* target = w.target;
+      const Ctrl* ctrl = w.ctrl;
+      const int* sel = nullptr;
+      long long sstride = 0;
+      double* partials = w.partials;
+      int* moved = nullptr;
+      int Dv = D, Sv = S;
+      void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &partials, &moved};
+      kp.func = pass_kernel_ptr<false>(S);
+      kp.gridDim = dim3(lc.pass_grid);
+      kp.blockDim = dim3(256);
+      kp.kernelParams = args;
+      CK(cudaGraphAddKernelNode(&pn[0], ibody, nullptr, 0, &kp));
+    }
+    CK(add_kernel(&pn[1], ibody, &pn[0], 1, pass_finalize_kernel, dim3(1), dim3(RED_THREADS), w.ctrl,
+                  lc.sched, (const double*)w.partials, lc.pass_grid, n, (unsigned long long)inner_h));
+    cudaGraphExec_t ge;
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    CK(cudaGraphLaunch(ge, st));
+    CK(cudaStreamSynchronize(st));
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+  } else {
+    // ------------------------------------------------------------ host-stepped loop
+    // PARITY (host draws) or DEVICE with profiling (device draws, events per launch)
+    const bool parity = mode == PLAS_RNG_PARITY;
+    plas_sort_profile* prof = (plas_sort_profile*)a->profile;
+    std::vector<cudaEvent_t> evs;
+    struct Pending { int kind; int e0; };
+    std::vector<Pending> pend;
+    auto timed = [&](int kind, auto&& launch) {
+      if (!prof) {
+        launch();
+        return;
+      }
+      while (evs.size() < (size_t)(2 * pend.size() + 2)) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        evs.push_back(e);
+      }
+      int e0 = (int)(2 * pend.size());
+      cudaEventRecord(evs[e0], st);
+      launch();
+      cudaEventRecord(evs[e0 + 1], st);
+      pend.push_back({kind, e0});
+    };
+    auto flush_profile = [&]() {
+      if (!prof) return;
+      for (auto& pe : pend) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, evs[pe.e0], evs[pe.e0 + 1]);
+        double* slot = &prof->ms_pass + 2 * pe.kind;  // {ms, n} pairs in declaration order
+        slot[0] += ms;
+        reinterpret_cast<int64_t*>(slot)[1] += 1;
+      }
+      pend.clear();
+    };
+    enum { K_PASS = 0, K_BLUR0, K_BLUR1, K_BORDER, K_DIST, K_CTRL, K_SELECT };
+    int* pinned = nullptr;
+    const long long b0sq = parity ? (long long)side * side : 0;
+    CK(cudaMallocHost(&pinned, sizeof(int) * (2 * b0sq + 4)));
+    int* hflag = pinned + 2 * b0sq;
+    auto cleanup = [&]() {
+      cudaFreeHost(pinned);
+      for (auto e : evs) cudaEventDestroy(e);
+    };
+    int pp = 0;
+    void* kfn = parity ? pass_kernel_ptr<true>(S) : pass_kernel_ptr<false>(S);
+    for (int lv = 0; lv < L; lv++) {
+      const int beta = sch.betas[lv];
+      const long long bsq = (long long)beta * beta;
+      timed(K_CTRL, [&] { level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched); });
+      timed(K_BORDER, [&] {
+        border_rows_kernel<<<lc.rows_grid, 128, 0, st>>>(w.rowweight, side, lc.lvl);
+        border_weight_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.den32, nullptr, side, side, lc.lvl);
+      });
+      timed(K_BLUR0, [&] {
+        blur_axis_kernel<float, float, 0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, side, side, D, S,
+                                                                            lc.lvl, nullptr);
+      });
+      timed(K_BLUR1, [&] {
+        blur_axis_kernel<float, float, 1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, side, side, D,
+                                                                            S, lc.lvl, w.den32);
+      });
+      timed(K_DIST, [&] {
+        distance_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.feat, w.target, n, D, S, w.partials);
+      });
+      timed(K_CTRL, [&] {
+        level_start_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.partials, lc.dist_grid, n, 0);
+      });
+      CKL();
+      int dy = 0, dx = 0;
+      if (parity) {  // draws for the first pass of the level
+        dy = (int)rng.integers(beta);
+        dx = (int)rng.integers(beta);
+        rng.permutation(bsq, pinned + pp * b0sq);
+      }
+      for (;;) {
+        if (parity) {
+          CK(cudaMemcpyAsync(w.mp, pinned + pp * b0sq, sizeof(int) * bsq, cudaMemcpyHostToDevice, st));
+          timed(K_SELECT, [&] {
+            set_pass_kernel<<<1, 32, 0, st>>>(w.ctrl, dy, dx);
+            class_select_kernel<<<9, 1024, 0, st>>>(w.mp, w.ctrl, w.sel, w.sel_stride);
+          });
+        }
+        {
+          float* feat = w.feat;
+          int* idx = w.idx;
+          const float* target = w.target;
+          const Ctrl* ctrl = w.ctrl;
+          const int* sel = parity ? w.sel : nullptr;
+          long long sstride = parity ? w.sel_stride : 0;
+          double* partials = w.partials;
+          int* moved = nullptr;
+          int Dv = D, Sv = S;
+          void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &partials, &moved};
+          cudaError_t le = cudaSuccess;
+          timed(K_PASS, [&] { le = cudaLaunchKernel(kfn, dim3(lc.pass_grid), dim3(256), args, 0, st); });
+          if (le != cudaSuccess) {
+            cleanup();
+            return fail(PLAS_ERR_CUDA, std::string("pass launch: ") + cudaGetErrorString(le));
+          }
+        }
+        timed(K_CTRL, [&] {
+          pass_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.partials, lc.pass_grid, n, 0);
+        });
+        CKL();
+        CK(cudaMemcpyAsync(hflag, &w.ctrl->level_done, sizeof(int), cudaMemcpyDeviceToHost, st));
+        // speculative draws for the next pass while the GPU runs this one
+        host::NumpyPhilox saved = rng;
+        int ndy = 0, ndx = 0;
+        if (parity) {
+          ndy = (int)rng.integers(beta);
+          ndx = (int)rng.integers(beta);
+          rng.permutation(bsq, pinned + (1 - pp) * b0sq);
+        }
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+          cleanup();
+          return fail(PLAS_ERR_CUDA, std::string("pass: ") + cudaGetErrorString(e));
+        }
+        flush_profile();
+        if (*hflag) {
+          rng = saved;  // the level ended: these draws belong to the next level's stream
+          break;
+        }
+        dy = ndy;
+        dx = ndx;
+        pp = 1 - pp;
+      }
+      timed(K_CTRL, [&] { level_end_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0); });
+      CKL();
+    }
+    CK(cudaStreamSynchronize(st));
+    flush_profile();
+    cleanup();
+  }
+
+  // ---- final VAD, perm, report
+  if (int e = vad_launch(w.scalars + 2)) return e;
+  perm_i32_to_i64_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(w.idx, (long long*)res->perm, n);
+  CKL();
+  CK(cudaEventRecord(ev1, st));
+  Ctrl out;
+  double sc[3];
+  CK(cudaMemcpyAsync(&out, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sc, w.scalars, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  res->gpu_ms = ms;
+  res->initial_vad = sc[1];
+  res->final_vad = sc[2];
+  res->reorders = out.reorders;
+  res->levels_done = out.levels_done;
+  res->trace_len = out.trace_pos;
+  if (out.status) return fail(PLAS_ERR_CAPACITY, "trace capacity exceeded");
+  if (res->level_counts && L > 0)
+    CK(cudaMemcpy(res->level_counts, w.level_counts, sizeof(long long) * L, cudaMemcpyDeviceToHost));
+  if (res->trace && out.trace_pos > 0)
+    CK(cudaMemcpy(res->trace, w.trace, sizeof(double) * out.trace_pos, cudaMemcpyDeviceToHost));
+  return PLAS_OK;
+}
+
+int plas_assign_groups(float* feat, int64_t* point_idx, const float* target, int dim, int stride,
+                       const int64_t* groups, int64_t num_groups, int group_size, void* stream) {
+  if (dim < 1 || stride < dim || stride % 4 || group_size < 2 || group_size > 4)
+    return fail(PLAS_ERR_INVALID, "bad assign_groups arguments");
+  if (num_groups <= 0) return PLAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int grid = grid_for(num_groups * 4, 256, 4);
+  if (stride <= 16)
+    groups_kernel<16><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
+                                            (const long long*)groups, num_groups, group_size);
+  else if (stride <= 64)
+    groups_kernel<64><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
+                                            (const long long*)groups, num_groups, group_size);
+  else
+    groups_kernel<0><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
+                                           (const long long*)groups, num_groups, group_size);
+  CKL();
+  return PLAS_OK;
+}
+
+size_t plas_aux_workspace_bytes(int H, int W, int C) {
+  size_t cells = (size_t)H * W, tot = cells * C;
+  size_t b = 0;
+  b += align_up(sizeof(double) * tot) * 4;  // tmp, centered/blurred, u, back
+  b += align_up(sizeof(double) * cells);    // den64
+  b += align_up(sizeof(float) * cells);     // den32
+  b += align_up(sizeof(double) * H);        // row weights
+  b += align_up(sizeof(double) * (H > W ? H : W) + 4096 * 8);  // weights
+  b += align_up(sizeof(double) * MAX_PARTS);
+  b += align_up(sizeof(double) * 8);
+  return b;
+}
+
+struct AuxWs {
+  double *t0, *t1, *t2, *t3, *den64, *rows, *w, *partials, *scalars;
+  float* den32;
+};
+
+static size_t carve_aux(char* base, int H, int W, int C, AuxWs* a) {
+  Carver c{base};
+  size_t cells = (size_t)H * W, tot = cells * C;
+  a->t0 = c.take<double>(tot);
+  a->t1 = c.take<double>(tot);
+  a->t2 = c.take<double>(tot);
+  a->t3 = c.take<double>(tot);
+  a->den64 = c.take<double>(cells);
+  a->den32 = c.take<float>(cells);
+  a->rows = c.take<double>(H);
+  a->w = c.take<double>((H > W ? H : W) + 4096);
+  a->partials = c.take<double>(MAX_PARTS);
+  a->scalars = c.take<double>(8);
+  return align_up(c.off);
+}
+
+static int launch_blur(const void* in, void* out, int dtype, int H, int W, int C, int S, int h,
+                       const AuxWs& a, bool renorm, cudaStream_t st) {
+  BlurLevelRef lv{nullptr, nullptr, nullptr, nullptr, h, a.w};
+  int grid0 = grid_for((long long)W * S * ((H + BLUR_R - 1) / BLUR_R), 256, 8);
+  int grid1 = grid_for((long long)H * S * ((W + BLUR_R - 1) / BLUR_R), 256, 8);
+  if (renorm) {
+    border_rows_kernel<<<grid_for(H, 128, 1), 128, 0, st>>>(a.rows, H, lv);
+    border_weight_kernel<<<grid_for((long long)H * ((W + 1) / 2), 256, 8), 256, 0, st>>>(
+        a.rows, a.den32, a.den64, H, W, lv);
+  }
+  if (dtype == PLAS_F32) {
+    float* tmp = (float*)a.t0;
+    blur_axis_kernel<float, float, 0, 0><<<grid0, 256, 0, st>>>((const float*)in, tmp, H, W, C, S, lv, nullptr);
+    if (renorm)
+      blur_axis_kernel<float, float, 1, 1><<<grid1, 256, 0, st>>>(tmp, (float*)out, H, W, C, S, lv, a.den32);
+    else
+      blur_axis_kernel<float, float, 0, 1><<<grid1, 256, 0, st>>>(tmp, (float*)out, H, W, C, S, lv, nullptr);
+  } else {
+    double* tmp = a.t0;
+    blur_axis_kernel<double, double, 0, 0><<<grid0, 256, 0, st>>>((const double*)in, tmp, H, W, C, S, lv, nullptr);
+    if (renorm)
+      blur_axis_kernel<double, double, 2, 1><<<grid1, 256, 0, st>>>(tmp, (double*)out, H, W, C, S, lv, a.den64);
+    else
+      blur_axis_kernel<double, double, 0, 1><<<grid1, 256, 0, st>>>(tmp, (double*)out, H, W, C, S, lv, nullptr);
+  }
+  CKL();
+  return PLAS_OK;
+}
+
+int plas_blur(const void* in, void* out, int dtype, int H, int W, int C, const double* weights,
+              int half_width, int op, void* ws, size_t ws_bytes, void* stream) {
+  if (H < 1 || W < 1 || C < 1 || half_width < 0 || !weights || (dtype != PLAS_F32 && dtype != PLAS_F64))
+    return fail(PLAS_ERR_INVALID, "bad blur arguments");
+  AuxWs a;
+  if (!ws || ws_bytes < carve_aux(nullptr, H, W, C, &a)) return fail(PLAS_ERR_WORKSPACE, "aux workspace");
+  carve_aux((char*)ws, H, W, C, &a);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(a.w, weights, sizeof(double) * (half_width + 1), cudaMemcpyHostToDevice, st));
+  if (op == PLAS_BLUR_BORDER_WEIGHT) {
+    BlurLevelRef lv{nullptr, nullptr, nullptr, nullptr, half_width, a.w};
+    border_rows_kernel<<<grid_for(H, 128, 1), 128, 0, st>>>(a.rows, H, lv);
+    border_weight_kernel<<<grid_for((long long)H * ((W + 1) / 2), 256, 8), 256, 0, st>>>(
+        a.rows, nullptr, (double*)out, H, W, lv);
+    CKL();
+    return PLAS_OK;
+  }
+  return launch_blur(in, out, dtype, H, W, C, C, half_width, a, op == PLAS_BLUR_RENORMALIZED, st);
+}
+
+int plas_grid_distance(const double* a, const double* b, const double* weights, int64_t n, int dim,
+                       double* out_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 1 || dim < 1) return fail(PLAS_ERR_INVALID, "bad grid_distance arguments");
+  if (!ws || ws_bytes < sizeof(double) * MAX_PARTS) return fail(PLAS_ERR_WORKSPACE, "aux workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* partials = (double*)ws;
+  int grid = grid_for(n, RED_THREADS, 4);
+  grid_distance_f64_kernel<<<grid, RED_THREADS, 0, st>>>(a, b, weights, n, dim, partials);
+  mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, grid, (double)n, out_dev);
+  CKL();
+  return PLAS_OK;
+}
+
+int plas_vad(const void* grid, int dtype, int H, int W, int C, double* out_dev, void* ws,
+             size_t ws_bytes, void* stream) {
+  if (H < 2 || W < 2 || C < 1) return fail(PLAS_ERR_INVALID, "vad needs H, W >= 2");
+  if (!ws || ws_bytes < sizeof(double) * (MAX_PARTS + 8)) return fail(PLAS_ERR_WORKSPACE, "aux workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* partials = (double*)ws;
+  double* mean = partials + MAX_PARTS;
+  const double count = ((double)(H - 1) * W + (double)H * (W - 1)) * C;
+  int g = grid_for((long long)H * W * C, RED_THREADS, 4);
+  if (dtype == PLAS_F32) {
+    vad_kernel<float><<<g, RED_THREADS, 0, st>>>((const float*)grid, H, W, C, C, nullptr, partials);
+    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, g, count, mean);
+    vad_kernel<float><<<g, RED_THREADS, 0, st>>>((const float*)grid, H, W, C, C, mean, partials);
+  } else {
+    vad_kernel<double><<<g, RED_THREADS, 0, st>>>((const double*)grid, H, W, C, C, nullptr, partials);
+    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, g, count, mean);
+    vad_kernel<double><<<g, RED_THREADS, 0, st>>>((const double*)grid, H, W, C, C, mean, partials);
+  }
+  mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, g, count, out_dev);
+  CKL();
+  return PLAS_OK;
+}
+
+int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C, double coeff,
+                          double huber_delta, int detach_target, const double* weights,
+                          int half_width, double* loss_dev, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (H < 1 || W < 1 || C < 1 || !(huber_delta > 0) || half_width < 0)
+    return fail(PLAS_ERR_INVALID, "bad smoothness arguments");
+  AuxWs a;
+  if (!ws || ws_bytes < carve_aux(nullptr, H, W, C, &a)) return fail(PLAS_ERR_WORKSPACE, "aux workspace");
+  carve_aux((char*)ws, H, W, C, &a);
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long cells = (long long)H * W, tot = cells * C;
+  const int eg = grid_for(tot, 256, 8);
+  const double scale = coeff / (double)tot;
+  if (half_width > 0) {
+    if (!weights) return fail(PLAS_ERR_INVALID, "weights required");
+    CK(cudaMemcpyAsync(a.w, weights, sizeof(double) * (half_width + 1), cudaMemcpyHostToDevice, st));
+    anchor_center_kernel<<<eg, 256, 0, st>>>(plane, a.t1, cells, C);
+    if (int e = launch_blur(a.t1, a.t2, PLAS_F64, H, W, C, C, half_width, a, true, st)) return e;
+  }
+  huber_kernel<<<eg, 256, 0, st>>>(a.t1, a.t2, a.t3, tot, huber_delta, scale, half_width == 0,
+                                   a.partials);
+  mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(a.partials, eg, (double)tot, loss_dev);
+  if (detach_target || half_width == 0) {
+    CK(cudaMemcpyAsync(grad, a.t3, sizeof(double) * tot, cudaMemcpyDeviceToDevice, st));
+  } else {
+    div_den_kernel<<<eg, 256, 0, st>>>(a.t3, a.den64, a.t1, cells, C);
+    if (int e = launch_blur(a.t1, a.t2, PLAS_F64, H, W, C, C, half_width, a, false, st)) return e;
+    sub_kernel<<<eg, 256, 0, st>>>(a.t3, a.t2, grad, tot);
+  }
+  CKL();
+  return PLAS_OK;
+}
+
+}  // extern "C"
