@@ -100,6 +100,8 @@ typedef struct plas_sort_result {
   double* trace;                 /* host [trace_capacity] out: radius_trace distances */
   int64_t trace_len;
   double gpu_ms;                 /* device time from init gather to perm ready */
+  int64_t cells_moved;           /* elements that changed cell, summed over passes */
+  int64_t exact_warps;           /* warps whose decision needed the exact fp64 tier */
 } plas_sort_result;
 
 int plas_abi_version(void);

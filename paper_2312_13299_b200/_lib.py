@@ -51,7 +51,7 @@ class SortResult(ctypes.Structure):
     _fields_ = [
         ("perm", P), ("initial_vad", f64), ("final_vad", f64), ("reorders", i64),
         ("levels_done", i32), ("level_counts", P), ("trace", P), ("trace_len", i64),
-        ("gpu_ms", f64),
+        ("gpu_ms", f64), ("cells_moved", i64), ("exact_warps", i64),
     ]
 
 

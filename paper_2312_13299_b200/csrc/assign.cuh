@@ -1,88 +1,95 @@
 // K3: fused group assignment (plas.py:113-156 _assign_groups, driven by
-// plas.py:196-223 _reassign_pass) + the per-pass distance statistic
-// (plas.py:266 grid_distance) in one kernel.
+// plas.py:196-223 _reassign_pass), one kernel per pass.
 //
-// Four lanes cooperate on one group of k <= 4 cells (8 groups per warp):
-//   lane s loads its own feature row F_s and every target row T_j of the
-//   group (the 4 lanes load the same T_j address, which the LSU merges), and
-//   computes cost[s][j] with the reference's arithmetic:
-//      c = fp32( sqrt_fp64( sum_d fp64( fp32(F_s[d] - T_j[d])^2 ) ) )
-//   sequential in d, no FMA.  The 16 costs are exchanged with shuffles; lane s
-//   evaluates the (k-1)! lexicographic arrangements that start with s
-//   (cost summed in fp64 in slot order, strict '<' keeps the first minimum),
-//   the four lane minima are reduced on (cost, index) so the lexicographically
-//   first strict minimum wins exactly as in the reference.  The element in slot
-//   i then moves to slot P[i]; identity arrangements and fixed points write
-//   nothing (~3.6% of cells move per pass).
-//   Finally each lane adds the fp64 distance of its element to the target of
-//   its new cell, so the pass statistic needs no second sweep over HBM.
+// Four lanes cooperate on one group of k <= 4 cells (8 groups per warp).
+// Lane s of a group loads float4 chunk s (s+4, s+8, ... for rows wider than
+// 16 floats) of all 4 feature rows and all 4 target rows of the group, so one
+// load instruction moves whole 64-byte rows of 8 groups (8 L1 wavefronts
+// instead of 32 for a thread-per-group layout).  The lanes accumulate the
+// partial squared distances of the 16 (element, target) pairs over their
+// chunk, reduce-scatter them (lane s ends with row s of the cost matrix) and
+// exchange the costs with shuffles.
+//
+// Decision = the reference's first strict minimum over the k! lexicographic
+// arrangements of sum_i c[i][p(i)] with
+//     c = fp32( sqrt_f64( sum_d f64( fp32(F_d - T_d)^2 ) ) )
+// (sequential fp64 sums, no FMA), taken in two tiers:
+//   fast:  costs and arrangement sums in fp32 (FFMA partial sums in any order,
+//          sqrt.approx).  Every fast cost is within (D/2 + 7) 2^-24 (relative)
+//          of the reference cost and every fast arrangement sum within
+//          (D/2 + 10) 2^-24 of the reference sum (non-negative terms), so if
+//          the second-best fast sum exceeds the best by more than
+//          2 (D+24) 2^-24 of itself, the reference's strict minimum is the same
+//          arrangement and is unique.
+//   exact: otherwise (near-ties, exact ties, overflow, tiny costs) the warp
+//          recomputes the costs with the reference arithmetic in fp64
+//          (__fsub_rn / __fmul_rn / __dadd_rn / __dsqrt_rn) and applies the
+//          lexicographic first-minimum rule.  Such groups are counted.
+// The element in slot i moves to slot P[i]; identity arrangements and fixed
+// points write nothing (~3.6% of cells move per pass).
+// The destination cells of all moves go to a moved-cell list (per-CTA shared
+// staging, one global reservation per flush); the statistic kernel
+// (control.cuh pass_stats_kernel) then updates the per-cell fp64 distance
+// cache and the running sum for exactly those cells.
 #pragma once
 #include "common.cuh"
 
 namespace plas {
 
-// slot destination of slot s under arrangement p of k elements (k = 2, 3, 4)
-__device__ __forceinline__ int perm_dest(int k, int p, int s) {
-  if (k == 4) {
-    int first = p / 6, local = p % 6;
-    int o0 = first == 0 ? 1 : 0;
-    int o1 = first <= 1 ? 2 : 1;
-    int o2 = first <= 2 ? 3 : 2;
-    // local order: (o0,o1,o2),(o0,o2,o1),(o1,o0,o2),(o1,o2,o0),(o2,o0,o1),(o2,o1,o0)
-    int a = local < 2 ? o0 : (local < 4 ? o1 : o2);
-    int b, c;
-    switch (local) {
-      case 0: b = o1; c = o2; break;
-      case 1: b = o2; c = o1; break;
-      case 2: b = o0; c = o2; break;
-      case 3: b = o2; c = o0; break;
-      case 4: b = o0; c = o1; break;
-      default: b = o1; c = o0; break;
-    }
-    return s == 0 ? first : (s == 1 ? a : (s == 2 ? b : c));
-  } else if (k == 3) {
-    int first = p / 2, local = p % 2;
-    int o0 = first == 0 ? 1 : 0;
-    int o1 = first == 2 ? 1 : 2;
-    int a = local == 0 ? o0 : o1, b = local == 0 ? o1 : o0;
-    return s == 0 ? first : (s == 1 ? a : b);
-  } else if (k == 2) {
-    return s == 0 ? p : 1 - p;
-  }
-  return s;
+__device__ __forceinline__ float4 ld4g(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4v(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, const float4& v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float f4get(const float4& v, int e) {
+  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
-
-// C[i][j] for the group lives in lane (base + i) as c[j]; fetch by (i, j)
-struct CostMat {
-  float v[4][4];
-};
-
+__device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float sel4(const float* r, int i) {
   return i == 0 ? r[0] : (i == 1 ? r[1] : (i == 2 ? r[2] : r[3]));
 }
+template <typename T>
+__device__ __forceinline__ T pick4(const T (&a)[4], int i) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : (i == 2 ? a[2] : a[3]));
+}
 
-// Evaluate the arrangements starting with slot s; return (best cost, best p).
-// All register indices are static (runtime choices go through selects) so the
-// cost matrix never spills to local memory.
-__device__ __forceinline__ void lane_best(const CostMat& C, int k, int s, double* best_cost,
-                                          int* best_p) {
+// destination slot of slot i under lexicographic arrangement p of k elements
+// (itertools.permutations order, plas.py:31-34), packed 2 bits per slot
+__device__ __forceinline__ int perm_dest(int k, int p, int i) {
+  if (k == 4) {
+    const unsigned long long w =
+        p < 8 ? 0xb1e16c9c78d8b4e4ull : (p < 16 ? 0x36c672d22d8d39c9ull : 0x1b4b278763931e4eull);
+    return (int)((w >> (8 * (p & 7) + 2 * i)) & 3ull);
+  }
+  if (k == 3) return (int)((0x61209211824ull >> (8 * p + 2 * i)) & 3ull);
+  if (k == 2) return p == 0 ? i : 1 - i;
+  return i;
+}
+
+struct CostMat {
+  float v[4][4];  // v[i][j] = cost of slot i's element in slot j's target
+};
+
+// Arrangements that start with slot s, lexicographic: k=4 -> (s, a, b, e) over
+// the remaining {o0 < o1 < o2}, p = 6s + l; k=3 -> p = 2s + l; k=2 -> p = s.
+// exact tier: reference arithmetic in fp64 (first strict minimum)
+__device__ __forceinline__ void lane_best_exact(const CostMat& C, int k, int s, double* best_cost,
+                                                int* best_p) {
   double bc = __longlong_as_double(0x7ff0000000000000ll);  // +inf
   int bp = 0x7fffffff;
   if (s < k) {
     const double c0 = (double)sel4(C.v[0], s);
     if (k == 4) {
-      const int o0 = s == 0 ? 1 : 0, o1 = s <= 1 ? 2 : 1, o2 = s <= 2 ? 3 : 2;
+      const int o[3] = {s == 0 ? 1 : 0, s <= 1 ? 2 : 1, s <= 2 ? 3 : 2};
       double x[4][3];
 #pragma unroll
-      for (int i = 1; i < 4; i++) {
-        x[i][0] = (double)sel4(C.v[i], o0);
-        x[i][1] = (double)sel4(C.v[i], o1);
-        x[i][2] = (double)sel4(C.v[i], o2);
-      }
-      // lexicographic arrangements (s, a, b, d) over the remaining {o0 < o1 < o2}
-      const int A[6] = {0, 0, 1, 1, 2, 2};
-      const int B[6] = {1, 2, 0, 2, 0, 1};
-      const int E[6] = {2, 1, 2, 0, 1, 0};
+      for (int i = 1; i < 4; i++)
+#pragma unroll
+        for (int q = 0; q < 3; q++) x[i][q] = (double)sel4(C.v[i], o[q]);
+      const int A[6] = {0, 0, 1, 1, 2, 2}, B[6] = {1, 2, 0, 2, 0, 1}, E[6] = {2, 1, 2, 0, 1, 0};
 #pragma unroll
       for (int l = 0; l < 6; l++) {
         double c = __dadd_rn(0.0, c0);
@@ -115,222 +122,521 @@ __device__ __forceinline__ void lane_best(const CostMat& C, int k, int s, double
   *best_p = bp;
 }
 
-__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ float4 ld4v(const float* p) { return *reinterpret_cast<const float4*>(p); }
-__device__ __forceinline__ float f4get(const float4& v, int e) {
-  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+// fast tier: fp32 sums; this lane's best (b1, p1) and second best b2
+__device__ __forceinline__ void lane_best_fast(const CostMat& C, int k, int s, float* b1, int* p1,
+                                               float* b2) {
+  const float INF = __int_as_float(0x7f800000);
+  float v1 = INF, v2 = INF;
+  int q1 = 0x7fffffff;
+  if (s < k) {
+    const float c0 = sel4(C.v[0], s);
+    if (k == 4) {
+      const int o[3] = {s == 0 ? 1 : 0, s <= 1 ? 2 : 1, s <= 2 ? 3 : 2};
+      float x[4][3];
+#pragma unroll
+      for (int i = 1; i < 4; i++)
+#pragma unroll
+        for (int q = 0; q < 3; q++) x[i][q] = sel4(C.v[i], o[q]);
+      const int A[6] = {0, 0, 1, 1, 2, 2}, B[6] = {1, 2, 0, 2, 0, 1}, E[6] = {2, 1, 2, 0, 1, 0};
+#pragma unroll
+      for (int l = 0; l < 6; l++) {
+        const float c = ((c0 + x[1][A[l]]) + x[2][B[l]]) + x[3][E[l]];
+        if (c < v1) {
+          v2 = v1;
+          v1 = c;
+          q1 = 6 * s + l;
+        } else if (c < v2) {
+          v2 = c;
+        }
+      }
+    } else if (k == 3) {
+      const int o0 = s == 0 ? 1 : 0, o1 = s == 2 ? 1 : 2;
+      const float ca = (c0 + sel4(C.v[1], o0)) + sel4(C.v[2], o1);
+      const float cb = (c0 + sel4(C.v[1], o1)) + sel4(C.v[2], o0);
+      if (cb < ca) {
+        v1 = cb;
+        q1 = 2 * s + 1;
+        v2 = ca;
+      } else {
+        v1 = ca;
+        q1 = 2 * s;
+        v2 = cb;
+      }
+    } else if (k == 2) {
+      v1 = c0 + sel4(C.v[1], 1 - s);
+      q1 = s;
+    }
+  }
+  *b1 = v1;
+  *p1 = q1;
+  *b2 = v2;
 }
 
-// Process one group per 4 lanes.  All 32 lanes of the warp must call this
-// together.  `cell` is this lane's cell (valid when s < k); k may differ
-// between the 8 groups of a warp.  Rows have stride S (multiple of 4).
-// REG: feature/target rows of up to FCAP floats are kept in registers; the
-// generic path (FCAP == 0) streams rows and moves them chunk by chunk.
-// Returns this lane's fp64 distance contribution (0 when !want_dist).
-template <int FCAP, typename IdxT>
-__device__ __forceinline__ double group_assign(float* __restrict__ feat, IdxT* __restrict__ idx,
-                                               const float* __restrict__ target, int D, int S,
-                                               long long cell, int k, bool want_dist,
-                                               int* moved) {
+// Decide one group (all 32 lanes call together; k may differ between the 8
+// groups of a warp).  rowj[j] = row index (cell or staged local index) of slot
+// j, Fb/Tb the row bases.  With WIDE == false (S <= 16) Fc[i] returns chunk s
+// of feature row i for the move.  Returns the arrangement index (0 = identity).
+template <bool WIDE, bool TNC>
+__device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const int (&rowj)[4], int D,
+                                       int S, int k, float4 (&Fc)[4], int* exact) {
   const int lane = threadIdx.x & 31;
   const int s = lane & 3;
   const int gbase = lane & ~3;
-  const bool act = s < k;
   const int nch = S >> 2;
-  long long cj[4];
+  float part[4][4];
 #pragma unroll
-  for (int j = 0; j < 4; j++) cj[j] = __shfl_sync(PLAS_FULL_MASK, cell, gbase + j);
-
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  constexpr int NC = FCAP > 0 ? FCAP / 4 : 1;
-  float4 F[NC];
-  float4 T[FCAP > 0 && FCAP <= 16 ? 4 : 1][FCAP > 0 && FCAP <= 16 ? NC : 1];
-  if (FCAP > 0) {
+  for (int i = 0; i < 4; i++)
 #pragma unroll
-    for (int c = 0; c < NC; c++) {
-      if (c < nch) {
-        F[c] = act ? ld4v(feat + cell * S + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < 4; j++) part[i][j] = 0.f;
+  const int rounds = WIDE ? (nch + 3) >> 2 : 1;
+  for (int r = 0; r < rounds; r++) {
+    const int c = 4 * r + s;
+    const bool valid = c < nch;
+    float4 Tc[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-          float4 t = (act && j < k) ? ld4(target + cj[j] * S + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (FCAP <= 16) T[j][c] = t;
-#pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const int d = 4 * c + e;
-            if (d < D) {
-              float df = __fsub_rn(f4get(F[c], e), f4get(t, e));
-              acc[j] = __dadd_rn(acc[j], (double)__fmul_rn(df, df));
-            }
-          }
-        }
-      }
+    for (int i = 0; i < 4; i++) {
+      const long long off = (long long)rowj[i] * S + 4 * c;
+      Fc[i] = (valid && i < k) ? ld4v(Fb + off) : f4zero();
+      Tc[i] = (valid && i < k) ? (TNC ? ld4g(Tb + off) : ld4v(Tb + off)) : f4zero();
     }
-  } else {
-    for (int c = 0; c < nch; c++) {
-      float4 f = act ? ld4v(feat + cell * S + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        float4 t = (act && j < k) ? ld4(target + cj[j] * S + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = 0; e < 4; e++) {
+      if (4 * c + e < D) {
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const int d = 4 * c + e;
-          if (d < D) {
-            float df = __fsub_rn(f4get(f, e), f4get(t, e));
-            acc[j] = __dadd_rn(acc[j], (double)__fmul_rn(df, df));
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const float df = f4get(Fc[i], e) - f4get(Tc[j], e);
+            part[i][j] = fmaf(df, df, part[i][j]);
           }
-        }
       }
     }
   }
+  // reduce-scatter over the 4 lanes: lane s ends with row i = s
+  const bool hi2 = (s & 2) != 0, hi1 = (s & 1) != 0;
+  float half[2][4];
+#pragma unroll
+  for (int t = 0; t < 2; t++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float send = hi2 ? part[t][j] : part[2 + t][j];
+      const float keep = hi2 ? part[2 + t][j] : part[t][j];
+      half[t][j] = keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 2);
+    }
   float cst[4];
 #pragma unroll
-  for (int j = 0; j < 4; j++) cst[j] = __double2float_rn(__dsqrt_rn(acc[j]));
+  for (int j = 0; j < 4; j++) {
+    const float send = hi1 ? half[0][j] : half[1][j];
+    const float keep = hi1 ? half[1][j] : half[0][j];
+    cst[j] = sqrt_approx(keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 1));
+  }
   CostMat C;
 #pragma unroll
   for (int i = 0; i < 4; i++)
 #pragma unroll
     for (int j = 0; j < 4; j++) C.v[i][j] = __shfl_sync(PLAS_FULL_MASK, cst[j], gbase + i);
-
-  double bc;
+  float b1, b2;
   int bp;
-  lane_best(C, k, s, &bc, &bp);
+  lane_best_fast(C, k, s, &b1, &bp, &b2);
 #pragma unroll
   for (int o = 1; o <= 2; o <<= 1) {
-    double oc = __shfl_xor_sync(PLAS_FULL_MASK, bc, o);
-    int op = __shfl_xor_sync(PLAS_FULL_MASK, bp, o);
-    if (oc < bc || (oc == bc && op < bp)) {
-      bc = oc;
+    const float ob1 = __shfl_xor_sync(PLAS_FULL_MASK, b1, o);
+    const int op = __shfl_xor_sync(PLAS_FULL_MASK, bp, o);
+    const float ob2 = __shfl_xor_sync(PLAS_FULL_MASK, b2, o);
+    const bool take = ob1 < b1 || (ob1 == b1 && op < bp);
+    const float lose = take ? b1 : ob1;  // the loser's best is a candidate for second
+    b2 = fminf(fminf(b2, ob2), lose);
+    if (take) {
+      b1 = ob1;
       bp = op;
     }
   }
-  if (k < 2) bp = 0;
-  const int dst = act ? perm_dest(k, bp, s) : s;
-  const long long cdst = dst == 0 ? cj[0] : (dst == 1 ? cj[1] : (dst == 2 ? cj[2] : cj[3]));
-  const bool move = act && bp != 0 && dst != s;
-  IdxT my_idx = 0;
-  if (move) my_idx = idx[cell];
-  double dist = 0.0;
-  if (FCAP > 0) {
-    __syncwarp();
-    if (move) {
+  const float margin = 2.0f * (float)(D + 24) * 5.9604645e-08f;  // 2 (D+24) 2^-24
+  const bool certain =
+      k < 2 || (b2 < __int_as_float(0x7f800000) && b2 > 1e-30f && (b2 - b1) > margin * b2);
+  if (__any_sync(PLAS_FULL_MASK, !certain)) {
+    // ---- exact tier for the whole warp (same decision wherever the fast one was
+    // certain): lane s recomputes row s with the reference arithmetic
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const long long fo = (long long)pick4(rowj, s) * S;
 #pragma unroll
-      for (int c = 0; c < NC; c++)
-        if (c < nch) *reinterpret_cast<float4*>(feat + cdst * S + 4 * c) = F[c];
-      idx[cdst] = my_idx;
-    }
-    if (want_dist && act) {
+    for (int j = 0; j < 4; j++) {
+      if (s < k && j < k) {
+        const long long to = (long long)rowj[j] * S;
+        for (int c = 0; c < nch; c++) {
+          const float4 f = ld4v(Fb + fo + 4 * c);
+          const float4 t = ld4v(Tb + to + 4 * c);
 #pragma unroll
-      for (int c = 0; c < NC; c++) {
-        if (c < nch) {
-          float4 t;
-          if (FCAP <= 16) {
-            t = dst == 0 ? T[0][c] : (dst == 1 ? T[1][c] : (dst == 2 ? T[2][c] : T[3][c]));
-          } else {
-            t = ld4(target + cdst * S + 4 * c);
-          }
-#pragma unroll
-          for (int e = 0; e < 4; e++) {
+          for (int e = 0; e < 4; e++)
             if (4 * c + e < D) {
-              double df = (double)f4get(F[c], e) - (double)f4get(t, e);
-              dist = fma(df, df, dist);
+              const float df = __fsub_rn(f4get(f, e), f4get(t, e));
+              acc[j] = __dadd_rn(acc[j], (double)__fmul_rn(df, df));
             }
-          }
         }
       }
-      dist = sqrt(dist);
+      cst[j] = __double2float_rn(__dsqrt_rn(acc[j]));
     }
-  } else {
-    // generic rows: read chunk c of every slot, then write it to the
-    // destination; reads of a chunk complete warp-wide before its writes.
-    for (int c = 0; c < nch; c++) {
-      float4 f = act ? ld4v(feat + cell * S + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncwarp();
-      if (move) *reinterpret_cast<float4*>(feat + cdst * S + 4 * c) = f;
-      __syncwarp();
-      if (want_dist && act) {
-        float4 t = ld4(target + cdst * S + 4 * c);
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          if (4 * c + e < D) {
-            double df = (double)f4get(f, e) - (double)f4get(t, e);
-            dist = fma(df, df, dist);
-          }
-        }
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) C.v[i][j] = __shfl_sync(PLAS_FULL_MASK, cst[j], gbase + i);
+    double bc;
+    lane_best_exact(C, k, s, &bc, &bp);
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const double oc = __shfl_xor_sync(PLAS_FULL_MASK, bc, o);
+      const int op = __shfl_xor_sync(PLAS_FULL_MASK, bp, o);
+      if (oc < bc || (oc == bc && op < bp)) {
+        bc = oc;
+        bp = op;
       }
     }
-    if (move) idx[cdst] = my_idx;
-    if (want_dist && act) dist = sqrt(dist);
+    if (s == 0 && k >= 2 && !certain) *exact += 1;
   }
-  if (move) *moved += 1;
-  return dist;
+  return k < 2 ? 0 : bp;
 }
 
-// Per-pass kernel: group g of the pass -> (block, quad) -> 4 cells.
+// Local index l of the block's grouping for slot s of quad q (plas.py:209):
+// PARITY: the filtered master permutation; DEVICE: the keyed bijection.
+template <bool PARITY>
+__device__ __forceinline__ unsigned group_local(const int* __restrict__ sel, long long sel_stride, int cls,
+                                                const unsigned (&keys)[6], int lb, int rb, unsigned m,
+                                                unsigned q, int s) {
+  if (PARITY) return (unsigned)__ldg(sel + (long long)cls * sel_stride + 4 * q + s);
+  Feistel fe;
+  fe.init_keys(keys, lb, rb, m);
+  return fe(4 * q + s);
+}
+
+// l -> (ly, lx) = (l / ww, l % ww) with a float reciprocal (l < 2^24) and a +-1 fix
+__device__ __forceinline__ void split_local(unsigned l, int ww, float rw, int* ly, int* lx) {
+  int y = (int)__float2uint_rz(__fmul_rn((float)l, rw));
+  int x = (int)l - y * ww;
+  if (x < 0) {
+    y--;
+    x += ww;
+  } else if (x >= ww) {
+    y++;
+    x -= ww;
+  }
+  *ly = y;
+  *lx = x;
+}
+
+// Moved-cell list: CTAs stage the destination cells of their moves in shared
+// memory and append them to list[] with one reservation on *count per flush.
+struct MoveOut {
+  int* list;
+  int* count;
+};
+
+constexpr int LIST_CAP = 4096;  // shared staging entries per CTA
+
+// append this lane's moved cell (if mv) to the CTA staging list
+__device__ __forceinline__ void stage_move(bool mv, int cell, int* s_list, int* s_cnt) {
+  const unsigned bal = __ballot_sync(PLAS_FULL_MASK, mv);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(bal) - 1) base = atomicAdd(s_cnt, __popc(bal));
+  base = __shfl_sync(PLAS_FULL_MASK, base, __ffs(bal) - 1);
+  if (mv) s_list[base + __popc(bal & ((1u << lane) - 1u))] = cell;
+}
+
+// CTA-wide: copy the staged list to the global list (one reservation)
+__device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int* s_cnt, int* s_base) {
+  __syncthreads();
+  const int n = *s_cnt;
+  if (n) {
+    if (threadIdx.x == 0) *s_base = atomicAdd(mo.count, n);
+    __syncthreads();
+    const int b = *s_base;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) mo.list[b + i] = s_list[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *s_cnt = 0;
+  __syncthreads();
+}
+
+// per-pass class tables in shared memory
+struct PassShared {
+  unsigned keys[9][6];
+  int bits[9][2];
+  int seg[6];
+  int cnt;
+  int base;
+};
+
+__device__ __forceinline__ void load_pass_shared(PassShared& ps, const Ctrl* __restrict__ ctrl) {
+  for (int t = threadIdx.x; t < 54; t += blockDim.x) ps.keys[t / 6][t % 6] = ctrl->fe_keys[t / 6][t % 6];
+  if (threadIdx.x < 9) {
+    ps.bits[threadIdx.x][0] = ctrl->fe_lbits[threadIdx.x];
+    ps.bits[threadIdx.x][1] = ctrl->fe_rbits[threadIdx.x];
+  }
+  if (threadIdx.x < 3) {
+    ps.seg[threadIdx.x] = ctrl->seg_h[threadIdx.x];
+    ps.seg[3 + threadIdx.x] = ctrl->seg_w[threadIdx.x];
+  }
+  if (threadIdx.x == 0) ps.cnt = 0;
+  __syncthreads();
+}
+
+// Per-pass kernel (gather regime): CTA iteration = 64 consecutive groups of
+// the pass (8 warps x 8 groups); group g -> (block, quad) -> 4 cells.
 // PARITY: the class grouping is the filtered master permutation
 //   sel[cls][...] (plas.py:209, built by class_select_kernel).
-// DEVICE: the class grouping is a keyed bijection on [0, m).
-template <int FCAP, bool PARITY>
-__global__ void __launch_bounds__(256) pass_kernel(float* __restrict__ feat, int* __restrict__ idx,
-                                                    const float* __restrict__ target, int D, int S,
-                                                    const Ctrl* __restrict__ ctrl,
-                                                    const int* __restrict__ sel, long long sel_stride,
-                                                    double* __restrict__ partials,
-                                                    int* __restrict__ moved_out) {
-  __shared__ double sh[32];
+// DEVICE: the class grouping is a keyed bijection on [0, m) (Ctrl.fe_*).
+template <bool WIDE, bool PARITY>
+__global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, int* __restrict__ idx,
+                                                       const float* __restrict__ target, int D, int S,
+                                                       const Ctrl* __restrict__ ctrl,
+                                                       const int* __restrict__ sel, long long sel_stride,
+                                                       MoveOut mo, int* __restrict__ counters) {
+  __shared__ PassShared ps;
+  __shared__ int s_list[LIST_CAP];
+  load_pass_shared(ps, ctrl);
   const int side = ctrl->side;
   const int beta = ctrl->beta;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
-  const long long cap = ctrl->cap;
-  const long long total = ctrl->total_groups;
-  unsigned long long gkey = 0;
-  if (!PARITY) {
-    int ddy, ddx;
-    device_pass_draws(ctrl, &ddy, &ddx, &gkey);
-  }
-  const int lane = threadIdx.x & 31;
-  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  double dsum = 0.0;
-  int moved = 0;
-  for (long long gb = warp * 8; gb < total; gb += nwarps * 8) {
-    const long long g = gb + (lane >> 2);
-    const int s = lane & 3;
-    int k = 0;
-    long long cell = 0;
+  const unsigned cap = (unsigned)ctrl->cap;
+  const unsigned total = (unsigned)ctrl->total_groups;
+  const unsigned cap_m = ctrl->cap_m, nbx_m = ctrl->nbx_m;
+  const int cap_l = ctrl->cap_l, nbx_l = ctrl->nbx_l;
+  const int nch = S >> 2;
+  const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
+  int exact = 0;
+  for (unsigned base = blockIdx.x * 64u; base < total; base += gridDim.x * 64u) {
+    const unsigned g = base + gl;
+    int k = 0, cell = 0;
     if (g < total) {
-      const long long b = g / cap;
-      const long long q = g - b * cap;
-      const int by = (int)(b / nbx), bx = (int)(b - (long long)by * nbx);
-      int y0, y1, x0, x1;
-      segment(by, fy, beta, side, &y0, &y1);
-      segment(bx, fx, beta, side, &x0, &x1);
-      const int hh = y1 - y0, ww = x1 - x0;
-      const long long m = (long long)hh * ww;
-      const long long rem = m - 4 * q;
-      k = rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0);
-      if (s < k) {
-        long long l;
-        if (PARITY) {
-          const int ty = by == 0 ? 0 : (by == nby - 1 ? 2 : 1);
-          const int tx = bx == 0 ? 0 : (bx == nbx - 1 ? 2 : 1);
-          l = sel[(long long)(ty * 3 + tx) * sel_stride + 4 * q + s];
-        } else {
-          Feistel fe;
-          fe.init(class_key(gkey, hh, ww), (unsigned)m);
-          l = fe((unsigned)(4 * q + s));
+      const unsigned b = fastdiv(g, cap_m, cap_l);
+      const unsigned q = g - b * cap;
+      const unsigned by = fastdiv(b, nbx_m, nbx_l);
+      const unsigned bx = b - by * (unsigned)nbx;
+      const int ty = by == 0 ? 0 : (by == (unsigned)nby - 1 ? 2 : 1);
+      const int tx = bx == 0 ? 0 : (bx == (unsigned)nbx - 1 ? 2 : 1);
+      const int hh = ps.seg[ty], ww = ps.seg[3 + tx];
+      const unsigned m = (unsigned)(hh * ww);
+      const int rem = (int)m - 4 * (int)q;
+      if (rem >= 2) {  // a single leftover cell never moves
+        k = rem >= 4 ? 4 : rem;
+        if (s < k) {
+          const int cls = ty * 3 + tx;
+          const unsigned l = group_local<PARITY>(sel, sel_stride, cls, ps.keys[cls], ps.bits[cls][0],
+                                                 ps.bits[cls][1], m, q, s);
+          int ly, lx;
+          split_local(l, ww, __frcp_rn((float)ww), &ly, &lx);
+          const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
+          const int x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
+          cell = (y0 + ly) * side + x0 + lx;
         }
-        cell = (long long)(y0 + l / ww) * side + x0 + l % ww;
       }
     }
-    dsum += group_assign<FCAP, int>(feat, idx, target, D, S, cell, k, true, &moved);
+    int rowj[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+    float4 Fc[4];
+    const int bp = decide4<WIDE, true>(feat, target, rowj, D, S, k, Fc, &exact);
+    int dst[4];
+    bool mv[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      dst[i] = i < k ? perm_dest(k, bp, i) : i;
+      mv[i] = bp != 0 && i < k && dst[i] != i;
+    }
+    const bool my_mv = pick4(mv, s);
+    const int my_idx = my_mv ? idx[cell] : 0;
+    __syncwarp();
+    if (!WIDE) {
+      if (s < nch) {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (mv[i]) st4(feat + (long long)pick4(rowj, dst[i]) * S + 4 * s, Fc[i]);
+      }
+    } else {
+      // chunk columns: every read of a column precedes its writes
+      for (int r = 0; r < (nch + 3) >> 2; r++) {
+        const int c = 4 * r + s;
+        float4 f[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) f[i] = (mv[i] && c < nch) ? ld4v(feat + (long long)rowj[i] * S + 4 * c) : f4zero();
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (mv[i] && c < nch) st4(feat + (long long)pick4(rowj, dst[i]) * S + 4 * c, f[i]);
+        __syncwarp();
+      }
+    }
+    const int dcell = pick4(rowj, pick4(dst, s));
+    if (my_mv) idx[dcell] = my_idx;
+    stage_move(my_mv, dcell, s_list, &ps.cnt);
+    __syncthreads();
+    if (ps.cnt > LIST_CAP - 256) flush_moves(mo, s_list, &ps.cnt, &ps.base);
   }
-  double tot = block_sum<256>(dsum, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
-  if (moved_out) {
-    int mv = __reduce_add_sync(PLAS_FULL_MASK, moved);
-    if (lane == 0 && mv) atomicAdd(moved_out, mv);
+  flush_moves(mo, s_list, &ps.cnt, &ps.base);
+  const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
+  if (lane == 0 && ex) atomicAdd(counters + 1, ex);
+}
+
+// Tile-regime pass kernel (small blocks).  A CTA walks blocks b = blockIdx.x,
+// +gridDim.x, ... with a two-stage cp.async pipeline: while the groups of
+// block b are decided from shared memory, the feature rows, target rows and
+// indices of the next block are being copied in (every block row is
+// contiguous in HBM, so the copies are coalesced 16-byte transfers).  Only
+// moved rows are written back, from the staged copy, so in-place swaps need
+// no ordering.  Same decisions as pass_kernel.
+constexpr int TILE_THREADS = 256;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// bytes of one pipeline stage for blocks of up to bmax x bmax cells
+__host__ __device__ __forceinline__ long long tile_stage_bytes(int bmax, int S) {
+  const long long m = (long long)bmax * bmax;
+  return (2 * m * S * 4 + m * 4 + 15) / 16 * 16;  // F rows, T rows, idx
+}
+
+struct TileGeom {
+  int y0, x0, hh, ww, cls;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(int b, int nbx, int nby, int fy, int fx, int beta,
+                                              const int* seg) {
+  TileGeom g;
+  const int by = b / nbx, bx = b - by * nbx;
+  const int ty = by == 0 ? 0 : (by == nby - 1 ? 2 : 1);
+  const int tx = bx == 0 ? 0 : (bx == nbx - 1 ? 2 : 1);
+  g.hh = seg[ty];
+  g.ww = seg[3 + tx];
+  g.y0 = by == 0 ? 0 : fy + (by - 1) * beta;
+  g.x0 = bx == 0 ? 0 : fx + (bx - 1) * beta;
+  g.cls = ty * 3 + tx;
+  return g;
+}
+
+template <bool WIDE, bool PARITY>
+__global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
+    float* __restrict__ feat, int* __restrict__ idx, const float* __restrict__ target, int D, int S,
+    const Ctrl* __restrict__ ctrl, const int* __restrict__ sel, long long sel_stride, MoveOut mo,
+    int* __restrict__ counters) {
+  extern __shared__ float4 smem4[];
+  __shared__ PassShared ps;
+  __shared__ int s_list[LIST_CAP];
+  load_pass_shared(ps, ctrl);
+  const int side = ctrl->side;
+  const int beta = ctrl->beta;
+  const int fy = ctrl->first_y, fx = ctrl->first_x;
+  const int nby = ctrl->nby, nbx = ctrl->nbx;
+  const int nblocks = nby * nbx;
+  const int nch = S >> 2;
+  const long long mmax = (long long)beta * beta;
+  const size_t stage_floats = (size_t)(tile_stage_bytes(beta, S) / 4);
+  float* stage_base = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
+
+  // issue the copies of block b into stage st
+  auto prefetch = [&](int b, int st) {
+    if (b < nblocks) {
+      const TileGeom g = tile_geom(b, nbx, nby, fy, fx, beta, ps.seg);
+      float* sF = stage_base + st * stage_floats;
+      float* sT = sF + mmax * S;
+      int* sI = reinterpret_cast<int*>(sT + mmax * S);
+      const int row4 = g.ww * nch;
+      for (int e = threadIdx.x; e < g.hh * row4; e += blockDim.x) {
+        const int r = e / row4, c = e - r * row4;
+        const long long go = ((long long)(g.y0 + r) * side + g.x0) * S + 4 * c;
+        cp_async16(sF + 4 * e, feat + go);
+        cp_async16(sT + 4 * e, target + go);
+      }
+      for (int e = threadIdx.x; e < g.hh * g.ww; e += blockDim.x) {
+        const int r = e / g.ww, c = e - r * g.ww;
+        cp_async4(sI + e, idx + (long long)(g.y0 + r) * side + g.x0 + c);
+      }
+    }
+    cp_async_commit();
+  };
+
+  int exact = 0;
+  int b = blockIdx.x, st = 0;
+  prefetch(b, 0);
+  for (; b < nblocks; b += gridDim.x, st ^= 1) {
+    prefetch(b + gridDim.x, st ^ 1);
+    cp_async_wait<1>();  // block b's stage has landed
+    __syncthreads();
+    const TileGeom g = tile_geom(b, nbx, nby, fy, fx, beta, ps.seg);
+    const float* sF = stage_base + st * stage_floats;
+    const float* sT = sF + mmax * S;
+    const int* sI = reinterpret_cast<const int*>(sT + mmax * S);
+    const int m = g.hh * g.ww;
+    const int ngroups = (m + 3) >> 2;
+    const float rw = __frcp_rn((float)g.ww);
+    for (int q0 = 0; q0 < ngroups; q0 += TILE_THREADS / 4) {
+      const int q = q0 + gl;
+      int k = 0, l = 0;
+      if (q < ngroups) {
+        const int rem = m - 4 * q;
+        if (rem >= 2) k = rem >= 4 ? 4 : rem;
+        if (s < k)
+          l = (int)group_local<PARITY>(sel, sel_stride, g.cls, ps.keys[g.cls], ps.bits[g.cls][0],
+                                       ps.bits[g.cls][1], (unsigned)m, (unsigned)q, s);
+      }
+      int rowj[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, l, (lane & ~3) + j);
+      float4 Fc[4];
+      const int bp = decide4<WIDE, false>(sF, sT, rowj, D, S, k, Fc, &exact);
+      int dst[4];
+      bool mv[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        dst[i] = i < k ? perm_dest(k, bp, i) : i;
+        mv[i] = bp != 0 && i < k && dst[i] != i;
+      }
+      long long gcell[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        int ly, lx;
+        split_local((unsigned)rowj[j], g.ww, rw, &ly, &lx);
+        gcell[j] = (long long)(g.y0 + ly) * side + g.x0 + lx;
+      }
+      if (!WIDE) {
+        if (s < nch) {
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+            if (mv[i]) st4(feat + pick4(gcell, dst[i]) * S + 4 * s, Fc[i]);
+        }
+      } else {
+        for (int c = s; c < nch; c += 4) {
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+            if (mv[i]) st4(feat + pick4(gcell, dst[i]) * S + 4 * c, ld4v(sF + (long long)rowj[i] * S + 4 * c));
+        }
+      }
+      const bool my_mv = pick4(mv, s);
+      const long long dcell = pick4(gcell, pick4(dst, s));
+      if (my_mv) idx[dcell] = sI[pick4(rowj, s)];
+      stage_move(my_mv, (int)dcell, s_list, &ps.cnt);
+      __syncthreads();
+      if (ps.cnt > LIST_CAP - TILE_THREADS) flush_moves(mo, s_list, &ps.cnt, &ps.base);
+    }
+    __syncthreads();  // stage st is refilled by the prefetch two iterations on
   }
+  cp_async_wait<0>();
+  flush_moves(mo, s_list, &ps.cnt, &ps.base);
+  const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
+  if (lane == 0 && ex) atomicAdd(counters + 1, ex);
 }
 
 // Parity mode: per class (ty, tx) the stable filter master_perm[master_perm < m]
@@ -342,15 +648,12 @@ __global__ void __launch_bounds__(1024) class_select_kernel(const int* __restric
   __shared__ int counts[1024];
   const int cls = blockIdx.x;
   const int ty = cls / 3, tx = cls % 3;
-  const int side = ctrl->side, beta = ctrl->beta;
+  const int beta = ctrl->beta;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
   // class exists?  type 0 = first segment, 2 = last (needs >= 2 segments), 1 = interior (>= 3)
   auto exists = [](int t, int n) { return t == 0 || (t == 2 && n >= 2) || (t == 1 && n >= 3); };
   if (!exists(ty, nby) || !exists(tx, nbx)) return;
-  int y0, y1, x0, x1;
-  segment(ty == 0 ? 0 : (ty == 2 ? nby - 1 : 1), ctrl->first_y, beta, side, &y0, &y1);
-  segment(tx == 0 ? 0 : (tx == 2 ? nbx - 1 : 1), ctrl->first_x, beta, side, &x0, &x1);
-  const long long m = (long long)(y1 - y0) * (x1 - x0);
+  const long long m = (long long)ctrl->seg_h[ty] * ctrl->seg_w[tx];
   const long long n = (long long)beta * beta;
   const long long per = (n + blockDim.x - 1) / blockDim.x;
   const long long s0 = threadIdx.x * per, s1 = min(n, s0 + per);
@@ -358,7 +661,7 @@ __global__ void __launch_bounds__(1024) class_select_kernel(const int* __restric
   for (long long i = s0; i < s1; i++) cnt += mp[i] < m;
   counts[threadIdx.x] = cnt;
   __syncthreads();
-  // exclusive scan (Hillis-Steele on 1024 entries)
+  // inclusive scan (Hillis-Steele on 1024 entries)
   for (int off = 1; off < 1024; off <<= 1) {
     int v = threadIdx.x >= off ? counts[threadIdx.x - off] : 0;
     __syncthreads();
@@ -373,23 +676,49 @@ __global__ void __launch_bounds__(1024) class_select_kernel(const int* __restric
   }
 }
 
+
 // ABI kernel for _assign_groups on an explicit (G, k) group list (plas.py:113-156).
-template <int FCAP>
+template <bool WIDE>
 __global__ void __launch_bounds__(256) groups_kernel(float* __restrict__ feat,
                                                      long long* __restrict__ idx,
                                                      const float* __restrict__ target, int D, int S,
                                                      const long long* __restrict__ groups,
-                                                     long long G, int k) {
-  const int lane = threadIdx.x & 31;
-  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  int moved = 0;
-  for (long long gb = warp * 8; gb < G; gb += nwarps * 8) {
-    const long long g = gb + (lane >> 2);
-    const int s = lane & 3;
-    const int kk = g < G ? k : 0;
-    const long long cell = (s < kk) ? groups[g * k + s] : 0;
-    group_assign<FCAP, long long>(feat, idx, target, D, S, cell, kk, false, &moved);
+                                                     long long G, int kk) {
+  const int lane = threadIdx.x & 31, s = lane & 3;
+  const int nch = S >> 2;
+  int exact = 0;
+  const long long wstride = ((long long)gridDim.x * blockDim.x) >> 2;  // groups per grid iteration
+  for (long long base = ((long long)blockIdx.x * blockDim.x) >> 2; base < G; base += wstride) {
+    const long long g = base + (threadIdx.x >> 2);
+    const int k = g < G ? kk : 0;
+    const int cell = s < k ? (int)groups[g * kk + s] : 0;
+    int rowj[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+    float4 Fc[4];
+    const int bp = decide4<WIDE, true>(feat, target, rowj, D, S, k, Fc, &exact);
+    int dst[4];
+    bool mv[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      dst[i] = i < k ? perm_dest(k, bp, i) : i;
+      mv[i] = bp != 0 && i < k && dst[i] != i;
+    }
+    const bool my_mv = pick4(mv, s);
+    const long long my_idx = my_mv ? idx[cell] : 0;
+    __syncwarp();
+    for (int r = 0; r < (nch + 3) >> 2; r++) {
+      const int c = 4 * r + s;
+      float4 f[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) f[i] = (mv[i] && c < nch) ? ld4v(feat + (long long)rowj[i] * S + 4 * c) : f4zero();
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if (mv[i] && c < nch) st4(feat + (long long)pick4(rowj, dst[i]) * S + 4 * c, f[i]);
+      __syncwarp();
+    }
+    if (my_mv) idx[pick4(rowj, pick4(dst, s))] = my_idx;
   }
 }
 

@@ -39,7 +39,45 @@ struct Ctrl {
   double threshold;
   int min_block;
   int pad_;
+  // derived per-pass geometry (set_pass_geometry)
+  int seg_h[3], seg_w[3];          // first / interior / last segment extents
+  unsigned cap_m, nbx_m;           // fast-division magics for cap and nbx
+  int cap_l, nbx_l;
+  unsigned fe_keys[9][6];          // DEVICE mode: Feistel round keys per block class
+  int fe_lbits[9], fe_rbits[9];
+  // running sum of per-cell distances (level-start sum + exact per-pass deltas)
+  double dist_sum;
+  long long fallbacks;             // warps that took the exact fp64 decision path
+  int S;                           // row stride (floats)
+  int tile;                        // this pass runs the shared-memory tile kernel
 };
+
+// Blocks whose feature + target rows fit in TILE_SMEM_MAX bytes of shared
+// memory are processed by the tile kernel (coalesced staging), larger blocks
+// by the gather kernel.
+constexpr int TILE_ROWS_MAX = 32 * 1024;  // F + T rows of one block
+__host__ __device__ __forceinline__ bool use_tile(int beta, int S) {
+  return 2ll * beta * beta * S * 4 <= TILE_ROWS_MAX;
+}
+
+// ------------------------------------------------------------------
+// Division by a runtime-invariant 32-bit divisor (round-up method):
+// q = (umulhi(n, m) + n) >> l with l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1.
+// ------------------------------------------------------------------
+__host__ __device__ __forceinline__ void make_fastdiv(unsigned d, unsigned* m, int* l) {
+  int s = 0;
+  while ((1ull << s) < d) s++;
+  *l = s;
+  *m = (unsigned)((((1ull << 32) * ((1ull << s) - d)) / d) + 1ull);
+}
+__host__ __device__ __forceinline__ unsigned fastdiv(unsigned n, unsigned m, int l) {
+#ifdef __CUDA_ARCH__
+  unsigned hi = __umulhi(n, m);
+#else
+  unsigned hi = (unsigned)(((unsigned long long)n * m) >> 32);
+#endif
+  return (unsigned)(((unsigned long long)hi + n) >> l);
+}
 
 // ------------------------------------------------------------------
 // Philox4x64-10 (Random123 constants; same generator NumPy's Philox uses)
@@ -156,12 +194,20 @@ struct Feistel {
       keys[r] = (unsigned int)(k >> 32);
     }
   }
+  __host__ __device__ void init_keys(const unsigned* k, int lb, int rb, unsigned m_) {
+#pragma unroll
+    for (int r = 0; r < 6; r++) keys[r] = k[r];
+    lbits = lb;
+    rbits = rb;
+    m = m_;
+  }
   __host__ __device__ __forceinline__ unsigned int once(unsigned int x) const {
-    // state (L: a bits, R: b bits) -> (R, L ^ F(R)); shapes alternate, 6 rounds
+    // state (L: a bits, R: b bits) -> (R, L ^ F(R)); shapes alternate, 4 rounds
+    // (Luby-Rackoff: 4 rounds of a keyed mixing function give a strong PRP)
     unsigned int a = lbits, b = rbits;
     unsigned int L = x >> b, R = x & ((1u << b) - 1u);
 #pragma unroll
-    for (int r = 0; r < 6; r++) {
+    for (int r = 0; r < 4; r++) {
       unsigned int f = mix32(R ^ keys[r]) & ((1u << a) - 1u);
       unsigned int nL = R, nR = L ^ f;
       // new shape: L has b bits, R has a bits
@@ -197,7 +243,19 @@ __host__ __device__ __forceinline__ int num_segments(int first, int beta, int si
   return first < side ? 1 + (side - first + beta - 1) / beta : 1;
 }
 
-__host__ __device__ __forceinline__ void set_pass_geometry(Ctrl* c, int dy, int dx) {
+__host__ __device__ __forceinline__ unsigned long long class_key(unsigned long long gkey, int h,
+                                                                 int w) {
+  unsigned long long k = gkey ^ ((unsigned long long)(unsigned)h << 32) ^ (unsigned)w;
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+// Geometry of the pass about to run (everything but the DEVICE-mode keys).
+__host__ __device__ __forceinline__ void set_pass_geometry_base(Ctrl* c, int dy, int dx) {
   c->dy = dy;
   c->dx = dx;
   c->first_y = dy > 0 ? dy : c->beta;
@@ -206,6 +264,39 @@ __host__ __device__ __forceinline__ void set_pass_geometry(Ctrl* c, int dy, int 
   c->nbx = num_segments(c->first_x, c->beta, c->side);
   c->cap = (c->beta * c->beta + 3) / 4;
   c->total_groups = (long long)c->nby * c->nbx * c->cap;
+  int lo, hi;
+  segment(0, c->first_y, c->beta, c->side, &lo, &hi);
+  c->seg_h[0] = hi - lo;
+  c->seg_h[1] = c->beta;
+  segment(c->nby - 1, c->first_y, c->beta, c->side, &lo, &hi);
+  c->seg_h[2] = hi - lo;
+  segment(0, c->first_x, c->beta, c->side, &lo, &hi);
+  c->seg_w[0] = hi - lo;
+  c->seg_w[1] = c->beta;
+  segment(c->nbx - 1, c->first_x, c->beta, c->side, &lo, &hi);
+  c->seg_w[2] = hi - lo;
+  c->tile = use_tile(c->beta, c->S) ? 1 : 0;
+  make_fastdiv((unsigned)c->cap, &c->cap_m, &c->cap_l);
+  make_fastdiv((unsigned)c->nbx, &c->nbx_m, &c->nbx_l);
+}
+
+// DEVICE-mode Feistel keys of block class cls.  gkey keys the per-class
+// groupings; classes with equal (h, w) get identical keys, so all blocks of
+// one shape share one grouping (plas.py:209).
+__host__ __device__ __forceinline__ void set_class_keys(Ctrl* c, int cls, unsigned long long gkey) {
+  const int hh = c->seg_h[cls / 3], ww = c->seg_w[cls % 3];
+  Feistel fe;
+  fe.init(class_key(gkey, hh, ww), (unsigned)(hh * ww));
+  for (int r = 0; r < 6; r++) c->fe_keys[cls][r] = fe.keys[r];
+  c->fe_lbits[cls] = fe.lbits;
+  c->fe_rbits[cls] = fe.rbits;
+}
+
+__host__ __device__ __forceinline__ void set_pass_geometry(Ctrl* c, int dy, int dx,
+                                                           unsigned long long gkey) {
+  set_pass_geometry_base(c, dy, dx);
+  if (c->rng_mode == 1)
+    for (int cls = 0; cls < 9; cls++) set_class_keys(c, cls, gkey);
 }
 
 // DEVICE-mode per-pass draws: dy, dx and the grouping key come from the
@@ -219,17 +310,6 @@ __host__ __device__ __forceinline__ void device_pass_draws(const Ctrl* c, int* d
   *dy = (int)d.bounded((unsigned)c->beta);
   *dx = (int)d.bounded((unsigned)c->beta);
   *gkey = d.next64();
-}
-
-__host__ __device__ __forceinline__ unsigned long long class_key(unsigned long long gkey, int h,
-                                                                 int w) {
-  unsigned long long k = gkey ^ ((unsigned long long)(unsigned)h << 32) ^ (unsigned)w;
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdull;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ull;
-  k ^= k >> 33;
-  return k;
 }
 
 // warp / block reductions in fp64 with a fixed order (deterministic)

@@ -57,33 +57,27 @@ __global__ void perm_i32_to_i64_kernel(const int* __restrict__ in, long long* __
 }
 
 // ---------------------------------------------------------------- distance
-// partial sums of per-cell fp64 Euclidean distances between feat and target
-__global__ void __launch_bounds__(RED_THREADS) distance_kernel(const float* __restrict__ a,
-                                                               const float* __restrict__ b,
-                                                               long long n, int D, int S,
-                                                               double* __restrict__ partials) {
-  __shared__ double sh[32];
-  double sum = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    const float* pa = a + i * S;
-    const float* pb = b + i * S;
-    for (int c = 0; c < S; c += 4) {
-      float4 x = *reinterpret_cast<const float4*>(pa + c);
-      float4 y = *reinterpret_cast<const float4*>(pb + c);
-      float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+// Per-cell squared distance in fp64 with a fixed evaluation order shared with
+// the pass kernel (assign.cuh dist_accum): chunk c (4 channels) extends the
+// sequential fma chain p[c % 4]; the cell's value is ((p0 + p1) + (p2 + p3)).
+// grid_distance (plas.py:71-84) is order-free in fp64.
+__device__ __forceinline__ double cell_dist2(const float* __restrict__ a, const float* __restrict__ b,
+                                             int D, int S) {
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c = 0; c < (S >> 2); c++) {
+    const float4 x = *reinterpret_cast<const float4*>(a + 4 * c);
+    const float4 y = *reinterpret_cast<const float4*>(b + 4 * c);
+    const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+    double acc = p[c & 3];
 #pragma unroll
-      for (int e = 0; e < 4; e++)
-        if (c + e < D) {
-          double df = (double)xs[e] - (double)ys[e];
-          s = fma(df, df, s);
-        }
-    }
-    sum += sqrt(s);
+    for (int e = 0; e < 4; e++)
+      if (4 * c + e < D) {
+        const double df = (double)xs[e] - (double)ys[e];
+        acc = fma(df, df, acc);
+      }
+    p[c & 3] = acc;
   }
-  double tot = block_sum<RED_THREADS>(sum, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  return (p[0] + p[1]) + (p[2] + p[3]);
 }
 
 // fixed-order fp64 reduction of `nparts` partials by one CTA (thread 0 result)
@@ -106,12 +100,28 @@ __device__ __forceinline__ void set_cond(unsigned long long handle, unsigned v) 
   if (handle) cudaGraphSetConditional((cudaGraphConditionalHandle)handle, v);
 }
 
-// prepare the pass about to run (DEVICE mode draws its own offsets)
+// Prepare the pass about to run (DEVICE mode draws its own offsets).  Called
+// by all threads of one CTA: thread 0 draws and lays out the pass, threads
+// 0..8 derive the nine block-class Feistel keys in parallel.
+__device__ __forceinline__ void prepare_device_pass_cta(Ctrl* c, unsigned long long* s_gkey) {
+  if (threadIdx.x == 0) {
+    int dy, dx;
+    unsigned long long gk;
+    device_pass_draws(c, &dy, &dx, &gk);
+    set_pass_geometry_base(c, dy, dx);
+    *s_gkey = gk;
+  }
+  __syncthreads();
+  if (threadIdx.x < 9) set_class_keys(c, threadIdx.x, *s_gkey);
+  __syncthreads();
+}
+
+// serial version (host-stepped DEVICE mode launches it as its own kernel)
 __device__ __forceinline__ void prepare_device_pass(Ctrl* c) {
   int dy, dx;
   unsigned long long gk;
   device_pass_draws(c, &dy, &dx, &gk);
-  set_pass_geometry(c, dy, dx);
+  set_pass_geometry(c, dy, dx, gk);
 }
 
 __global__ void level_begin_kernel(Ctrl* c, Sched s) {
@@ -124,54 +134,140 @@ __global__ void level_begin_kernel(Ctrl* c, Sched s) {
   c->level_done = 0;
 }
 
-// level-start distance -> previous (plas.py:256-258); opens the pass loop
-__global__ void __launch_bounds__(RED_THREADS) level_start_finalize_kernel(
-    Ctrl* c, Sched s, const double* partials, int nparts, long long n, unsigned long long inner) {
-  __shared__ double sh[32];
-  double tot = reduce_partials(partials, nparts, sh);
-  if (threadIdx.x) return;
-  double d = tot / (double)n;
-  c->previous = d;
-  if (c->trace_pos >= c->trace_cap) {
-    c->status = 1;
-    c->level_done = 1;
-    set_cond(inner, 0);
-    return;
+// Last-CTA-done protocol: every CTA writes its partial, fences and takes a
+// ticket; the CTA with the last ticket sees all partials, reduces them in a
+// fixed order (deterministic) and runs the controller.  Returns true there.
+__device__ __forceinline__ bool last_cta_reduce(double v, double* partials, int* done, double* total,
+                                                double* sh) {
+  __shared__ int s_last;
+  const double blk = block_sum<RED_THREADS>(v, sh);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = blk;
+    __threadfence();
+    s_last = atomicAdd(done, 1) == (int)gridDim.x - 1;
   }
-  s.trace[c->trace_pos++] = d;
-  if (c->rng_mode == 1) prepare_device_pass(c);
-  set_cond(inner, 1);
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += ((volatile double*)partials)[i];
+  t = block_sum<RED_THREADS>(t, sh);
+  if (threadIdx.x == 0) {
+    *total = t;
+    *done = 0;
+  }
+  __syncthreads();
+  return true;
 }
 
-// after a pass: current, strike logic (plas.py:266-272), next pass geometry
-__global__ void __launch_bounds__(RED_THREADS) pass_finalize_kernel(
-    Ctrl* c, Sched s, const double* partials, int nparts, long long n, unsigned long long inner) {
+// Level start (plas.py:256-258): fp64 distance of every cell to the fresh
+// target into the cache, sum -> previous, trace, open the pass loop.
+__global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
+    Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
+    double* __restrict__ dcache, long long n, int D, int S, double* partials, int* done,
+    unsigned long long inner, unsigned long long tile_cond) {
   __shared__ double sh[32];
-  double tot = reduce_partials(partials, nparts, sh);
-  if (threadIdx.x) return;
-  const double current = tot / (double)n;
-  const double previous = c->previous;
-  c->current = current;
-  c->reorders++;
-  c->pass++;
-  if (c->trace_pos >= c->trace_cap) {
-    c->status = 1;
-    c->level_done = 1;
-    set_cond(inner, 0);
-    return;
+  __shared__ double s_tot;
+  __shared__ unsigned long long s_gkey;
+  double sum = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double d = sqrt(cell_dist2(feat + i * S, target + i * S, D, S));
+    dcache[i] = d;
+    sum += d;
   }
-  s.trace[c->trace_pos++] = current;
-  if (previous <= 0.0 || (previous - current) / previous < c->threshold)
-    c->strikes++;
-  else
-    c->strikes = 0;
-  c->previous = current;
-  if (c->strikes >= 2) {
-    c->level_done = 1;
-    set_cond(inner, 0);
-  } else if (c->rng_mode == 1) {
-    prepare_device_pass(c);
+  if (!last_cta_reduce(sum, partials, done, &s_tot, sh)) return;
+  bool go = false;
+  if (threadIdx.x == 0) {
+    const double tot = s_tot;
+    c->dist_sum = tot;
+    c->previous = tot / (double)n;
+    if (c->trace_pos >= c->trace_cap) {
+      c->status = 1;
+      c->level_done = 1;
+      set_cond(inner, 0);
+    } else {
+      s.trace[c->trace_pos++] = c->previous;
+      go = true;
+    }
   }
+  go = __syncthreads_or(go);
+  if (!go) return;
+  if (c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
+  if (threadIdx.x == 0) {
+    if (c->rng_mode == 1) set_cond(tile_cond, c->tile);
+    set_cond(inner, 1);
+  }
+}
+
+// After a pass: exact fp64 distance change of the moved cells (cells that
+// keep their element keep their cached distance), so current =
+// (level-start sum + deltas) / n equals grid_distance(feat, target)
+// (plas.py:266) up to fp64 summation order; then the strike logic
+// (plas.py:267-272) and the next pass's geometry.
+__global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
+    Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
+    double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
+    double* partials, int* done, long long n, unsigned long long inner, unsigned long long tile_cond) {
+  __shared__ double sh[32];
+  __shared__ double s_tot;
+  __shared__ unsigned long long s_gkey;
+  const int count = counters[2];
+  double sum = 0.0;
+  const int stride = gridDim.x * blockDim.x;
+  // four independent cells per thread in flight
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < count; e0 += 4 * stride) {
+    long long cell[4];
+    double old[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int e = e0 + u * stride;
+      cell[u] = e < count ? list[e] : -1;
+      old[u] = cell[u] >= 0 ? dcache[cell[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      if (cell[u] >= 0) {
+        const double d = sqrt(cell_dist2(feat + cell[u] * S, target + cell[u] * S, D, S));
+        sum += d - old[u];
+        dcache[cell[u]] = d;
+      }
+    }
+  }
+  if (!last_cta_reduce(sum, partials, done, &s_tot, sh)) return;
+  bool more = false;
+  if (threadIdx.x == 0) {
+    counters[0] += count;
+    counters[2] = 0;
+    c->dist_sum += s_tot;
+    const double current = c->dist_sum / (double)n;
+    const double previous = c->previous;
+    c->current = current;
+    c->reorders++;
+    c->pass++;
+    if (c->trace_pos >= c->trace_cap) {
+      c->status = 1;
+      c->level_done = 1;
+      set_cond(inner, 0);
+    } else {
+      s.trace[c->trace_pos++] = current;
+      if (previous <= 0.0 || (previous - current) / previous < c->threshold)
+        c->strikes++;
+      else
+        c->strikes = 0;
+      c->previous = current;
+      if (c->strikes >= 2) {
+        c->level_done = 1;
+        set_cond(inner, 0);
+      } else {
+        more = true;
+      }
+    }
+  }
+  more = __syncthreads_or(more);
+  if (!more || c->rng_mode != 1) return;
+  prepare_device_pass_cta(c, &s_gkey);
+  if (threadIdx.x == 0) set_cond(tile_cond, c->tile);
 }
 
 // level bookkeeping (plas.py:273-274); radius decay is the schedule table
@@ -186,7 +282,7 @@ __global__ void level_end_kernel(Ctrl* c, Sched s, unsigned long long outer) {
 // parity mode: host-drawn offsets for the next pass
 __global__ void set_pass_kernel(Ctrl* c, int dy, int dx) {
   if (threadIdx.x) return;
-  set_pass_geometry(c, dy, dx);
+  set_pass_geometry(c, dy, dx, 0ull);
 }
 
 // ---------------------------------------------------------------- VAD

@@ -152,6 +152,7 @@ void build_schedule(const plas_sort_args* a, int side, Schedule* s) {
 struct SortWs {
   Ctrl* ctrl;
   float *feat, *target, *tmp, *den32;
+  double* dcache;  // per-cell fp64 distance to the target (level start + pass updates)
   int* idx;
   double* rowweight;
   double* partials;
@@ -166,10 +167,12 @@ struct SortWs {
   int* mp;   // parity: master permutation (beta0^2)
   int* sel;  // parity: 9 class selections
   long long sel_stride;
+  int* list;      // moved-cell list of the current pass
+  double* spart;  // statistic-kernel partials
 };
 
 size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long long tcap,
-                  int rng_mode, int side, SortWs* w) {
+                  int rng_mode, int side, long long list_cap, SortWs* w) {
   Carver c{base};
   const int S = row_stride(dim);
   w->ctrl = c.take<Ctrl>(1);
@@ -177,6 +180,7 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->target = c.take<float>((size_t)n * S);
   w->tmp = c.take<float>((size_t)n * S);
   w->den32 = c.take<float>((size_t)n);
+  w->dcache = c.take<double>((size_t)n);
   w->idx = c.take<int>((size_t)n);
   w->rowweight = c.take<double>((size_t)side);
   w->partials = c.take<double>(MAX_PARTS);
@@ -193,6 +197,8 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->sel_stride = rng_mode == PLAS_RNG_PARITY ? b0 * b0 : 0;
   w->mp = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(b0 * b0) : 1);
   w->sel = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(9 * b0 * b0) : 1);
+  w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
+  w->spart = c.take<double>(MAX_PARTS);
   return align_up(c.off);
 }
 
@@ -232,21 +238,20 @@ cudaError_t add_while(cudaGraphNode_t* out, cudaGraph_t g, const cudaGraphNode_t
 struct Launch {
   int S, D, side;
   long long n;
-  int blur_grid, den_grid, rows_grid, dist_grid, pass_grid, vad_grid;
+  int blur_grid, den_grid, rows_grid, dist_grid, pass_grid, tile_grid, vad_grid;
   BlurLevelRef lvl;
   Sched sched;
 };
 
 template <bool PARITY>
 void* pass_kernel_ptr(int S) {
-  if (S <= 16) return (void*)pass_kernel<16, PARITY>;
-  if (S <= 64) return (void*)pass_kernel<64, PARITY>;
-  return (void*)pass_kernel<0, PARITY>;
+  if (S <= 16) return (void*)pass_kernel<false, PARITY>;
+  return (void*)pass_kernel<true, PARITY>;
 }
 
 int pass_grid_size(int S) {
   static int cached[3] = {0, 0, 0};
-  int which = S <= 16 ? 0 : (S <= 64 ? 1 : 2);
+  int which = S <= 16 ? 0 : 1;
   if (!cached[which]) {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)pass_kernel_ptr<false>(S), 256, 0);
@@ -255,6 +260,41 @@ int pass_grid_size(int S) {
   }
   return cached[which];
 }
+
+template <bool PARITY>
+void* tile_kernel_ptr(int S) {
+  if (S <= 16) return (void*)tile_pass_kernel<false, PARITY>;
+  return (void*)tile_pass_kernel<true, PARITY>;
+}
+
+// largest tile block side for row stride S and its two-stage shared memory
+int tile_beta_max(int S) {
+  int b = 1;
+  while (use_tile(b + 1, S)) b++;
+  return b;
+}
+size_t tile_smem_bytes(int S) { return (size_t)(2 * tile_stage_bytes(tile_beta_max(S), S)); }
+
+int tile_grid_size(int S) {
+  static int cached[65] = {0};
+  const int key = S <= 64 ? S : 64;
+  // the attribute is per kernel, so set it for this S on every sort
+  const size_t smem = tile_smem_bytes(S);
+  cudaFuncSetAttribute(tile_kernel_ptr<false>(S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(tile_kernel_ptr<true>(S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!cached[key]) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel_ptr<false>(S), TILE_THREADS, smem);
+    if (occ <= 0) occ = 1;
+    cached[key] = std::min(num_sms() * occ, MAX_PARTS);
+  }
+  return cached[key];
+}
+
+// Capacity of the moved-cell list: every cell changes element at most once per pass.
+long long list_capacity(long long n) { return n; }
+
+int stats_grid_size() { return std::min(num_sms() * 4, MAX_PARTS); }
 
 }  // namespace
 
@@ -282,8 +322,9 @@ int plas_num_levels(int64_t n, double radius_decay, double initial_radius) {
 size_t plas_sort_workspace_bytes(int64_t n, int dim, int num_levels, int64_t weights_len,
                                  int64_t trace_capacity, int rng_mode) {
   SortWs w;
-  int side = (int)llround(sqrt((double)n));
-  return carve_sort(nullptr, n, dim, num_levels, weights_len, trace_capacity, rng_mode, side, &w);
+  const int side = (int)llround(sqrt((double)n));
+  const long long lc = list_capacity(n);
+  return carve_sort(nullptr, n, dim, num_levels, weights_len, trace_capacity, rng_mode, side, lc, &w);
 }
 
 void plas_seed_key(uint64_t seed, uint64_t key[2]) { host::seed_key(seed, key); }
@@ -316,11 +357,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   const int L = (int)sch.radii.size();
   const long long tcap = std::max<long long>(a->trace_capacity, 1);
   SortWs w;
-  size_t need = carve_sort(nullptr, n, D, L, (long long)sch.weights.size(), tcap, mode, side, &w);
+  const int S = row_stride(D);
+  const long long lcap = list_capacity(n);
+  size_t need = carve_sort(nullptr, n, D, L, (long long)sch.weights.size(), tcap, mode, side, lcap, &w);
   if (!wsp || ws_bytes < need)
     return fail(PLAS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
-  carve_sort((char*)wsp, n, D, L, (long long)sch.weights.size(), tcap, mode, side, &w);
-  const int S = row_stride(D);
+  carve_sort((char*)wsp, n, D, L, (long long)sch.weights.size(), tcap, mode, side, lcap, &w);
 
   // ---- upload schedule + controller
   if (L > 0) {
@@ -335,6 +377,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   memset(&hc, 0, sizeof(hc));
   hc.num_levels = L;
   hc.side = side;
+  hc.S = row_stride(D);
   hc.trace_cap = tcap;
   hc.rng_mode = mode;
   hc.threshold = a->improvement_threshold;
@@ -403,6 +446,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.dist_grid = grid_for(n, RED_THREADS, 4);
   lc.vad_grid = grid_for(n * D, RED_THREADS, 4);
   lc.pass_grid = pass_grid_size(S);
+  lc.tile_grid = tile_grid_size(S);
   lc.lvl = BlurLevelRef{w.ctrl, w.hs, w.weights, w.woff, 0, nullptr};
   lc.sched = Sched{w.radii, w.betas, w.hs, w.level_counts, w.trace};
 
@@ -418,16 +462,24 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   };
   if (int e = vad_launch(w.scalars + 1)) return e;
 
+  const int sgrid = stats_grid_size();
+  int* counters = w.flags + 2;  // [0] moved cells, [1] exact decisions, [2] moved-list length
+  MoveOut ml{w.list, counters + 2};
+  int* done = w.flags + 6;      // last-CTA ticket of the statistic kernels
   if (mode == PLAS_RNG_DEVICE && !a->profile) {
     // ------------------------------------------------------------ graph
+    // outer WHILE (levels): level_begin, border weight, blur axis 0, blur axis 1,
+    //   level statistics, inner WHILE (passes): IF(tile){tile}ELSE{gather},
+    //   pass statistics (+controller); level_end.
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle outer_h, inner_h;
+    cudaGraphConditionalHandle outer_h, inner_h, tile_h;
     CK(cudaGraphConditionalHandleCreate(&outer_h, g, L > 0 ? 1 : 0, cudaGraphCondAssignDefault));
     cudaGraphNode_t outer_node;
     cudaGraph_t obody;
     CK(add_while(&outer_node, g, nullptr, 0, outer_h, &obody));
     CK(cudaGraphConditionalHandleCreate(&inner_h, obody, 0, 0));
+    CK(cudaGraphConditionalHandleCreate(&tile_h, obody, 0, 0));
     cudaGraphNode_t nd[8];
     CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched));
     CK(add_kernel(&nd[1], obody, &nd[0], 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
@@ -439,18 +491,26 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(add_kernel(&nd[4], obody, &nd[3], 1, blur_axis_kernel<float, float, 1, 1>, dim3(lc.blur_grid),
                   dim3(256), (const float*)w.tmp, w.target, side, side, D, S, lc.lvl,
                   (const void*)w.den32));
-    CK(add_kernel(&nd[5], obody, &nd[4], 1, distance_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
-                  (const float*)w.feat, (const float*)w.target, n, D, S, w.partials));
-    CK(add_kernel(&nd[6], obody, &nd[5], 1, level_start_finalize_kernel, dim3(1), dim3(RED_THREADS),
-                  w.ctrl, lc.sched, (const double*)w.partials, lc.dist_grid, n,
-                  (unsigned long long)inner_h));
+    CK(add_kernel(&nd[5], obody, &nd[4], 1, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
+                  w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
+                  w.spart, done, (unsigned long long)inner_h, (unsigned long long)tile_h));
     cudaGraphNode_t inner_node;
     cudaGraph_t ibody;
-    CK(add_while(&inner_node, obody, &nd[6], 1, inner_h, &ibody));
-    CK(add_kernel(&nd[7], obody, &inner_node, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl,
+    CK(add_while(&inner_node, obody, &nd[5], 1, inner_h, &ibody));
+    CK(add_kernel(&nd[6], obody, &inner_node, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl,
                   lc.sched, (unsigned long long)outer_h));
-    cudaGraphNode_t pn[2];
-    cudaKernelNodeParams kp{};
+    cudaGraphNode_t if_node, pn[3];
+    cudaGraph_t if_bodies[2];
+    {
+      cudaGraphNodeParams p{};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = tile_h;
+      p.conditional.type = cudaGraphCondTypeIf;
+      p.conditional.size = 2;
+      CK(cudaGraphAddNode(&if_node, ibody, nullptr, 0, &p));
+      if_bodies[0] = p.conditional.phGraph_out[0];
+      if_bodies[1] = p.conditional.phGraph_out[1];
+    }
     {
       float* feat = w.feat;
       int* idx = w.idx;
@@ -458,18 +518,25 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       const Ctrl* ctrl = w.ctrl;
       const int* sel = nullptr;
       long long sstride = 0;
-      double* partials = w.partials;
-      int* moved = nullptr;
       int Dv = D, Sv = S;
-      void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &partials, &moved};
+      void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &ml, &counters};
+      cudaKernelNodeParams kp{};
+      kp.func = tile_kernel_ptr<false>(S);
+      kp.gridDim = dim3(lc.tile_grid);
+      kp.blockDim = dim3(TILE_THREADS);
+      kp.sharedMemBytes = (unsigned)tile_smem_bytes(S);
+      kp.kernelParams = args;
+      CK(cudaGraphAddKernelNode(&pn[0], if_bodies[0], nullptr, 0, &kp));
       kp.func = pass_kernel_ptr<false>(S);
       kp.gridDim = dim3(lc.pass_grid);
       kp.blockDim = dim3(256);
-      kp.kernelParams = args;
-      CK(cudaGraphAddKernelNode(&pn[0], ibody, nullptr, 0, &kp));
+      kp.sharedMemBytes = 0;
+      CK(cudaGraphAddKernelNode(&pn[1], if_bodies[1], nullptr, 0, &kp));
     }
-    CK(add_kernel(&pn[1], ibody, &pn[0], 1, pass_finalize_kernel, dim3(1), dim3(RED_THREADS), w.ctrl,
-                  lc.sched, (const double*)w.partials, lc.pass_grid, n, (unsigned long long)inner_h));
+    CK(add_kernel(&pn[2], ibody, &if_node, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl,
+                  lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, D, S,
+                  (const int*)w.list, counters, w.spart, done, n, (unsigned long long)inner_h,
+                  (unsigned long long)tile_h));
     cudaGraphExec_t ge;
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
@@ -522,6 +589,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     };
     int pp = 0;
     void* kfn = parity ? pass_kernel_ptr<true>(S) : pass_kernel_ptr<false>(S);
+    void* tfn = parity ? tile_kernel_ptr<true>(S) : tile_kernel_ptr<false>(S);
     for (int lv = 0; lv < L; lv++) {
       const int beta = sch.betas[lv];
       const long long bsq = (long long)beta * beta;
@@ -539,10 +607,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                                                                             S, lc.lvl, w.den32);
       });
       timed(K_DIST, [&] {
-        distance_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.feat, w.target, n, D, S, w.partials);
-      });
-      timed(K_CTRL, [&] {
-        level_start_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.partials, lc.dist_grid, n, 0);
+        level_stats_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, n,
+                                                                 D, S, w.spart, done, 0, 0);
       });
       CKL();
       int dy = 0, dx = 0;
@@ -566,19 +632,24 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           const Ctrl* ctrl = w.ctrl;
           const int* sel = parity ? w.sel : nullptr;
           long long sstride = parity ? w.sel_stride : 0;
-          double* partials = w.partials;
-          int* moved = nullptr;
           int Dv = D, Sv = S;
-          void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &partials, &moved};
+          void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &ml, &counters};
           cudaError_t le = cudaSuccess;
-          timed(K_PASS, [&] { le = cudaLaunchKernel(kfn, dim3(lc.pass_grid), dim3(256), args, 0, st); });
+          if (use_tile(beta, S))
+            timed(K_PASS, [&] {
+              le = cudaLaunchKernel(tfn, dim3(lc.tile_grid), dim3(TILE_THREADS), args,
+                                    (size_t)(2 * tile_stage_bytes(beta, S)), st);
+            });
+          else
+            timed(K_PASS, [&] { le = cudaLaunchKernel(kfn, dim3(lc.pass_grid), dim3(256), args, 0, st); });
           if (le != cudaSuccess) {
             cleanup();
             return fail(PLAS_ERR_CUDA, std::string("pass launch: ") + cudaGetErrorString(le));
           }
         }
         timed(K_CTRL, [&] {
-          pass_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.partials, lc.pass_grid, n, 0);
+          pass_stats_kernel<<<sgrid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, D, S,
+                                                           w.list, counters, w.spart, done, n, 0, 0);
         });
         CKL();
         CK(cudaMemcpyAsync(hflag, &w.ctrl->level_done, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -619,7 +690,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   CK(cudaEventRecord(ev1, st));
   Ctrl out;
   double sc[3];
+  int fl[8];
   CK(cudaMemcpyAsync(&out, w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(fl, w.flags, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(sc, w.scalars, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   float ms = 0.f;
@@ -632,6 +705,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   res->reorders = out.reorders;
   res->levels_done = out.levels_done;
   res->trace_len = out.trace_pos;
+  res->cells_moved = fl[2];
+  res->exact_warps = fl[3];
   if (out.status) return fail(PLAS_ERR_CAPACITY, "trace capacity exceeded");
   if (res->level_counts && L > 0)
     CK(cudaMemcpy(res->level_counts, w.level_counts, sizeof(long long) * L, cudaMemcpyDeviceToHost));
@@ -648,14 +723,11 @@ int plas_assign_groups(float* feat, int64_t* point_idx, const float* target, int
   cudaStream_t st = (cudaStream_t)stream;
   int grid = grid_for(num_groups * 4, 256, 4);
   if (stride <= 16)
-    groups_kernel<16><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
-                                            (const long long*)groups, num_groups, group_size);
-  else if (stride <= 64)
-    groups_kernel<64><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
-                                            (const long long*)groups, num_groups, group_size);
+    groups_kernel<false><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
+                                               (const long long*)groups, num_groups, group_size);
   else
-    groups_kernel<0><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
-                                           (const long long*)groups, num_groups, group_size);
+    groups_kernel<true><<<grid, 256, 0, st>>>(feat, (long long*)point_idx, target, dim, stride,
+                                              (const long long*)groups, num_groups, group_size);
   CKL();
   return PLAS_OK;
 }

@@ -259,6 +259,8 @@ class SortPlan:
             "reorders": int(res.reorders),
             "radius_trace": tuple(traces),
             "gpu_ms": float(res.gpu_ms),
+            "cells_moved": int(res.cells_moved),
+            "exact_warps": int(res.exact_warps),
         }
 
 
