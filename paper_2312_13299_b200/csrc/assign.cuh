@@ -330,32 +330,43 @@ struct MoveOut {
   int* count;
 };
 
-constexpr int LIST_CAP = 4096;  // shared staging entries per CTA
+constexpr int WARP_LIST = 512;  // shared staging entries per warp
 
-// append this lane's moved cell (if mv) to the CTA staging list
-__device__ __forceinline__ void stage_move(bool mv, int cell, int* s_list, int* s_cnt) {
+// Append this lane's moved cell (if mv) to its warp's staging segment; the
+// warp-uniform fill level lives in *wcnt (a register in every lane).  A full
+// segment is flushed by the warp with one global reservation.
+__device__ __forceinline__ void stage_move(bool mv, int cell, int* wlist, int* wcnt, const MoveOut& mo) {
   const unsigned bal = __ballot_sync(PLAS_FULL_MASK, mv);
   if (!bal) return;
   const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (lane == __ffs(bal) - 1) base = atomicAdd(s_cnt, __popc(bal));
-  base = __shfl_sync(PLAS_FULL_MASK, base, __ffs(bal) - 1);
-  if (mv) s_list[base + __popc(bal & ((1u << lane) - 1u))] = cell;
+  if (mv) wlist[*wcnt + __popc(bal & ((1u << lane) - 1u))] = cell;
+  *wcnt += __popc(bal);
+  if (*wcnt > WARP_LIST - 32) {
+    __syncwarp();
+    int base = 0;
+    if (lane == 0) base = atomicAdd(mo.count, *wcnt);
+    base = __shfl_sync(PLAS_FULL_MASK, base, 0);
+    for (int i = lane; i < *wcnt; i += 32) mo.list[base + i] = wlist[i];
+    __syncwarp();
+    *wcnt = 0;
+  }
 }
 
-// CTA-wide: copy the staged list to the global list (one reservation)
-__device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int* s_cnt, int* s_base) {
+// CTA-wide: append every warp's remaining entries with one reservation
+__device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int wcnt, int* s_wcnt,
+                                            int* s_base) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) s_wcnt[wid] = wcnt;
   __syncthreads();
-  const int n = *s_cnt;
-  if (n) {
-    if (threadIdx.x == 0) *s_base = atomicAdd(mo.count, n);
-    __syncthreads();
-    const int b = *s_base;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) mo.list[b + i] = s_list[i];
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < nw; w++) tot += s_wcnt[w];
+    *s_base = tot ? atomicAdd(mo.count, tot) : 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) *s_cnt = 0;
-  __syncthreads();
+  int off = *s_base;
+  for (int w = 0; w < wid; w++) off += s_wcnt[w];
+  for (int i = lane; i < wcnt; i += 32) mo.list[off + i] = s_list[wid * WARP_LIST + i];
 }
 
 // per-pass class tables in shared memory
@@ -363,7 +374,7 @@ struct PassShared {
   unsigned keys[9][6];
   int bits[9][2];
   int seg[6];
-  int cnt;
+  int wcnt[32];
   int base;
 };
 
@@ -377,7 +388,6 @@ __device__ __forceinline__ void load_pass_shared(PassShared& ps, const Ctrl* __r
     ps.seg[threadIdx.x] = ctrl->seg_h[threadIdx.x];
     ps.seg[3 + threadIdx.x] = ctrl->seg_w[threadIdx.x];
   }
-  if (threadIdx.x == 0) ps.cnt = 0;
   __syncthreads();
 }
 
@@ -393,8 +403,10 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
                                                        const int* __restrict__ sel, long long sel_stride,
                                                        MoveOut mo, int* __restrict__ counters) {
   __shared__ PassShared ps;
-  __shared__ int s_list[LIST_CAP];
+  __shared__ int s_list[8 * WARP_LIST];
   load_pass_shared(ps, ctrl);
+  int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
+  int wcnt = 0;
   const int side = ctrl->side;
   const int beta = ctrl->beta;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
@@ -470,11 +482,9 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
     }
     const int dcell = pick4(rowj, pick4(dst, s));
     if (my_mv) idx[dcell] = my_idx;
-    stage_move(my_mv, dcell, s_list, &ps.cnt);
-    __syncthreads();
-    if (ps.cnt > LIST_CAP - 256) flush_moves(mo, s_list, &ps.cnt, &ps.base);
+    stage_move(my_mv, dcell, wlist, &wcnt, mo);
   }
-  flush_moves(mo, s_list, &ps.cnt, &ps.base);
+  flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
 }
@@ -533,8 +543,10 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
     int* __restrict__ counters) {
   extern __shared__ float4 smem4[];
   __shared__ PassShared ps;
-  __shared__ int s_list[LIST_CAP];
+  __shared__ int s_list[8 * WARP_LIST];
   load_pass_shared(ps, ctrl);
+  int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
+  int wcnt = 0;
   const int side = ctrl->side;
   const int beta = ctrl->beta;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
@@ -627,14 +639,12 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
       const bool my_mv = pick4(mv, s);
       const long long dcell = pick4(gcell, pick4(dst, s));
       if (my_mv) idx[dcell] = sI[pick4(rowj, s)];
-      stage_move(my_mv, (int)dcell, s_list, &ps.cnt);
-      __syncthreads();
-      if (ps.cnt > LIST_CAP - TILE_THREADS) flush_moves(mo, s_list, &ps.cnt, &ps.base);
+      stage_move(my_mv, (int)dcell, wlist, &wcnt, mo);
     }
     __syncthreads();  // stage st is refilled by the prefetch two iterations on
   }
   cp_async_wait<0>();
-  flush_moves(mo, s_list, &ps.cnt, &ps.base);
+  flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
 }

@@ -1,194 +1,207 @@
-// K1 fast tier: separable-blur axis pass with fp32 output, bit-identical to
-// the exact SciPy fold (blur.cuh) by construction.
+// K1 fast tier for the sort: separable-blur axis passes with fp32 output,
+// bit-identical to the exact SciPy fold (blur.cuh) by construction.
 //
-// The exact fold is  acc = x0 w0;  for j = h..1: acc = RN(acc + RN(RN(lo+hi) w_j))
-// (3 fp64 ops per tap).  This kernel folds with  acc = fma(RN(lo+hi), w_j, acc)
-// (2 fp64 ops per tap).  Both results lie within (2h+3) 2^-53 A of the exact
-// real sum, A = sum_i |x_i| w_|i| <= 2 M (M = max |x| over the window,
-// sum_j w_j = 1), so when RN32(acc - B) == RN32(acc + B) with
-// B = (2h+4) 2^-53 2M, both round to the same fp32 value, which is the
-// reference's output.  Otherwise the element is appended to a fallback list
-// and blur_fallback_kernel recomputes it with the exact fold (rare: the bound
-// only straddles an fp32 rounding boundary for ~0.1-1% of the outputs at the
-// largest radii).  If the list overflows, every element is recomputed.
+// Exact fold (SciPy correlate1d):  acc = x0 w0;  for j = h..1:
+//     acc = RN(acc + RN(RN(lo + hi) w_j))                (3 fp64 ops per tap)
+// Fast fold here:                  acc = fma(RN(lo + hi), w_j, acc)  (2 ops)
+// Both lie within (2h+3) 2^-53 A of the exact real sum, A = sum_i |x_i| w_|i|
+// <= 2 M with M = max |x| over the thread's input window (the weights sum
+// to 1), so when RN32(acc - B) == RN32(acc + B) for B = (2h+4) 2^-53 2M (plus
+// slack) both round to the same fp32 value -- the reference's output.
+// Otherwise the element goes to a fallback list and blur_fallback_kernel
+// recomputes it with the exact fold (~0.1-1% of the outputs at the largest
+// radii, fewer at small radii).  If the list overflows, every element is
+// recomputed exactly.
+//
+// Inputs are zero-padded by at least h + R elements at both ends of every
+// line (feat: PAD zero rows above and below; tmp: PAD zero cells at both ends
+// of every row), so the inner loop has no bounds checks: each step loads one
+// new "lo" and one new "hi" value through pointers that move by one stride.
 #pragma once
-#include <algorithm>
 #include "blur.cuh"
 
 namespace plas {
 
 constexpr int FB_HEADER = 16;  // ints before the list: [0] count
 
-template <typename Tin, int EPI, int AXIS, int R>
-__global__ void __launch_bounds__(256) blur_fast_kernel(const Tin* __restrict__ in, float* __restrict__ out,
-                                                        int H, int W, int C, int S, BlurLevelRef lvl,
-                                                        const float* __restrict__ den32,
-                                                        int* __restrict__ fb, int fb_cap) {
+struct PadGeom {
+  int H, W, C, S;
+  int pad;        // zero elements before/after every line (>= hmax + BLUR_R)
+};
+
+// AXIS 0: in = feat interior (row stride W*S, PAD zero rows above/below),
+//         out = tmp interior (row stride (W + 2 pad) * S).
+// AXIS 1: in = tmp interior, out = target (row stride W*S), EPI 1 divides by den32.
+template <int AXIS, int EPI>
+__global__ void __launch_bounds__(256, 3) blur_pad_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                       PadGeom pg, BlurLevelRef lvl,
+                                                       const float* __restrict__ den32,
+                                                       int* __restrict__ fb, int fb_cap,
+                                                       int* __restrict__ fb_other) {
+  constexpr int R = BLUR_R;
+  // the other axis' fallback list has been consumed by now: clear its counter
+  if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) fb_other[0] = 0;
   int h;
   const double* w;
   lvl.get(&h, &w);
+  const int H = pg.H, W = pg.W, C = pg.C, S = pg.S;
   const int n = AXIS == 0 ? H : W;
-  const long long stride = AXIS == 0 ? (long long)W * S : (long long)S;
+  const long long WS = (long long)W * S;
+  const long long WSP = (long long)(W + 2 * pg.pad) * S;  // tmp row stride
+  const long long in_stride = AXIS == 0 ? WS : (long long)S;
+  const long long out_stride = AXIS == 0 ? WSP : (long long)S;
   const int nchunks = (n + R - 1) / R;
   const double w0 = __ldg(w);
   const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
-  // axis 0: a CTA takes one 32-float column strip and 8 consecutive chunks, so its
-  // warps share input rows in L1; axis 1: consecutive threads walk channels, then chunks
-  const long long WS = (long long)W * S;
   const long long nstrips = (WS + 31) / 32;
   const long long ncg = (nchunks + 7) / 8;
-  const long long items = AXIS == 0 ? nstrips * ncg : 0;
-  const long long total = AXIS == 0 ? items * 256 : (long long)S * nchunks * H;
+  const long long total = AXIS == 0 ? nstrips * ncg * 256 : (long long)S * nchunks * H;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    long long base;
+    long long in_base, out_base, cellbase = 0;
     int chunk, c;
-    long long outer = 0, in_idx;
     if (AXIS == 0) {
+      // a CTA takes one 32-float column strip and 8 consecutive chunks, so its
+      // warps share input rows in L1
       const long long item = t >> 8;
       const int lt = (int)(t & 255);
       const long long strip = item % nstrips;
       chunk = (int)((item / nstrips) * 8 + (lt >> 5));
-      in_idx = strip * 32 + (lt & 31);
-      if (in_idx >= WS || chunk >= nchunks) continue;
-      c = (int)(in_idx % S);
-      base = in_idx;
+      const long long f = strip * 32 + (lt & 31);
+      if (f >= WS || chunk >= nchunks) continue;
+      c = (int)(f % S);
+      in_base = f;
+      out_base = (f / S) * S + c;  // same column of the tmp interior (row offset added per i)
+      cellbase = f / S;
     } else {
-      in_idx = t % S;
+      c = (int)(t % S);
       const long long rest = t / S;
       chunk = (int)(rest % nchunks);
-      outer = rest / nchunks;
-      c = (int)in_idx;
-      base = outer * WS + in_idx;
+      const long long y = rest / nchunks;
+      in_base = y * WSP + c;
+      out_base = y * WS + c;
+      cellbase = y * W;
     }
     if (c >= C) continue;
-    const Tin* line = in + base;
     const int i0 = chunk * R;
-    float mx = 0.f;
-    auto v = [&](int i) -> double {
-      if (i >= 0 && i < n) {
-        const float x = (float)__ldg(line + (long long)i * stride);
-        mx = fmaxf(mx, fabsf(x));
-        return (double)x;
-      }
-      return 0.0;
-    };
+    const float* line = in + in_base;
+    // lo ring: in[i0+k-h+t] at slot (k+t)%R ; hi ring: in[i0+k+h-t] at slot (k-t)%R
     double acc[R], lo[R], hi[R];
+    float mx = 0.f;
 #pragma unroll
     for (int k = 0; k < R; k++) {
-      acc[k] = __dmul_rn(v(i0 + k), w0);
-      lo[k] = v(i0 + k - h);
-      hi[k] = v(i0 + k + h);
+      const float xc = __ldg(line + (long long)(i0 + k) * in_stride);
+      const float xl = __ldg(line + (long long)(i0 + k - h) * in_stride);
+      const float xh = __ldg(line + (long long)(i0 + k + h) * in_stride);
+      mx = fmaxf(mx, fmaxf(fabsf(xc), fmaxf(fabsf(xl), fabsf(xh))));
+      acc[k] = __dmul_rn((double)xc, w0);
+      lo[k] = (double)xl;
+      hi[k] = (double)xh;
     }
+    const float* plo = line + (long long)(i0 + R - h) * in_stride;  // next lo value
+    const float* phi = line + (long long)(i0 + h - 1) * in_stride;  // next hi value
+    const double* pw = w + h;
     const int nblk = h / R, rem = h % R;
     for (int b = 0; b < nblk; b++) {
 #pragma unroll
       for (int u = 0; u < R; u++) {
-        const int tt = b * R + u;
-        const double wj = __ldg(w + (h - tt));
+        const double wj = __ldg(pw - u);
 #pragma unroll
         for (int k = 0; k < R; k++) acc[k] = fma(__dadd_rn(lo[(k + u) % R], hi[(k - u + R) % R]), wj, acc[k]);
-        lo[u % R] = v(i0 + R - h + tt);
-        hi[(R - 1 - u) % R] = v(i0 + h - tt - 1);
+        const float xl = __ldg(plo), xh = __ldg(phi);
+        mx = fmaxf(mx, fmaxf(fabsf(xl), fabsf(xh)));
+        lo[u % R] = (double)xl;
+        hi[(R - 1 - u) % R] = (double)xh;
+        plo += in_stride;
+        phi -= in_stride;
       }
+      pw -= R;
     }
 #pragma unroll
     for (int u = 0; u < R; u++) {
       if (u < rem) {
-        const int tt = nblk * R + u;
-        const double wj = __ldg(w + (h - tt));
+        const double wj = __ldg(pw - u);
 #pragma unroll
         for (int k = 0; k < R; k++) acc[k] = fma(__dadd_rn(lo[(k + u) % R], hi[(k - u + R) % R]), wj, acc[k]);
-        lo[u % R] = v(i0 + R - h + tt);
-        hi[(R - 1 - u) % R] = v(i0 + h - tt - 1);
+        const float xl = __ldg(plo), xh = __ldg(phi);
+        mx = fmaxf(mx, fmaxf(fabsf(xl), fabsf(xh)));
+        lo[u % R] = (double)xl;
+        hi[(R - 1 - u) % R] = (double)xh;
+        plo += in_stride;
+        phi -= in_stride;
       }
     }
     const double B = bscale * (double)mx;
-    float* oline = out + base;
 #pragma unroll
     for (int k = 0; k < R; k++) {
       const int i = i0 + k;
       if (i < n) {
         const float a = __double2float_rn(__dsub_rn(acc[k], B));
-        const float b = __double2float_rn(__dadd_rn(acc[k], B));
+        const float bb = __double2float_rn(__dadd_rn(acc[k], B));
         float r = __double2float_rn(acc[k]);
-        if (a != b) {
+        const long long o = out_base + (long long)i * out_stride;
+        if (a != bb) {
           const int slot = atomicAdd(fb, 1);
-          if (slot < fb_cap) fb[FB_HEADER + slot] = (int)(base + (long long)i * stride);
+          if (slot < fb_cap) fb[FB_HEADER + slot] = (int)(AXIS == 0 ? (long long)i * WS + in_base : o);
         }
-        if (EPI == 1) {
-          const long long cell = AXIS == 0 ? (long long)i * W + in_idx / S : outer * W + i;
-          r = __fdiv_rn(r, den32[cell]);
-        }
-        oline[(long long)i * stride] = r;
+        if (EPI == 1) r = __fdiv_rn(r, den32[cellbase + i]);
+        out[o] = r;
       }
     }
   }
 }
 
-// exact SciPy fold for the listed elements (or all elements after an overflow)
-template <typename Tin, int EPI, int AXIS>
-__global__ void blur_fallback_kernel(const Tin* __restrict__ in, float* __restrict__ out, int H, int W,
-                                     int C, int S, BlurLevelRef lvl, const float* __restrict__ den32,
-                                     int* __restrict__ fb, int fb_cap) {
+// exact SciPy fold for the listed elements (or every element after an overflow).
+// List entries: AXIS 0 -> feat-interior offset (y*W*S + x*S + c);
+//               AXIS 1 -> target offset (same layout).
+template <int AXIS, int EPI>
+__global__ void blur_pad_fallback_kernel(const float* __restrict__ in, float* __restrict__ out, PadGeom pg,
+                                         BlurLevelRef lvl, const float* __restrict__ den32,
+                                         int* __restrict__ fb, int fb_cap) {
   int h;
   const double* w;
   lvl.get(&h, &w);
   const int count = *(volatile int*)fb;
-  const bool all = count > fb_cap;
+  const int H = pg.H, W = pg.W, C = pg.C, S = pg.S;
   const long long WS = (long long)W * S;
+  const long long WSP = (long long)(W + 2 * pg.pad) * S;
+  const bool all = count > fb_cap;
   const long long total = all ? (long long)H * WS : count;
-  const int n = AXIS == 0 ? H : W;
-  const long long stride = AXIS == 0 ? WS : (long long)S;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long o = all ? e : (long long)fb[FB_HEADER + e];
     const int c = (int)(o % S);
     if (c >= C) continue;
+    const long long y = o / WS;
+    const int x = (int)((o - y * WS) / S);
+    const float* line;
+    long long stride, oo;
     int i;
-    long long base, cell;
     if (AXIS == 0) {
-      i = (int)(o / WS);
-      base = o - (long long)i * WS;
-      cell = (long long)i * W + base / S;
+      line = in + (long long)x * S + c;  // column (x, c) of feat
+      stride = WS;
+      i = (int)y;
+      oo = y * WSP + (long long)x * S + c;  // tmp interior
     } else {
-      const long long y = o / WS;
-      i = (int)((o - y * WS) / S);
-      base = o - (long long)i * S;
-      cell = y * W + i;
+      line = in + y * WSP + c;  // row y of tmp
+      stride = S;
+      i = x;
+      oo = o;
     }
-    const Tin* line = in + base;
-    auto v = [&](int k) -> double { return (k >= 0 && k < n) ? (double)__ldg(line + (long long)k * stride) : 0.0; };
-    double acc = __dmul_rn(v(i), __ldg(w));
-    for (int j = h; j >= 1; j--) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(v(i - j), v(i + j)), __ldg(w + j)));
+    double acc = __dmul_rn((double)__ldg(line + (long long)i * stride), __ldg(w));
+    for (int j = h; j >= 1; j--)
+      acc = __dadd_rn(acc, __dmul_rn(__dadd_rn((double)__ldg(line + (long long)(i - j) * stride),
+                                               (double)__ldg(line + (long long)(i + j) * stride)),
+                                     __ldg(w + j)));
     float r = __double2float_rn(acc);
-    if (EPI == 1) r = __fdiv_rn(r, den32[cell]);
-    out[o] = r;
+    if (EPI == 1) r = __fdiv_rn(r, den32[y * W + x]);
+    out[oo] = r;
   }
-  __syncthreads();
 }
 
-// resets the fallback counter after the fallback kernel consumed it
+// clears the fallback counter (runs after the fallback kernel)
 __global__ void fb_reset_kernel(int* fb) {
   if (threadIdx.x == 0 && blockIdx.x == 0) fb[0] = 0;
 }
-
-#ifndef PLAS_NO_HOST_LAUNCHERS
-template <typename Tin, typename Tout, int EPI>
-inline void launch_blur_fast(int axis, const Tin* in, float* out, int H, int W, int C, int S,
-                             BlurLevelRef lvl, const float* den32, int* fb, int sms, int fb_cap_in,
-                             cudaStream_t st = 0) {
-  constexpr int R = BLUR_R;
-  const int fb_cap = fb_cap_in > 0 ? fb_cap_in : (int)std::min<long long>((long long)H * W * S / 16, 1 << 26);
-  const int grid = sms * 6;
-  if (axis == 0) {
-    blur_fast_kernel<Tin, EPI, 0, R><<<grid, 256, 0, st>>>(in, out, H, W, C, S, lvl, den32, fb, fb_cap);
-    blur_fallback_kernel<Tin, EPI, 0><<<sms * 4, 256, 0, st>>>(in, out, H, W, C, S, lvl, den32, fb, fb_cap);
-  } else {
-    blur_fast_kernel<Tin, EPI, 1, R><<<grid, 256, 0, st>>>(in, out, H, W, C, S, lvl, den32, fb, fb_cap);
-    blur_fallback_kernel<Tin, EPI, 1><<<sms * 4, 256, 0, st>>>(in, out, H, W, C, S, lvl, den32, fb, fb_cap);
-  }
-}
-#endif
 
 }  // namespace plas

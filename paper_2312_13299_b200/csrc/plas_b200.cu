@@ -27,6 +27,7 @@
 #include "../../include/plas_b200.h"
 #include "assign.cuh"
 #include "blur.cuh"
+#include "blur_fast.cuh"
 #include "common.cuh"
 #include "control.cuh"
 #include "host_rng.h"
@@ -151,7 +152,13 @@ void build_schedule(const plas_sort_args* a, int side, Schedule* s) {
 // ---------------------------------------------------------------- workspace
 struct SortWs {
   Ctrl* ctrl;
-  float *feat, *target, *tmp, *den32;
+  float *feat, *target, *tmp, *den32;  // feat / tmp point at the interior of zero-padded buffers
+  float *feat_alloc, *tmp_alloc;
+  size_t feat_alloc_floats, tmp_alloc_floats;
+  int* fb0;  // blur fallback lists (axis 0 / axis 1)
+  int* fb1;
+  int fb_cap;
+  int pad;
   double* dcache;  // per-cell fp64 distance to the target (level start + pass updates)
   int* idx;
   double* rowweight;
@@ -171,14 +178,26 @@ struct SortWs {
   double* spart;  // statistic-kernel partials
 };
 
+// zero halo of the padded blur buffers: the largest half-width plus one chunk
+int blur_pad(int side) { return (int)ceil(std::max(side / 2.0 - 1.0, 2.0)) + BLUR_R + 1; }
+
 size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long long tcap,
                   int rng_mode, int side, long long list_cap, SortWs* w) {
   Carver c{base};
   const int S = row_stride(dim);
+  const int P = blur_pad(side);
+  w->pad = P;
   w->ctrl = c.take<Ctrl>(1);
-  w->feat = c.take<float>((size_t)n * S);
+  w->feat_alloc_floats = (size_t)(side + 2 * P) * side * S;
+  w->feat_alloc = c.take<float>(w->feat_alloc_floats);
+  w->feat = w->feat_alloc ? w->feat_alloc + (size_t)P * side * S : nullptr;
   w->target = c.take<float>((size_t)n * S);
-  w->tmp = c.take<float>((size_t)n * S);
+  w->tmp_alloc_floats = (size_t)side * (side + 2 * P) * S;
+  w->tmp_alloc = c.take<float>(w->tmp_alloc_floats);
+  w->tmp = w->tmp_alloc ? w->tmp_alloc + (size_t)P * S : nullptr;
+  w->fb_cap = (int)std::min<long long>(n * S / 8 + 1024, 1LL << 26);
+  w->fb0 = c.take<int>((size_t)FB_HEADER + w->fb_cap);
+  w->fb1 = c.take<int>((size_t)FB_HEADER + w->fb_cap);
   w->den32 = c.take<float>((size_t)n);
   w->dcache = c.take<double>((size_t)n);
   w->idx = c.take<int>((size_t)n);
@@ -238,7 +257,8 @@ cudaError_t add_while(cudaGraphNode_t* out, cudaGraph_t g, const cudaGraphNode_t
 struct Launch {
   int S, D, side;
   long long n;
-  int blur_grid, den_grid, rows_grid, dist_grid, pass_grid, tile_grid, vad_grid;
+  int blur_grid, fb_grid, den_grid, rows_grid, dist_grid, pass_grid, tile_grid, vad_grid;
+  PadGeom pg;
   BlurLevelRef lvl;
   Sched sched;
 };
@@ -388,11 +408,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.key1 = key[1];
   CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
-  // pad channels of target/tmp must read as zero
-  if (S != D) {
-    CK(cudaMemsetAsync(w.target, 0, sizeof(float) * n * S, st));
-    CK(cudaMemsetAsync(w.tmp, 0, sizeof(float) * n * S, st));
-  }
+  // zero halos of the padded blur buffers, pad channels, fallback counters
+  CK(cudaMemsetAsync(w.feat_alloc, 0, sizeof(float) * w.feat_alloc_floats, st));
+  CK(cudaMemsetAsync(w.tmp_alloc, 0, sizeof(float) * w.tmp_alloc_floats, st));
+  CK(cudaMemsetAsync(w.target, 0, sizeof(float) * n * S, st));
+  CK(cudaMemsetAsync(w.fb0, 0, sizeof(int) * FB_HEADER, st));
+  CK(cudaMemsetAsync(w.fb1, 0, sizeof(int) * FB_HEADER, st));
 
   // ---- initial permutation (plas.py:241)
   host::NumpyPhilox rng;
@@ -442,6 +463,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.n = n;
   lc.blur_grid = grid_for((long long)side * S * ((side + BLUR_R - 1) / BLUR_R), 256, 8);
   lc.den_grid = grid_for((long long)side * ((side + 1) / 2), 256, 8);
+  lc.fb_grid = num_sms() * 2;
+  lc.pg = PadGeom{side, side, D, S, w.pad};
   lc.rows_grid = grid_for(side, 128, 1);
   lc.dist_grid = grid_for(n, RED_THREADS, 4);
   lc.vad_grid = grid_for(n * D, RED_THREADS, 4);
@@ -486,11 +509,16 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                   w.rowweight, side, lc.lvl));
     CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight_kernel, dim3(lc.den_grid), dim3(256),
                   (const double*)w.rowweight, w.den32, (double*)nullptr, side, side, lc.lvl));
-    CK(add_kernel(&nd[3], obody, &nd[2], 1, blur_axis_kernel<float, float, 0, 0>, dim3(lc.blur_grid),
-                  dim3(256), (const float*)w.feat, w.tmp, side, side, D, S, lc.lvl, (const void*)nullptr));
-    CK(add_kernel(&nd[4], obody, &nd[3], 1, blur_axis_kernel<float, float, 1, 1>, dim3(lc.blur_grid),
-                  dim3(256), (const float*)w.tmp, w.target, side, side, D, S, lc.lvl,
-                  (const void*)w.den32));
+    cudaGraphNode_t bn[4];
+    CK(add_kernel(&bn[0], obody, &nd[2], 1, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
+                  (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
+    CK(add_kernel(&bn[1], obody, &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
+                  (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
+    CK(add_kernel(&bn[2], obody, &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
+                  (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
+    CK(add_kernel(&bn[3], obody, &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
+                  (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
+    nd[4] = bn[3];
     CK(add_kernel(&nd[5], obody, &nd[4], 1, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
                   w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
                   w.spart, done, (unsigned long long)inner_h, (unsigned long long)tile_h));
@@ -599,12 +627,16 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         border_weight_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.den32, nullptr, side, side, lc.lvl);
       });
       timed(K_BLUR0, [&] {
-        blur_axis_kernel<float, float, 0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, side, side, D, S,
-                                                                            lc.lvl, nullptr);
+        blur_pad_kernel<0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0, w.fb_cap,
+                                                            w.fb1);
+        blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
+                                                                   w.fb_cap);
       });
       timed(K_BLUR1, [&] {
-        blur_axis_kernel<float, float, 1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, side, side, D,
-                                                                            S, lc.lvl, w.den32);
+        blur_pad_kernel<1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+                                                            w.fb_cap, w.fb0);
+        blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+                                                                   w.fb_cap);
       });
       timed(K_DIST, [&] {
         level_stats_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, n,

@@ -64,6 +64,7 @@ def line_map(lib, mangled_hint):
             funcs[cur][int(m.group(1), 16)] = (inner, own)
             fresh = True
     cands = [f for f in funcs if all(h in f for h in mangled_hint)]
+    cands.sort(key=len)
     return funcs, cands
 
 
@@ -93,7 +94,8 @@ def main():
         tot_s += s
     tot_e = sum(v[1] for v in agg.values())
     print(f"function {cands[0]}  samples {tot_s}  warp-instructions {tot_e}")
-    for loc, (s, e, n) in sorted(agg.items(), key=lambda x: -x[1][0])[:40]:
+    limit = int(os.environ.get("NCU_LINES_TOP", "40"))
+    for loc, (s, e, n) in sorted(agg.items(), key=lambda x: -x[1][0])[:limit]:
         print(f"{100 * s / max(tot_s, 1):5.1f}% samples {100 * e / max(tot_e, 1):5.1f}% instr  {n:4d} sass  {loc[0]}:{loc[1]}")
 
 
