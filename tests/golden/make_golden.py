@@ -8,7 +8,7 @@ small fixtures under tests/golden/ that the CPU oracle tests and the GPU parity
 tests compare against.
 
 Usage:  python tests/golden/make_golden.py PART [PART ...]
-PART in: versions rng blur assign metrics smooth sort_small c0 c1 c2 paired_c0 paired_c1
+PART in: versions rng blur assign metrics smooth sort_small c0 c1 c2 paired_null_c0 paired_null_c1
 """
 
 import hashlib
@@ -318,26 +318,79 @@ def part_c2():
     print("c2", d["reorders"], d["time_s"], d["nbr_l2"], flush=True)
 
 
-def part_paired_c0():
-    """Reference nbr-L2 per seed at configs[0] for the paired DEVICE-mode protocol."""
-    features = synthetic.c0(0)
-    rows = []
-    for seed in range(int(os.environ.get("PAIRED_C0", "80"))):
-        _, d = sort_case(features, {"rng_seed": seed, "radius_decay": 0.5, "improvement_threshold": 1e-5})
-        rows.append({"seed": seed, "nbr_l2": d["nbr_l2"], "reorders": d["reorders"], "final_vad": d["final_vad"]})
-    with open(out("paired_c0.json"), "w") as f:
-        json.dump(rows, f)
+class _SplitStreamGenerator:
+    """Generator stand-in for the null arm of the paired protocol: the first
+    permutation(n) (draw #1, plas.py:241) comes from Generator(Philox(seed)),
+    every later draw (plas.py:260-262) from the independent Generator(Philox(seed + offset))."""
+
+    def __init__(self, seed, offset):
+        self._init = np.random.Generator(np.random.Philox(seed))
+        self._pass = np.random.Generator(np.random.Philox(seed + offset))
+        self._first = True
+
+    def permutation(self, n):
+        if self._first:
+            self._first = False
+            return self._init.permutation(n)
+        return self._pass.permutation(n)
+
+    def integers(self, *a, **k):
+        return self._pass.integers(*a, **k)
 
 
-def part_paired_c1():
-    features = synthetic.c1(0)
+class _NumpyShim:
+    def __init__(self, seed, offset):
+        import types
+        self.random = types.SimpleNamespace(
+            Generator=lambda bitgen: _SplitStreamGenerator(seed, offset), Philox=lambda s: None)
+
+    def __getattr__(self, name):
+        return getattr(np, name)
+
+
+def _null_run(args):
+    """One reference sort (the unmodified sogs code path) with draw #1 from `seed`
+    and every pass draw from an independent stream `seed + offset`."""
+    features, cfg_kw, seed, offset = args
+    ref_plas.np = _NumpyShim(seed, offset)
+    try:
+        perm, _ = ref_plas.sort_grid_report(features, ref_plas.SortConfig(rng_seed=seed, **cfg_kw), threads=1)
+    finally:
+        ref_plas.np = np
+    side = int(round(len(perm) ** 0.5))
+    return synthetic.neighbour_l2(np.asarray(features, dtype=np.float64)[perm].reshape(side, side, -1))
+
+
+def _own_run(args):
+    features, cfg_kw, seed = args
+    _, d = sort_case(features, dict(cfg_kw, rng_seed=seed))
+    return d["nbr_l2"]
+
+
+def _paired_null(name, features, cfg_kw, seeds, offsets=(1000, 2000)):
+    """Reference runs per seed for the paired DEVICE-mode protocol:
+    `ref` = the reference's own stream; `null` = reference-law runs that share only
+    the initial permutation (the noise floor an equal-in-law stream must match)."""
+    from multiprocessing import Pool
+    sort_case(np.random.default_rng(0).random((64, 3)), {})  # numba JIT before the workers fork
+    with Pool(os.cpu_count()) as pool:
+        own = pool.map(_own_run, [(features, cfg_kw, s) for s in seeds])
+        nulls = pool.map(_null_run, [(features, cfg_kw, s, o) for s in seeds for o in offsets])
     rows = []
-    for seed in range(int(os.environ.get("PAIRED_C1", "16"))):
-        _, d = sort_case(features, {"rng_seed": seed})
-        rows.append({"seed": seed, "nbr_l2": d["nbr_l2"], "reorders": d["reorders"], "final_vad": d["final_vad"]})
-        print("paired_c1", seed, d["nbr_l2"], flush=True)
-    with open(out("paired_c1.json"), "w") as f:
-        json.dump(rows, f)
+    for i, s in enumerate(seeds):
+        rows.append({"seed": s, "nbr_l2": own[i], "null_offsets": list(offsets),
+                     "null_nbr_l2": nulls[i * len(offsets):(i + 1) * len(offsets)]})
+    with open(out(name), "w") as f:
+        json.dump({"cfg": cfg_kw, "rows": rows}, f)
+
+
+def part_paired_null_c0():
+    _paired_null("paired_null_c0.json", synthetic.c0(0), {"radius_decay": 0.5, "improvement_threshold": 1e-5},
+                 list(range(int(os.environ.get("PAIRED_C0", "80")))))
+
+
+def part_paired_null_c1():
+    _paired_null("paired_null_c1.json", synthetic.c1(0), {}, list(range(int(os.environ.get("PAIRED_C1", "32")))))
 
 
 PARTS = {k[5:]: v for k, v in globals().items() if k.startswith("part_")}

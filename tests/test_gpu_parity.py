@@ -320,30 +320,41 @@ def test_device_mode_valid_and_deterministic():
     assert not np.array_equal(p1, p3)
 
 
-def _paired(config_name, feats, rows, cfg_kw):
-    rel = []
-    for row in rows:
+def _paired(config_name, fixture):
+    """SURVEY 8(d) paired protocol.  Per seed s the DEVICE-mode sort starts from the
+    reference's own initial permutation (draw #1 of Generator(Philox(s)), plas.py:241)
+    and draws every pass on the GPU.  Two comparisons, both |mean| + 2 SE <= 0.5%:
+      * vs `null`: reference-law runs (the unmodified reference code path) that share
+        only the initial permutation and take their pass draws from independent
+        streams -- the test of "equal in law" (the reference's own runs carry a noise
+        component shared by every arm, which the null arm cancels);
+      * vs `ref`: the reference's own runs (BASELINE north_star: smoothness within 0.5%).
+    """
+    d = golden_json(fixture)
+    feats = synthetic.c0(0) if config_name == "C0" else synthetic.c1(0)
+    side = math.isqrt(len(feats))
+    ours = []
+    for row in d["rows"]:
         seed = row["seed"]
         init = np.random.Generator(np.random.Philox(seed)).permutation(len(feats))
-        perm, _ = plas.plas._sort(feats, plas.SortConfig(rng_seed=seed, rng_mode="device", **cfg_kw), 1,
+        perm, _ = plas.plas._sort(feats, plas.SortConfig(rng_seed=seed, rng_mode="device", **d["cfg"]), 1,
                                   initial_perm=init)
-        side = math.isqrt(len(feats))
-        nl = synthetic.neighbour_l2(feats[perm].reshape(side, side, -1))
-        rel.append(nl / row["nbr_l2"] - 1.0)
-    rel = np.array(rel)
-    mean, se = rel.mean(), rel.std(ddof=1) / math.sqrt(len(rel))
-    print(f"{config_name}: paired rel diff {100 * mean:+.3f}% +- {100 * se:.3f}% (n={len(rel)})")
-    return mean, se
+        assert sorted(perm.tolist()) == list(range(len(feats)))
+        ours.append(synthetic.neighbour_l2(feats[perm].reshape(side, side, -1)))
+    ours = np.array(ours)
+    ref = np.array([r["nbr_l2"] for r in d["rows"]])
+    null = np.array([np.mean(r["null_nbr_l2"]) for r in d["rows"]])
+    out = {}
+    for name, base in (("null", null), ("ref", ref)):
+        rel = ours / base - 1.0
+        out[name] = (rel.mean(), rel.std(ddof=1) / math.sqrt(len(rel)))
+        print(f"{config_name}: paired rel diff vs {name} {100 * out[name][0]:+.3f}% +- "
+              f"{100 * out[name][1]:.3f}% (n={len(rel)})")
+    return out
 
 
-def test_device_mode_paired_protocol_c0():
-    """|mean| + 2 SE <= 0.5% on the paired nbr-L2 difference (80 seeds)."""
-    rows = golden_json("paired_c0.json")
-    mean, se = _paired("C0", synthetic.c0(0), rows, {"radius_decay": 0.5, "improvement_threshold": 1e-5})
-    assert abs(mean) + 2 * se <= 0.005
-
-
-def test_device_mode_paired_protocol_c1():
-    rows = golden_json("paired_c1.json")
-    mean, se = _paired("C1", synthetic.c1(0), rows, {})
-    assert abs(mean) + 2 * se <= 0.005
+@pytest.mark.parametrize("config_name,fixture", [("C0", "paired_null_c0.json"), ("C1", "paired_null_c1.json")])
+def test_device_mode_paired_protocol(config_name, fixture):
+    res = _paired(config_name, fixture)
+    for name, (mean, se) in res.items():
+        assert abs(mean) + 2 * se <= 0.005, (name, mean, se)
