@@ -136,6 +136,17 @@ size_t plas_aux_workspace_bytes(int H, int W, int C);
 int plas_blur(const void* in, void* out, int dtype, int H, int W, int C, const double* weights,
               int half_width, int op, void* ws, size_t ws_bytes, void* stream);
 
+/* blur_target (plas.py:64-68) of an (H, W, C) f32 grid through the SORT's
+ * level-blur tiers: tier 0 = direct fast fold, tier 1 = FFT convolution; both
+ * certify every output against the SciPy fold and recompute the uncertain
+ * ones exactly, so the result is bit-identical to the reference.  weights:
+ * host [half_width + 1], centre first.  fallbacks: optional host [2] out, the
+ * outputs recomputed by the exact fold per axis.  Synchronises the stream. */
+size_t plas_blur_tiers_workspace_bytes(int H, int W, int C, int half_width);
+int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, const double* weights,
+                           int half_width, int tier, int64_t* fallbacks, void* ws, size_t ws_bytes,
+                           void* stream);
+
 /* grid_distance (plas.py:71-84): fp64 (n, dim) inputs, optional device
  * weights [dim]; result written to *out_dev (device double). */
 int plas_grid_distance(const double* a, const double* b, const double* weights, int64_t n, int dim,

@@ -73,3 +73,28 @@ def renormalized_blur(grid, sigma, radius):
     if radius < 1:
         raise ValueError("radius must be >= 1")
     return _run(grid, sigma, radius, _lib.PLAS_BLUR_RENORMALIZED)
+
+
+def blur_target_tiers(grid, radius, tier):
+    """blur_target (plas.py:64-68) of a float32 (H, W, C) grid through the sort's
+    level-blur tiers (tier 0: direct fast fold, 1: FFT), each certified against the
+    SciPy fold with exact recomputation of uncertain outputs.  Returns
+    (target, (fallbacks axis 0, fallbacks axis 1)).  Test / diagnostics entry."""
+    import math
+
+    import torch
+    L = _lib.lib()
+    a = np.ascontiguousarray(np.asarray(grid, dtype=np.float32))
+    shape = a.shape
+    H, W = shape[0], shape[1]
+    C = int(np.prod(shape[2:])) if len(shape) > 2 else 1
+    h = int(math.ceil(radius))
+    w = gaussian_weights(radius / 2.0, h)
+    g = torch.from_numpy(a).cuda()
+    out = torch.empty_like(g)
+    ws = _lib.workspace(L.plas_blur_tiers_workspace_bytes(H, W, C, h), "tiers")
+    fb = np.zeros(2, dtype=np.int64)
+    _lib.check(L.plas_blur_target_tiers(_lib.ptr(g), _lib.ptr(out), H, W, C, _lib.ptr(w), h, int(tier),
+                                        _lib.ptr(fb), _lib.ptr(ws), ws.numel(), _lib.stream_handle()),
+               "blur_target_tiers")
+    return out.cpu().numpy().reshape(shape), (int(fb[0]), int(fb[1]))

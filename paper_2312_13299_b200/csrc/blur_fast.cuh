@@ -24,6 +24,24 @@ namespace plas {
 
 constexpr int FB_HEADER = 16;  // ints before the list: [0] count
 
+// Append `entry` to the fallback list when `need` (warp-aggregated: one atomic
+// per warp and call).  Every lane of the warp must call it (the caller's
+// branches must be warp-uniform or the lanes inactive for good).
+__device__ __forceinline__ void fb_append(bool need, int entry, int* __restrict__ fb, int fb_cap) {
+  const unsigned active = __activemask();
+  const unsigned bal = __ballot_sync(active, need);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(bal) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(fb, __popc(bal));
+  base = __shfl_sync(active, base, leader);
+  if (need) {
+    const int slot = base + __popc(bal & ((1u << lane) - 1u));
+    if (slot < fb_cap) fb[FB_HEADER + slot] = entry;
+  }
+}
+
 struct PadGeom {
   int H, W, C, S;
   int pad;        // zero elements before/after every line (>= hmax + BLUR_R)
@@ -140,10 +158,7 @@ __global__ void __launch_bounds__(256, 3) blur_pad_kernel(const float* __restric
         const float bb = __double2float_rn(__dadd_rn(acc[k], B));
         float r = __double2float_rn(acc[k]);
         const long long o = out_base + (long long)i * out_stride;
-        if (a != bb) {
-          const int slot = atomicAdd(fb, 1);
-          if (slot < fb_cap) fb[FB_HEADER + slot] = (int)(AXIS == 0 ? (long long)i * WS + in_base : o);
-        }
+        fb_append(a != bb, (int)(AXIS == 0 ? (long long)i * WS + in_base : o), fb, fb_cap);
         if (EPI == 1) r = __fdiv_rn(r, den32[cellbase + i]);
         out[o] = r;
       }
@@ -154,10 +169,18 @@ __global__ void __launch_bounds__(256, 3) blur_pad_kernel(const float* __restric
 // exact SciPy fold for the listed elements (or every element after an overflow).
 // List entries: AXIS 0 -> feat-interior offset (y*W*S + x*S + c);
 //               AXIS 1 -> target offset (same layout).
+// One warp per element: the lanes form the tap terms
+// p_j = RN(RN(x[i-j] + x[i+j]) * w_j) in parallel (they do not depend on the
+// running sum) into shared memory, then lane 0 adds them in SciPy's order
+// j = h .. 1 onto acc = RN(x[i] w_0) -- the same roundings as the reference.
+constexpr int FB_CHUNK = 256;
+constexpr int FB_WARPS = 8;
+
 template <int AXIS, int EPI>
-__global__ void blur_pad_fallback_kernel(const float* __restrict__ in, float* __restrict__ out, PadGeom pg,
-                                         BlurLevelRef lvl, const float* __restrict__ den32,
-                                         int* __restrict__ fb, int fb_cap) {
+__global__ void __launch_bounds__(32 * FB_WARPS) blur_pad_fallback_kernel(
+    const float* __restrict__ in, float* __restrict__ out, PadGeom pg, BlurLevelRef lvl,
+    const float* __restrict__ den32, int* __restrict__ fb, int fb_cap) {
+  __shared__ double terms[FB_WARPS][FB_CHUNK];
   int h;
   const double* w;
   lvl.get(&h, &w);
@@ -167,11 +190,12 @@ __global__ void blur_pad_fallback_kernel(const float* __restrict__ in, float* __
   const long long WSP = (long long)(W + 2 * pg.pad) * S;
   const bool all = count > fb_cap;
   const long long total = all ? (long long)H * WS : count;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* tm = terms[wid];
+  for (long long e = (long long)blockIdx.x * FB_WARPS + wid; e < total; e += (long long)gridDim.x * FB_WARPS) {
     const long long o = all ? e : (long long)fb[FB_HEADER + e];
     const int c = (int)(o % S);
-    if (c >= C) continue;
+    if (c >= C) continue;  // warp-uniform
     const long long y = o / WS;
     const int x = (int)((o - y * WS) / S);
     const float* line;
@@ -189,13 +213,24 @@ __global__ void blur_pad_fallback_kernel(const float* __restrict__ in, float* __
       oo = o;
     }
     double acc = __dmul_rn((double)__ldg(line + (long long)i * stride), __ldg(w));
-    for (int j = h; j >= 1; j--)
-      acc = __dadd_rn(acc, __dmul_rn(__dadd_rn((double)__ldg(line + (long long)(i - j) * stride),
-                                               (double)__ldg(line + (long long)(i + j) * stride)),
-                                     __ldg(w + j)));
-    float r = __double2float_rn(acc);
-    if (EPI == 1) r = __fdiv_rn(r, den32[y * W + x]);
-    out[oo] = r;
+    for (int j0 = h; j0 >= 1; j0 -= FB_CHUNK) {
+      const int nt = j0 < FB_CHUNK ? j0 : FB_CHUNK;  // taps j0, j0-1, ..., j0-nt+1
+      for (int t = lane; t < nt; t += 32) {
+        const int j = j0 - t;
+        tm[t] = __dmul_rn(__dadd_rn((double)__ldg(line + (long long)(i - j) * stride),
+                                    (double)__ldg(line + (long long)(i + j) * stride)),
+                          __ldg(w + j));
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int t = 0; t < nt; t++) acc = __dadd_rn(acc, tm[t]);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      float r = __double2float_rn(acc);
+      if (EPI == 1) r = __fdiv_rn(r, den32[y * W + x]);
+      out[oo] = r;
+    }
   }
 }
 

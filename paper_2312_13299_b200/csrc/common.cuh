@@ -50,6 +50,8 @@ struct Ctrl {
   long long fallbacks;             // warps that took the exact fp64 decision path
   int S;                           // row stride (floats)
   int tile;                        // this pass runs the shared-memory tile kernel
+  int fft_min_h;                   // levels with h >= fft_min_h (> 0) blur by FFT
+  int fft_L;                       // FFT length (0 = no FFT tier)
 };
 
 // Blocks whose feature + target rows fit in TILE_SMEM_MAX bytes of shared

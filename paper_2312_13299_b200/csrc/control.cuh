@@ -124,11 +124,16 @@ __device__ __forceinline__ void prepare_device_pass(Ctrl* c) {
   set_pass_geometry(c, dy, dx, gk);
 }
 
-__global__ void level_begin_kernel(Ctrl* c, Sched s) {
+__device__ __host__ __forceinline__ bool level_uses_fft(int h, int side, int fft_min_h, int fft_L) {
+  return fft_min_h > 0 && fft_L > 0 && h >= fft_min_h && side + h <= fft_L;
+}
+
+__global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_cond) {
   if (threadIdx.x) return;
   const int lv = c->level;
   c->beta = s.betas[lv];
   c->h = s.hs[lv];
+  set_cond(blur_cond, level_uses_fft(c->h, c->side, c->fft_min_h, c->fft_L) ? 1u : 0u);
   c->pass = 0;
   c->strikes = 0;
   c->level_done = 0;

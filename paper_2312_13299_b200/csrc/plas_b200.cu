@@ -28,6 +28,7 @@
 #include "assign.cuh"
 #include "blur.cuh"
 #include "blur_fast.cuh"
+#include "blur_fft.cuh"
 #include "common.cuh"
 #include "control.cuh"
 #include "host_rng.h"
@@ -176,7 +177,75 @@ struct SortWs {
   long long sel_stride;
   int* list;      // moved-cell list of the current pass
   double* spart;  // statistic-kernel partials
+  double2* fft_tw;   // [fft_L] twiddles (large-radius FFT blur)
+  double* fft_spec;  // [fft_L] spectrum of the current level
+  int fft_L;
 };
+
+// ---------------------------------------------------------------- FFT blur tier
+constexpr int FFT_MIN_LOG2 = 5, FFT_MAX_LOG2 = 13;  // 32 <= L <= 8192 (16 L bytes of shared memory per CTA)
+
+template <int AXIS, int EPI>
+void* fft_kernel_ptr(int log2L) {
+  switch (log2L) {
+    case 5: return (void*)blur_fft_kernel<AXIS, EPI, 5>;
+    case 6: return (void*)blur_fft_kernel<AXIS, EPI, 6>;
+    case 7: return (void*)blur_fft_kernel<AXIS, EPI, 7>;
+    case 8: return (void*)blur_fft_kernel<AXIS, EPI, 8>;
+    case 9: return (void*)blur_fft_kernel<AXIS, EPI, 9>;
+    case 10: return (void*)blur_fft_kernel<AXIS, EPI, 10>;
+    case 11: return (void*)blur_fft_kernel<AXIS, EPI, 11>;
+    case 12: return (void*)blur_fft_kernel<AXIS, EPI, 12>;
+    case 13: return (void*)blur_fft_kernel<AXIS, EPI, 13>;
+  }
+  return nullptr;
+}
+
+int fft_threads(int L) { return L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8); }
+
+int next_log2(long long v) {
+  int k = 0;
+  while ((1LL << k) < v) k++;
+  return k;
+}
+
+// allocation: L = 2^k >= 2 side covers every h <= side; 0 when too long
+int fft_alloc_length(int side) {
+  const int k = std::max(next_log2(2LL * side), FFT_MIN_LOG2);
+  return k <= FFT_MAX_LOG2 ? (1 << k) : 0;
+}
+
+// smallest half-width that takes the FFT tier (0 = never); PLAS_FFT_MIN_H overrides
+int fft_min_h() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PLAS_FFT_MIN_H");
+    v = e ? atoi(e) : 16;
+    if (v < 0) v = 0;
+  }
+  return v;
+}
+
+// relative error constant of the FFT convolution (blur_fft.cuh), x2 safety
+double fft_error_constant(int log2L) {
+  const double u = ldexp(1.0, -53);
+  const double mu = 2.0 * u, g4 = 4.0 * u / (1.0 - 4.0 * u);
+  const double eta = mu + g4 * (sqrt(2.0) + mu);
+  const double k = (double)log2L;
+  const double c = k * eta / (1.0 - k * eta);
+  const double eK = 4.0 * u;
+  const double e2 = (c + u * (1.0 + c)) * (1.0 + eK) + eK;
+  return 2.0 * (c * (1.0 + e2) + e2);
+}
+
+void fft_twiddles(int L, std::vector<double2>* tw) {
+  tw->resize(L);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int t = 0; t < L; t++) {
+    const long double a = -2.0L * pi * (long double)t / (long double)L;
+    (*tw)[t] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+}
 
 // zero halo of the padded blur buffers: the largest half-width plus one chunk
 int blur_pad(int side) { return (int)ceil(std::max(side / 2.0 - 1.0, 2.0)) + BLUR_R + 1; }
@@ -218,6 +287,9 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->sel = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(9 * b0 * b0) : 1);
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS);
+  w->fft_L = fft_alloc_length(side);
+  w->fft_tw = c.take<double2>((size_t)std::max(w->fft_L, 1));
+  w->fft_spec = c.take<double>((size_t)std::max(w->fft_L, 1));
   return align_up(c.off);
 }
 
@@ -406,6 +478,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   host::seed_key(a->seed, key);
   hc.key0 = key[0];
   hc.key1 = key[1];
+  hc.fft_min_h = fft_min_h();
+  hc.fft_L = w.fft_L;
   CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
   // zero halos of the padded blur buffers, pad channels, fallback counters
@@ -414,6 +488,11 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   CK(cudaMemsetAsync(w.target, 0, sizeof(float) * n * S, st));
   CK(cudaMemsetAsync(w.fb0, 0, sizeof(int) * FB_HEADER, st));
   CK(cudaMemsetAsync(w.fb1, 0, sizeof(int) * FB_HEADER, st));
+  std::vector<double2> htw;
+  if (w.fft_L) {
+    fft_twiddles(w.fft_L, &htw);
+    CK(cudaMemcpyAsync(w.fft_tw, htw.data(), sizeof(double2) * w.fft_L, cudaMemcpyHostToDevice, st));
+  }
 
   // ---- initial permutation (plas.py:241)
   host::NumpyPhilox rng;
@@ -471,6 +550,21 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.pass_grid = pass_grid_size(S);
   lc.tile_grid = tile_grid_size(S);
   lc.lvl = BlurLevelRef{w.ctrl, w.hs, w.weights, w.woff, 0, nullptr};
+  const int fft_log2 = w.fft_L ? next_log2(w.fft_L) : 0;
+  const FftPlan fplan{fft_log2, w.fft_L, w.fft_tw, w.fft_spec, w.fft_L ? fft_error_constant(fft_log2) : 0.0};
+  const int fft_nthreads = w.fft_L ? fft_threads(w.fft_L) : 32;
+  void* fft0 = w.fft_L ? fft_kernel_ptr<0, 0>(fft_log2) : nullptr;
+  void* fft1 = w.fft_L ? fft_kernel_ptr<1, 1>(fft_log2) : nullptr;
+  const size_t fft_smem = (sizeof(double2) + sizeof(float)) * (size_t)w.fft_L;  // line pair + raw inputs (2 n <= L floats)
+  int fft_grid = 1;
+  if (w.fft_L) {
+    CK(cudaFuncSetAttribute(fft0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
+    CK(cudaFuncSetAttribute(fft1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft0, fft_nthreads, fft_smem));
+    fft_grid = side * ((D + 1) / 2);  // one CTA per line pair
+  }
+  const int spec_grid = std::max(1, w.fft_L / 128);
   lc.sched = Sched{w.radii, w.betas, w.hs, w.level_counts, w.trace};
 
   auto vad_launch = [&](double* out) -> int {
@@ -503,22 +597,73 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(add_while(&outer_node, g, nullptr, 0, outer_h, &obody));
     CK(cudaGraphConditionalHandleCreate(&inner_h, obody, 0, 0));
     CK(cudaGraphConditionalHandleCreate(&tile_h, obody, 0, 0));
+    cudaGraphConditionalHandle blur_h;
+    CK(cudaGraphConditionalHandleCreate(&blur_h, obody, 0, 0));
     cudaGraphNode_t nd[8];
-    CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched));
+    CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
+                  (unsigned long long)blur_h));
     CK(add_kernel(&nd[1], obody, &nd[0], 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
                   w.rowweight, side, lc.lvl));
     CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight_kernel, dim3(lc.den_grid), dim3(256),
                   (const double*)w.rowweight, w.den32, (double*)nullptr, side, side, lc.lvl));
-    cudaGraphNode_t bn[4];
-    CK(add_kernel(&bn[0], obody, &nd[2], 1, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
-                  (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
-    CK(add_kernel(&bn[1], obody, &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
-                  (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
-    CK(add_kernel(&bn[2], obody, &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
-                  (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
-    CK(add_kernel(&bn[3], obody, &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
-                  (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
-    nd[4] = bn[3];
+    // IF (FFT tier this level) { spectrum, fft axis 0, fallback 0, fft axis 1, fallback 1 }
+    // ELSE { direct fold axis 0, fallback 0, axis 1, fallback 1 }
+    cudaGraphNode_t blur_if;
+    cudaGraph_t bbody[2];
+    {
+      cudaGraphNodeParams p{};
+      p.type = cudaGraphNodeTypeConditional;
+      p.conditional.handle = blur_h;
+      p.conditional.type = cudaGraphCondTypeIf;
+      p.conditional.size = 2;
+      CK(cudaGraphAddNode(&blur_if, obody, &nd[2], 1, &p));
+      bbody[0] = p.conditional.phGraph_out[0];
+      bbody[1] = p.conditional.phGraph_out[1];
+    }
+    {
+      cudaGraphNode_t fn[5];
+      CK(add_kernel(&fn[0], bbody[0], nullptr, 0, fft_spectrum_kernel, dim3(spec_grid), dim3(128), lc.lvl, fplan));
+      {
+        const float* in0 = w.feat;
+        float* out0 = w.tmp;
+        const float* dnull = nullptr;
+        int* fb0 = w.fb0;
+        int* fb1 = w.fb1;
+        int cap = w.fb_cap;
+        PadGeom pg = lc.pg;
+        BlurLevelRef lv = lc.lvl;
+        FftPlan pl = fplan;
+        void* a0[] = {&in0, &out0, &pg, &lv, &pl, &dnull, &fb0, &cap, &fb1};
+        cudaKernelNodeParams kp{};
+        kp.func = fft0;
+        kp.gridDim = dim3(fft_grid);
+        kp.blockDim = dim3(fft_nthreads);
+        kp.sharedMemBytes = (unsigned)fft_smem;
+        kp.kernelParams = a0;
+        CK(cudaGraphAddKernelNode(&fn[1], bbody[0], &fn[0], 1, &kp));
+        CK(add_kernel(&fn[2], bbody[0], &fn[1], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
+                      (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
+        const float* in1 = w.tmp;
+        float* out1 = w.target;
+        const float* den = w.den32;
+        void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &fb1, &cap, &fb0};
+        kp.func = fft1;
+        kp.kernelParams = a1;
+        CK(cudaGraphAddKernelNode(&fn[3], bbody[0], &fn[2], 1, &kp));
+        CK(add_kernel(&fn[4], bbody[0], &fn[3], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
+                      (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
+      }
+      cudaGraphNode_t bn[4];
+      CK(add_kernel(&bn[0], bbody[1], nullptr, 0, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
+                    (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
+      CK(add_kernel(&bn[1], bbody[1], &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
+                    (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
+      CK(add_kernel(&bn[2], bbody[1], &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
+                    (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
+      CK(add_kernel(&bn[3], bbody[1], &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
+                    (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
+    }
+    nd[4] = blur_if;
     CK(add_kernel(&nd[5], obody, &nd[4], 1, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
                   w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
                   w.spart, done, (unsigned long long)inner_h, (unsigned long long)tile_h));
@@ -621,23 +766,58 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     for (int lv = 0; lv < L; lv++) {
       const int beta = sch.betas[lv];
       const long long bsq = (long long)beta * beta;
-      timed(K_CTRL, [&] { level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched); });
+      timed(K_CTRL, [&] { level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull); });
+      const bool use_fft = level_uses_fft(sch.hs[lv], side, hc.fft_min_h, hc.fft_L);
       timed(K_BORDER, [&] {
         border_rows_kernel<<<lc.rows_grid, 128, 0, st>>>(w.rowweight, side, lc.lvl);
         border_weight_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.den32, nullptr, side, side, lc.lvl);
       });
-      timed(K_BLUR0, [&] {
-        blur_pad_kernel<0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0, w.fb_cap,
-                                                            w.fb1);
-        blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
-                                                                   w.fb_cap);
-      });
-      timed(K_BLUR1, [&] {
-        blur_pad_kernel<1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
-                                                            w.fb_cap, w.fb0);
-        blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
-                                                                   w.fb_cap);
-      });
+      if (use_fft) {
+        timed(K_BLUR0, [&] {
+          fft_spectrum_kernel<<<spec_grid, 128, 0, st>>>(lc.lvl, fplan);
+          {
+            const float* in0 = w.feat;
+            float* out0 = w.tmp;
+            const float* dnull = nullptr;
+            PadGeom pg = lc.pg;
+            BlurLevelRef lv = lc.lvl;
+            FftPlan pl = fplan;
+            int cap = w.fb_cap;
+            void* a0[] = {&in0, &out0, &pg, &lv, &pl, &dnull, &w.fb0, &cap, &w.fb1};
+            cudaLaunchKernel(fft0, dim3(fft_grid), dim3(fft_nthreads), a0, fft_smem, st);
+          }
+          blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
+                                                                     w.fb_cap);
+        });
+        timed(K_BLUR1, [&] {
+          {
+            const float* in1 = w.tmp;
+            float* out1 = w.target;
+            const float* den = w.den32;
+            PadGeom pg = lc.pg;
+            BlurLevelRef lv = lc.lvl;
+            FftPlan pl = fplan;
+            int cap = w.fb_cap;
+            void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &w.fb1, &cap, &w.fb0};
+            cudaLaunchKernel(fft1, dim3(fft_grid), dim3(fft_nthreads), a1, fft_smem, st);
+          }
+          blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+                                                                     w.fb_cap);
+        });
+      } else {
+        timed(K_BLUR0, [&] {
+          blur_pad_kernel<0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0, w.fb_cap,
+                                                              w.fb1);
+          blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
+                                                                     w.fb_cap);
+        });
+        timed(K_BLUR1, [&] {
+          blur_pad_kernel<1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+                                                              w.fb_cap, w.fb0);
+          blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+                                                                     w.fb_cap);
+        });
+      }
       timed(K_DIST, [&] {
         level_stats_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, n,
                                                                  D, S, w.spart, done, 0, 0);
@@ -824,6 +1004,138 @@ static int launch_blur(const void* in, void* out, int dtype, int H, int W, int C
       blur_axis_kernel<double, double, 0, 1><<<grid1, 256, 0, st>>>(tmp, (double*)out, H, W, C, S, lv, nullptr);
   }
   CKL();
+  return PLAS_OK;
+}
+
+// ---- the sort's level blur (fast tiers + exact fallback) on an arbitrary grid
+struct TierWs {
+  float *feat_alloc, *feat, *tmp_alloc, *tmp, *target, *den32;
+  double *rows, *w, *spec;
+  double2* tw;
+  int *fb0, *fb1;
+  int pad, fb_cap, L;
+  size_t feat_floats, tmp_floats;
+};
+
+static size_t carve_tiers(char* base, int H, int W, int C, int h, TierWs* t) {
+  Carver c{base};
+  const int S = row_stride(C);
+  t->pad = h + BLUR_R + 1;
+  t->feat_floats = (size_t)(H + 2 * t->pad) * W * S;
+  t->feat_alloc = c.take<float>(t->feat_floats);
+  t->feat = t->feat_alloc ? t->feat_alloc + (size_t)t->pad * W * S : nullptr;
+  t->tmp_floats = (size_t)H * (W + 2 * t->pad) * S;
+  t->tmp_alloc = c.take<float>(t->tmp_floats);
+  t->tmp = t->tmp_alloc ? t->tmp_alloc + (size_t)t->pad * S : nullptr;
+  t->target = c.take<float>((size_t)H * W * S);
+  t->den32 = c.take<float>((size_t)H * W);
+  t->rows = c.take<double>((size_t)H);
+  t->w = c.take<double>((size_t)h + 1);
+  // FFT length: L >= n + h (linear convolution) and n <= L / 2 (the kernel's raw-line buffer)
+  const int k = std::max(std::max(next_log2((long long)std::max(H, W) + h), next_log2(2LL * std::max(H, W))),
+                         FFT_MIN_LOG2);
+  t->L = k <= FFT_MAX_LOG2 ? 1 << k : 0;
+  t->tw = c.take<double2>((size_t)std::max(t->L, 1));
+  t->spec = c.take<double>((size_t)std::max(t->L, 1));
+  t->fb_cap = (int)std::min<long long>((long long)H * W * S / 8 + 1024, 1LL << 26);
+  t->fb0 = c.take<int>((size_t)FB_HEADER + t->fb_cap);
+  t->fb1 = c.take<int>((size_t)FB_HEADER + t->fb_cap);
+  return align_up(c.off);
+}
+
+__global__ void pad_rows_kernel(const float* __restrict__ in, float* __restrict__ out, long long cells, int C, int S) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cells * S;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long cell = t / S;
+    const int c = (int)(t - cell * S);
+    out[t] = c < C ? in[cell * C + c] : 0.f;
+  }
+}
+
+__global__ void unpad_rows_kernel(const float* __restrict__ in, float* __restrict__ out, long long cells, int C, int S) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < cells * C;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long cell = t / C;
+    const int c = (int)(t - cell * C);
+    out[t] = in[cell * S + c];
+  }
+}
+
+size_t plas_blur_tiers_workspace_bytes(int H, int W, int C, int half_width) {
+  TierWs t;
+  return carve_tiers(nullptr, H, W, C, half_width, &t);
+}
+
+int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, const double* weights, int half_width,
+                           int tier, int64_t* fallbacks, void* ws, size_t ws_bytes, void* stream) {
+  if (H < 1 || W < 1 || C < 1 || half_width < 1 || !weights || tier < 0 || tier > 1)
+    return fail(PLAS_ERR_INVALID, "bad blur tier arguments");
+  TierWs t;
+  if (!ws || ws_bytes < carve_tiers(nullptr, H, W, C, half_width, &t))
+    return fail(PLAS_ERR_WORKSPACE, "tier workspace");
+  carve_tiers((char*)ws, H, W, C, half_width, &t);
+  if (tier == 1 && !t.L) return fail(PLAS_ERR_INVALID, "grid too long for the FFT tier");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = row_stride(C);
+  const long long cells = (long long)H * W;
+  CK(cudaMemsetAsync(t.feat_alloc, 0, sizeof(float) * t.feat_floats, st));
+  CK(cudaMemsetAsync(t.tmp_alloc, 0, sizeof(float) * t.tmp_floats, st));
+  CK(cudaMemsetAsync(t.fb0, 0, sizeof(int) * FB_HEADER, st));
+  CK(cudaMemsetAsync(t.fb1, 0, sizeof(int) * FB_HEADER, st));
+  CK(cudaMemcpyAsync(t.w, weights, sizeof(double) * (half_width + 1), cudaMemcpyHostToDevice, st));
+  pad_rows_kernel<<<grid_for(cells * S, 256, 8), 256, 0, st>>>(in, t.feat, cells, C, S);
+  BlurLevelRef lv{nullptr, nullptr, nullptr, nullptr, half_width, t.w};
+  PadGeom pg{H, W, C, S, t.pad};
+  border_rows_kernel<<<grid_for(H, 128, 1), 128, 0, st>>>(t.rows, H, lv);
+  border_weight_kernel<<<grid_for((long long)H * ((W + 1) / 2), 256, 8), 256, 0, st>>>(t.rows, t.den32, nullptr, H,
+                                                                                        W, lv);
+  const int fbg = num_sms() * 2;
+  int64_t counts[2] = {0, 0};
+  int hc[2];
+  if (tier == 0) {
+    const int g0 = grid_for((long long)W * S * ((H + BLUR_R - 1) / BLUR_R), 256, 8);
+    blur_pad_kernel<0, 0><<<g0, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap, t.fb1);
+    CK(cudaMemcpyAsync(&hc[0], t.fb0, sizeof(int), cudaMemcpyDeviceToHost, st));
+    blur_pad_fallback_kernel<0, 0><<<fbg, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap);
+    blur_pad_kernel<1, 1><<<g0, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap, t.fb0);
+    CK(cudaMemcpyAsync(&hc[1], t.fb1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    blur_pad_fallback_kernel<1, 1><<<fbg, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap);
+  } else {
+    std::vector<double2> htw;
+    fft_twiddles(t.L, &htw);
+    CK(cudaMemcpyAsync(t.tw, htw.data(), sizeof(double2) * t.L, cudaMemcpyHostToDevice, st));
+    const int lg = next_log2(t.L);
+    const FftPlan plan{lg, t.L, t.tw, t.spec, fft_error_constant(lg)};
+    void* f0 = fft_kernel_ptr<0, 0>(lg);
+    void* f1 = fft_kernel_ptr<1, 1>(lg);
+    const size_t smem = (sizeof(double2) + sizeof(float)) * (size_t)t.L;
+    CK(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nt = fft_threads(t.L);
+    fft_spectrum_kernel<<<std::max(1, t.L / 128), 128, 0, st>>>(lv, plan);
+    const float *i0 = t.feat, *i1 = t.tmp, *dn = nullptr, *den = t.den32;
+    float *o0 = t.tmp, *o1 = t.target;
+    int cap = t.fb_cap;
+    void* a0[] = {&i0, &o0, &pg, &lv, (void*)&plan, &dn, &t.fb0, &cap, &t.fb1};
+    void* a1[] = {&i1, &o1, &pg, &lv, (void*)&plan, &den, &t.fb1, &cap, &t.fb0};
+    const int g0 = W * ((C + 1) / 2);  // one CTA per line pair
+    const int g1 = H * ((C + 1) / 2);
+    CK(cudaLaunchKernel(f0, dim3(g0), dim3(nt), a0, smem, st));
+    CK(cudaMemcpyAsync(&hc[0], t.fb0, sizeof(int), cudaMemcpyDeviceToHost, st));
+    blur_pad_fallback_kernel<0, 0><<<fbg, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap);
+    CK(cudaLaunchKernel(f1, dim3(g1), dim3(nt), a1, smem, st));
+    CK(cudaMemcpyAsync(&hc[1], t.fb1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    blur_pad_fallback_kernel<1, 1><<<fbg, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap);
+  }
+  unpad_rows_kernel<<<grid_for(cells * C, 256, 8), 256, 0, st>>>(t.target, out, cells, C, S);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  counts[0] = hc[0];
+  counts[1] = hc[1];
+  if (fallbacks) {
+    fallbacks[0] = counts[0];
+    fallbacks[1] = counts[1];
+  }
   return PLAS_OK;
 }
 

@@ -358,3 +358,29 @@ def test_device_mode_paired_protocol(config_name, fixture):
     res = _paired(config_name, fixture)
     for name, (mean, se) in res.items():
         assert abs(mean) + 2 * se <= 0.005, (name, mean, se)
+
+
+# ------------------------------------------------------------------ sort-path blur tiers
+@pytest.mark.parametrize("tier", [0, 1])
+def test_blur_tiers_bit_exact_vs_oracle(tier):
+    """The sort's level blur (direct fast fold / FFT convolution, each certified against
+    the SciPy fold with exact fallback) is bit-identical to blur_target at every radius."""
+    rng = np.random.default_rng(17)
+    cases = [((300, 211, 5), (1.0, 2.5, 9.9, 16.0, 40.2, 149.0, 299.0)),
+             ((64, 64, 3), (2.0, 7.3, 15.5, 31.0, 32.0)),
+             ((128, 96, 14), (3.1, 20.0, 63.5, 127.0))]
+    for shape, radii in cases:
+        g = rng.normal(0, 1, shape).astype(np.float32)
+        for r in radii:
+            got, fb = gblur.blur_target_tiers(g, r, tier)
+            np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"tier {tier} {shape} r={r} fb={fb}")
+            assert fb[0] + fb[1] < 0.05 * g.size, fb
+
+
+def test_blur_fft_tier_top_level_c2_shape():
+    """h = 511 on a 1024-column grid (the first C2 level) through the FFT tier."""
+    rng = np.random.default_rng(23)
+    g = rng.normal(0, 1, (64, 1024, 3)).astype(np.float32)
+    got, fb = gblur.blur_target_tiers(g, 511.0, 1)
+    np.testing.assert_array_equal(got, O.blur_target(g, 511.0))
+    print("fallbacks", fb, "of", g.size)
