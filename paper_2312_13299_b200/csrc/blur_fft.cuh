@@ -36,7 +36,7 @@ namespace plas {
 struct FftPlan {
   int log2L;
   int L;
-  const double2* tw;   // [L] e^{-2 pi i t / L}
+  const double2* tw;   // [L] e^{-2 pi i t / L}, then the per-pass tables (fft_pass_twiddle_offset)
   double* spec;        // [L] real spectrum K of the current level (fft_spectrum_kernel)
   double cbound;       // relative FFT convolution error constant (x ||z_in||_2)
 };
@@ -108,117 +108,117 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
   }
 }
 
-// One Stockham pass of radix R over L points in shared memory (in place: every
-// thread reads its butterflies' inputs, the CTA syncs, then writes).  Ns = size
-// of the sub-transforms already done.  LAST: multiply the output by the real
-// spectrum and conjugate it (the pointwise step of the convolution).
 template <int L> __host__ __device__ constexpr int fft_threads_for() { return L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8); }
-
 // resident CTAs per SM the register budget must allow (~85 registers at 256 threads)
-template <int L> __host__ __device__ constexpr int fft_min_blocks() { return fft_threads_for<L>() >= 512 ? 1 : 768 / fft_threads_for<L>(); }
+template <int L> __host__ __device__ constexpr int fft_min_blocks() { return fft_threads_for<L>() >= 512 ? 1 : 512 / fft_threads_for<L>(); }
 
-template <int LOG2L, int R, int LOG2NS, bool LAST>
-__device__ __forceinline__ void stockham_pass(double2* buf, const double2* tw, const double* spec) {
-  constexpr int L = 1 << LOG2L;
-  constexpr int Ns = 1 << LOG2NS;
-  constexpr int T = fft_threads_for<L>();
-  constexpr int nb = L / R;
-  constexpr int NB = (nb + T - 1) / T;  // butterflies per thread
-  double2 v[NB][R];
-  int jj[NB];
-  // thread index re-read per pass: otherwise the compiler hoists every pass's
-  // (thread-only) address arithmetic to the kernel entry and spills it
-  unsigned tid;
-  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-#pragma unroll
-  for (int t = 0; t < NB; t++) {
-    const int j = (int)tid + t * T;
-    jj[t] = j;
-    if (j < nb) {
-#pragma unroll
-      for (int r = 0; r < R; r++) v[t][r] = buf[j + r * nb];
-      if (Ns > 1) {
-        const int k = j & (Ns - 1);
-        constexpr int step = L / (Ns * R);  // twiddle W_{Ns R}^{r k} = tw[r k step]
-#pragma unroll
-        for (int r = 1; r < R; r++) v[t][r] = cmul(v[t][r], ld_ordered(tw + ((r * k * step) & (L - 1))));
-      }
-      dft_small<R>(v[t]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < NB; t++) {
-    const int j = jj[t];
-    if (j < nb) {
+// Pass schedule of an L = 2^LOG2L point FFT: radix-8 passes, then one radix-4
+// or radix-2 pass for the remaining bits.  Pass p has sub-transform size
+// Ns = 8^p before it.
+__host__ __device__ constexpr int fft_npasses(int lg) { return lg / 3 + (lg % 3 ? 1 : 0); }
+__host__ __device__ constexpr int fft_radix(int lg, int p) { return p < lg / 3 ? 8 : (lg % 3 == 2 ? 4 : 2); }
+
+// Per-pass twiddle tables follow the L-entry table: pass p (Ns = 8^p, radix R)
+// holds W_{Ns R}^{r k} at [L + off_p + r Ns + k], k < Ns, r < R, so the lanes
+// of a warp (consecutive k) read consecutive entries.
+__host__ __device__ constexpr int fft_pass_twiddle_offset(int lg, int p) {
+  int off = 0;
+  for (int q = 0; q < p; q++) off += fft_radix(lg, q) * (1 << (3 * q));
+  return off;
+}
+__host__ __device__ constexpr int fft_twiddle_len(int lg) {
+  return (1 << lg) + fft_pass_twiddle_offset(lg, fft_npasses(lg));
+}
+
+// Shared-memory layout: one padding slot per 8 complex values, so the radix-8
+// scatter of the first pass (stride 8 x 16 B between lanes) is conflict-free.
+__host__ __device__ constexpr int fft_pad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int fft_buf_len(int L) { return L + L / 8; }
+
+// Stockham pass p of radix R: butterfly j reads v[r] = src[j + r L/R], applies
+// twiddles W_{Ns R}^{r k} (k = j mod Ns), runs the radix-R DFT and writes to
+// dst[(j - k) R + k + r Ns] (natural order after the last pass).
+template <int LOG2L, int P>
+struct FftPass {
+  static constexpr int L = 1 << LOG2L;
+  static constexpr int R = fft_radix(LOG2L, P);
+  static constexpr int Ns = 1 << (3 * P);
+  static constexpr int T = fft_threads_for<L>();
+  static constexpr int NB = (L / R + T - 1) / T;  // butterflies per thread
+
+  // twiddles W_{Ns R}^{r k}, r = 1..R-1 (all R-1 loads issued together)
+  __device__ __forceinline__ static void load_twiddles(double2 (&wv)[R], int j, const double2* __restrict__ tw) {
+    if (Ns > 1) {
       const int k = j & (Ns - 1);
-      const int d = (j - k) * R + k;
+      const double2* pt = tw + L + fft_pass_twiddle_offset(LOG2L, P) + k;
 #pragma unroll
-      for (int r = 0; r < R; r++) {
-        double2 o = v[t][r];
-        if (LAST) {
-          const double s = ld_ordered(spec + d + r * Ns);
-          o = make_double2(o.x * s, -(o.y * s));
+      for (int r = 1; r < R; r++) wv[r] = __ldg(pt + r * Ns);
+    }
+  }
+  __device__ __forceinline__ static void twiddle(double2 (&v)[R], const double2 (&wv)[R]) {
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; r++) v[r] = cmul(v[r], wv[r]);
+    }
+  }
+  __device__ __forceinline__ static int dest(int j, int r) {
+    const int k = j & (Ns - 1);
+    return (j - k) * R + k + r * Ns;
+  }
+  // smem -> smem (SPEC: multiply by the real spectrum and conjugate)
+  template <bool SPEC>
+  __device__ __forceinline__ static void run(const double2* src, double2* dst, int tid_, const double2* tw,
+                                             const double* spec) {
+    // the thread index is re-read per pass so no pass's (thread-only) twiddle
+    // loads and addresses are hoisted into an earlier pass
+    unsigned tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+#pragma unroll
+    for (int t = 0; t < NB; t++) {
+      const int j = (int)tid + t * T;
+      if (j < L / R) {
+        double2 v[R], wv[R];
+        load_twiddles(wv, j, tw);
+#pragma unroll
+        for (int r = 0; r < R; r++) v[r] = src[fft_pad(j + r * (L / R))];
+        twiddle(v, wv);
+        dft_small<R>(v);
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const int d = dest(j, r);
+          double2 o = v[r];
+          if (SPEC) {
+            const double sp = ld_ordered(spec + d);
+            o = make_double2(o.x * sp, -(o.y * sp));
+          }
+          dst[fft_pad(d)] = o;
         }
-        buf[d + r * Ns] = o;
       }
     }
   }
-  __syncthreads();
-}
+};
 
-// Forward FFT of buf (natural order in and out); LAST_SPEC applies the
-// spectrum + conjugation in the final pass.
-// radix-8 passes first (sub-transform size 8^i), then one radix-4 / radix-2
-// pass for the remaining bits; every pass is a compile-time instance.
-template <int LOG2L, bool LAST_SPEC, int PASS>
-__device__ __forceinline__ void fft_passes(double2* buf, const FftPlan& p) {
-  constexpr int NR8 = LOG2L / 3, REM = LOG2L % 3;
-  if constexpr (PASS < NR8) {
-    constexpr bool last = REM == 0 && PASS == NR8 - 1;
-    stockham_pass<LOG2L, 8, 3 * PASS, last && LAST_SPEC>(buf, p.tw, p.spec);
-    fft_passes<LOG2L, LAST_SPEC, PASS + 1>(buf, p);
-  } else if constexpr (REM == 2) {
-    stockham_pass<LOG2L, 4, 3 * NR8, LAST_SPEC>(buf, p.tw, p.spec);
-  } else if constexpr (REM == 1) {
-    stockham_pass<LOG2L, 2, 3 * NR8, LAST_SPEC>(buf, p.tw, p.spec);
+template <int LOG2L, int P, int LAST>
+struct FftChain {
+  // passes P .. LAST-1 of one FFT, ping-ponging between a and b (pass P reads a)
+  template <bool SPEC_LAST>
+  __device__ __forceinline__ static void run(double2* a, double2* b, int tid, const double2* tw, const double* spec) {
+    if constexpr (P < LAST) {
+      FftPass<LOG2L, P>::template run<SPEC_LAST && P == fft_npasses(LOG2L) - 1>(a, b, tid, tw, spec);
+      __syncthreads();
+      FftChain<LOG2L, P + 1, LAST>::template run<SPEC_LAST>(b, a, tid, tw, spec);
+    }
   }
-}
+};
 
-template <int LOG2L, bool LAST_SPEC>
-__device__ __forceinline__ void fft_forward(double2* buf, const FftPlan& p) {
-  fft_passes<LOG2L, LAST_SPEC, 0>(buf, p);
-}
-
-// The convolution's two FFTs.
-template <int LOG2L>
-__device__ __forceinline__ void fft_convolve(double2* buf, const double2* tw, double* spec) {
-  const FftPlan p{LOG2L, 1 << LOG2L, tw, spec, 0.0};
-  fft_forward<LOG2L, true>(buf, p);
-  fft_forward<LOG2L, false>(buf, p);
-}
-
-__device__ __forceinline__ double block_max_sum(double* red, double v, double m, double* out_max) {
-  // returns the CTA sum of v and writes the CTA max of m (all threads)
+__device__ __forceinline__ double warp_max_sum(double v, double m, double* out_max) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     v += __shfl_xor_sync(PLAS_FULL_MASK, v, o);
     m = fmax(m, __shfl_xor_sync(PLAS_FULL_MASK, m, o));
   }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  if (lane == 0) {
-    red[2 * wid] = v;
-    red[2 * wid + 1] = m;
-  }
-  __syncthreads();
-  double s = 0.0, mx = 0.0;
-  for (int i = 0; i < nw; i++) {
-    s += red[2 * i];
-    mx = fmax(mx, red[2 * i + 1]);
-  }
-  __syncthreads();
-  *out_max = mx;
-  return s;
+  *out_max = m;
+  return v;
 }
 
 // One axis pass of the level blur by FFT.  AXIS 0: lines = columns (x, c) of
@@ -226,9 +226,14 @@ __device__ __forceinline__ double block_max_sum(double* red, double v, double m,
 // AXIS 1: lines = rows (y, c) of tmp, output to target / den32 (EPI 1).
 // One CTA of fft_threads_for<L>() threads per line pair (no persistent loop:
 // across a loop the compiler hoists every pass's thread-only address
-// arithmetic out of it and spills).  The CTA also settles its own uncertain
-// outputs with the exact SciPy fold from a shared-memory copy of the two input
-// lines (FB_LOCAL of them; any excess goes to the global fallback list).
+// arithmetic out of it and spills).  Dataflow: the first pass of the forward
+// FFT reads the line pair straight from global memory (indices >= n are the
+// zero padding); passes ping-pong between two padded shared buffers with one
+// barrier each; the last pass of the second FFT keeps its outputs in
+// registers and certifies / stores them.  The CTA also settles its own
+// uncertain outputs with the exact SciPy fold from a shared-memory copy of
+// the two input lines (FB_LOCAL of them; any excess goes to the global list).
+// Callers guarantee n + h <= L and n <= L / 2.
 constexpr int FB_LOCAL = 512;
 
 template <int AXIS, int EPI, int LOG2L>
@@ -237,86 +242,151 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
                     FftPlan plan, const float* __restrict__ den32, int* __restrict__ fb, int fb_cap,
                     int* __restrict__ fb_other) {
   constexpr int L = 1 << LOG2L;
-  extern __shared__ double2 fbuf[];         // [L] complex line pair
-  float* raw = reinterpret_cast<float*>(fbuf + L);  // [2][n] input lines; callers guarantee n <= L/2
+  constexpr int T = fft_threads_for<L>();
+  constexpr int NP = fft_npasses(LOG2L);
+  extern __shared__ double2 fbuf[];
+  double2* bufA = fbuf;
+  double2* bufB = fbuf + fft_buf_len(L);
+  float* raw = reinterpret_cast<float*>(fbuf + 2 * fft_buf_len(L));  // [2][n] input lines
   __shared__ double red[64];
   __shared__ int flist[FB_LOCAL];
   __shared__ int nflag;
   if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) fb_other[0] = 0;
   if (threadIdx.x == 0) nflag = 0;
+  const int tid = threadIdx.x;
   const int H = pg.H, W = pg.W, C = pg.C, S = pg.S;
   const int n = AXIS == 0 ? H : W;
   const long long WS = (long long)W * S;
   const long long WSP = (long long)(W + 2 * pg.pad) * S;
-  const long long in_stride = AXIS == 0 ? WS : (long long)S;
   const int cpairs = (C + 1) >> 1;
-  const long long p = blockIdx.x;
-  const long long line = p / cpairs;
-  const int c = (int)(p - line * cpairs) * 2;
+  const long long line = blockIdx.x / cpairs;
+  const int c = (int)(blockIdx.x - line * cpairs) * 2;
   const bool has_b = c + 1 < C;
-  const long long in_base = AXIS == 0 ? line * S + c : line * WSP + c;
-  // ---- load the pair (zero-padded), ||z||_2^2 and max |x|
-  double ss = 0.0, mx = 0.0;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    double2 z = make_double2(0.0, 0.0);
-    if (i < n) {
-      const float* src = in + in_base + (long long)i * in_stride;
-      const float a = __ldg(src);
-      const float b = has_b ? __ldg(src + 1) : 0.f;
-      raw[i] = a;
-      raw[n + i] = b;
-      z = make_double2((double)a, (double)b);
-      ss = fma(z.x, z.x, fma(z.y, z.y, ss));
-      mx = fmax(mx, fmax(fabs(z.x), fabs(z.y)));
+  // ---- forward FFT pass 0 straight from global memory (+ raw copy, ||z||^2, max|x|)
+  {
+    using P0 = FftPass<LOG2L, 0>;
+    const long long in_stride = AXIS == 0 ? WS : (long long)S;
+    const float* src = in + (AXIS == 0 ? line * S + c : line * WSP + c);
+    double ss = 0.0, mx = 0.0;
+#pragma unroll
+    for (int t = 0; t < P0::NB; t++) {
+      const int j = tid + t * T;
+      if (j < L / P0::R) {
+        double2 v[P0::R];
+#pragma unroll
+        for (int r = 0; r < P0::R; r++) {
+          const int i = j + r * (L / P0::R);
+          v[r] = make_double2(0.0, 0.0);
+          if (i < n) {
+            float a, b;
+            if (has_b) {  // channels c, c+1 are adjacent (c even, rows 16-byte aligned)
+              const float2 ab = __ldg(reinterpret_cast<const float2*>(src + (long long)i * in_stride));
+              a = ab.x;
+              b = ab.y;
+            } else {
+              a = __ldg(src + (long long)i * in_stride);
+              b = 0.f;
+            }
+            raw[i] = a;
+            raw[n + i] = b;
+            v[r] = make_double2((double)a, (double)b);
+            ss = fma(v[r].x, v[r].x, fma(v[r].y, v[r].y, ss));
+            mx = fmax(mx, fmax(fabs(v[r].x), fabs(v[r].y)));
+          }
+        }
+        dft_small<P0::R>(v);
+#pragma unroll
+        for (int r = 0; r < P0::R; r++) bufA[fft_pad(P0::dest(j, r))] = v[r];
+      }
     }
-    fbuf[i] = z;
+    double m;
+    ss = warp_max_sum(ss, mx, &m);
+    if ((tid & 31) == 0) {
+      red[2 * (tid >> 5)] = ss;
+      red[2 * (tid >> 5) + 1] = m;
+    }
+    __syncthreads();
   }
-  double M;
-  const double norm2 = block_max_sum(red, ss, mx, &M);  // includes the barrier before the FFT
-  // ---- forward FFT, pointwise spectrum + conj, forward FFT again
-  fft_convolve<LOG2L>(fbuf, plan.tw, plan.spec);
-  // ---- outputs: conv(a) = re / L, conv(b) = -im / L
+  // ---- rest of the forward FFT (spectrum x conj in its last pass), then the
+  //      second FFT up to its last pass
+  FftChain<LOG2L, 1, NP>::template run<true>(bufA, bufB, tid, plan.tw, plan.spec);
+  double2* src2 = (NP - 1) % 2 == 0 ? bufA : bufB;  // where the forward FFT ended
+  double2* oth2 = (NP - 1) % 2 == 0 ? bufB : bufA;
+  FftChain<LOG2L, 0, NP - 1>::template run<false>(src2, oth2, tid, plan.tw, plan.spec);
+  const double2* last_src = (NP - 1) % 2 == 0 ? src2 : oth2;
+  // ---- bound B for this pair
   int h;
   const double* w;
   lvl.get(&h, &w);
-  const long long out_stride = AXIS == 0 ? WSP : (long long)S;
-  const long long out_base = AXIS == 0 ? line * S + c : line * WS + c;
-  const double invL = 1.0 / (double)L;
+  double norm2 = 0.0, M = 0.0;
+  for (int i = 0; i < T / 32; i++) {
+    norm2 += red[2 * i];
+    M = fmax(M, red[2 * i + 1]);
+  }
   const double fold_scale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16;
   const double B = (plan.cbound * sqrt(norm2) + fold_scale * M) * 1.0001;
-  // warp-uniform trip count (the list append below is warp-collective)
-  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    const bool in_range = i < n;
-    const double2 z = fbuf[in_range ? i : 0];
+  const double invL = 1.0 / (double)L;
+  const long long out_stride = AXIS == 0 ? WSP : (long long)S;
+  const long long out_base = AXIS == 0 ? line * S + c : line * WS + c;
+  // ---- last pass of the second FFT: outputs j + r Ns stay in registers
+  {
+    using PL = FftPass<LOG2L, NP - 1>;
 #pragma unroll
-    for (int q = 0; q < 2; q++) {
-      const bool valid = in_range && (q == 0 || has_b);
-      const double acc = q == 0 ? z.x * invL : -(z.y * invL);
-      const float lo = __double2float_rn(__dsub_rn(acc, B));
-      const float hi = __double2float_rn(__dadd_rn(acc, B));
-      const bool unsure = valid && lo != hi;
-      if (valid && !unsure) {
-        float r = __double2float_rn(acc);
-        if (EPI == 1) r = __fdiv_rn(r, den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)]);
-        out[out_base + q + (long long)i * out_stride] = r;
-      }
-      // local list (warp-aggregated), overflow to the global list
-      const unsigned bal = __ballot_sync(PLAS_FULL_MASK, unsure);
-      if (bal) {
-        const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&nflag, __popc(bal));
-        base = __shfl_sync(PLAS_FULL_MASK, base, leader);
-        if (unsure) {
-          const int slot = base + __popc(bal & ((1u << lane) - 1u));
-          if (slot < FB_LOCAL) {
-            flist[slot] = (q << 30) | i;
+    for (int t = 0; t < PL::NB; t++) {
+      const int j = tid + t * T;
+      const bool jv = j < L / PL::R;
+      double2 v[PL::R], wv[PL::R];
+      PL::load_twiddles(wv, j, plan.tw);
+#pragma unroll
+      for (int r = 0; r < PL::R; r++) v[r] = jv ? last_src[fft_pad(j + r * (L / PL::R))] : make_double2(0.0, 0.0);
+      PL::twiddle(v, wv);
+      dft_small<PL::R>(v);
+#pragma unroll
+      for (int r = 0; r < PL::R; r++) {
+        const int i = PL::dest(j, r);
+        if (PL::Ns * r >= L / 2) continue;  // dest(j, r) = j + r Ns >= L/2 >= n: zero padding, unused
+        const bool in_range = jv && i < n;
+        const float dn = (EPI == 1 && in_range) ? den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)] : 1.f;
+        float res[2];
+        bool sure[2];
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const double acc = q == 0 ? v[r].x * invL : -(v[r].y * invL);
+          sure[q] = __double2float_rn(__dsub_rn(acc, B)) == __double2float_rn(__dadd_rn(acc, B));
+          res[q] = __double2float_rn(acc);
+          if (EPI == 1) res[q] = __fdiv_rn(res[q], dn);
+        }
+        float* dsto = out + out_base + (long long)i * out_stride;
+        if (in_range) {
+          if (has_b && sure[0] && sure[1]) {
+            *reinterpret_cast<float2*>(dsto) = make_float2(res[0], res[1]);
           } else {
-            const long long o = out_base + q + (long long)i * out_stride;
-            const int e = (int)(AXIS == 0 ? (long long)i * WS + line * S + c + q : o);
-            const int g = atomicAdd(fb, 1);
-            if (g < fb_cap) fb[FB_HEADER + g] = e;
+            if (sure[0]) dsto[0] = res[0];
+            if (has_b && sure[1]) dsto[1] = res[1];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const bool valid = in_range && (q == 0 || has_b);
+          const bool unsure = valid && !sure[q];
+          // local list (warp-aggregated; trip counts are warp-uniform), overflow to the global list
+          const unsigned bal = __ballot_sync(PLAS_FULL_MASK, unsure);
+          if (bal) {
+            const int lane = tid & 31, leader = __ffs(bal) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&nflag, __popc(bal));
+            base = __shfl_sync(PLAS_FULL_MASK, base, leader);
+            if (unsure) {
+              const int slot = base + __popc(bal & ((1u << lane) - 1u));
+              if (slot < FB_LOCAL) {
+                flist[slot] = (q << 30) | i;
+              } else {
+                const long long o = out_base + q + (long long)i * out_stride;
+                const int e = (int)(AXIS == 0 ? (long long)i * WS + line * S + c + q : o);
+                const int g = atomicAdd(fb, 1);
+                if (g < fb_cap) fb[FB_HEADER + g] = e;
+              }
+            }
           }
         }
       }
@@ -325,21 +395,38 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
   __syncthreads();
   // ---- exact SciPy fold for this CTA's uncertain outputs (blur.cuh contract)
   const int nf = min(nflag, FB_LOCAL);
-  for (int t = threadIdx.x; t < nf; t += blockDim.x) {
+  for (int t = tid; t < nf; t += T) {
     const int e = flist[t];
     const int q = e >> 30, i = e & 0x3fffffff;
     const float* x = raw + q * n;
     double acc = __dmul_rn((double)x[i], __ldg(w));
-    for (int j = h; j >= 1; j--) {
+    // the terms do not depend on acc: 8 at a time, then the ordered adds
+    int j = h;
+    for (; j >= 8; j -= 8) {
+      double p[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int jj = j - u;
+        const double a = i - jj >= 0 ? (double)x[i - jj] : 0.0;
+        const double b = i + jj < n ? (double)x[i + jj] : 0.0;
+        p[u] = __dmul_rn(__dadd_rn(a, b), __ldg(w + jj));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, p[u]);
+    }
+    for (; j >= 1; j--) {
       const double a = i - j >= 0 ? (double)x[i - j] : 0.0;
       const double b = i + j < n ? (double)x[i + j] : 0.0;
       acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(a, b), __ldg(w + j)));
     }
-    float r = __double2float_rn(acc);
-    if (EPI == 1) r = __fdiv_rn(r, den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)]);
-    out[out_base + q + (long long)i * out_stride] = r;
+    float res = __double2float_rn(acc);
+    if (EPI == 1) res = __fdiv_rn(res, den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)]);
+    out[out_base + q + (long long)i * out_stride] = res;
   }
 }
+
+// shared memory of blur_fft_kernel for an L-point FFT
+inline size_t fft_smem_bytes(int L) { return sizeof(double2) * 2 * (size_t)fft_buf_len(L) + sizeof(float) * (size_t)L; }
 
 // Real spectrum of the current level's symmetric kernel on L points:
 // K[m] = w0 + 2 sum_{j=1..h} w_j cos(2 pi j m / L), cosines from the twiddle

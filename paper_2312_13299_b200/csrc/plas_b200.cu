@@ -220,7 +220,7 @@ int fft_min_h() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PLAS_FFT_MIN_H");
-    v = e ? atoi(e) : 16;
+    v = e ? atoi(e) : 64;  // measured crossover at C2: direct ~85 + 3.4 h us per axis, FFT ~290 us
     if (v < 0) v = 0;
   }
   return v;
@@ -238,12 +238,21 @@ double fft_error_constant(int log2L) {
   return 2.0 * (c * (1.0 + e2) + e2);
 }
 
+// e^{-2 pi i t / L} for t < L (correctly rounded from long double), then the
+// per-pass tables W_{Ns R}^{r k} = e^{-2 pi i r k step / L} (blur_fft.cuh)
 void fft_twiddles(int L, std::vector<double2>* tw) {
-  tw->resize(L);
+  const int lg = next_log2(L);
+  tw->resize(fft_twiddle_len(lg));
   const long double pi = 3.141592653589793238462643383279502884L;
   for (int t = 0; t < L; t++) {
     const long double a = -2.0L * pi * (long double)t / (long double)L;
     (*tw)[t] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  for (int p = 0; p < fft_npasses(lg); p++) {
+    const int R = fft_radix(lg, p), Ns = 1 << (3 * p), step = L / (Ns * R);
+    for (int r = 0; r < R; r++)
+      for (int k = 0; k < Ns; k++)
+        (*tw)[L + fft_pass_twiddle_offset(lg, p) + r * Ns + k] = (*tw)[((long long)r * k * step) & (L - 1)];
   }
 }
 
@@ -288,7 +297,7 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS);
   w->fft_L = fft_alloc_length(side);
-  w->fft_tw = c.take<double2>((size_t)std::max(w->fft_L, 1));
+  w->fft_tw = c.take<double2>(w->fft_L ? (size_t)fft_twiddle_len(next_log2(w->fft_L)) : 1);
   w->fft_spec = c.take<double>((size_t)std::max(w->fft_L, 1));
   return align_up(c.off);
 }
@@ -491,7 +500,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   std::vector<double2> htw;
   if (w.fft_L) {
     fft_twiddles(w.fft_L, &htw);
-    CK(cudaMemcpyAsync(w.fft_tw, htw.data(), sizeof(double2) * w.fft_L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.fft_tw, htw.data(), sizeof(double2) * htw.size(), cudaMemcpyHostToDevice, st));
   }
 
   // ---- initial permutation (plas.py:241)
@@ -555,7 +564,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   const int fft_nthreads = w.fft_L ? fft_threads(w.fft_L) : 32;
   void* fft0 = w.fft_L ? fft_kernel_ptr<0, 0>(fft_log2) : nullptr;
   void* fft1 = w.fft_L ? fft_kernel_ptr<1, 1>(fft_log2) : nullptr;
-  const size_t fft_smem = (sizeof(double2) + sizeof(float)) * (size_t)w.fft_L;  // line pair + raw inputs (2 n <= L floats)
+  const size_t fft_smem = w.fft_L ? fft_smem_bytes(w.fft_L) : 0;
   int fft_grid = 1;
   if (w.fft_L) {
     CK(cudaFuncSetAttribute(fft0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
@@ -1035,7 +1044,7 @@ static size_t carve_tiers(char* base, int H, int W, int C, int h, TierWs* t) {
   const int k = std::max(std::max(next_log2((long long)std::max(H, W) + h), next_log2(2LL * std::max(H, W))),
                          FFT_MIN_LOG2);
   t->L = k <= FFT_MAX_LOG2 ? 1 << k : 0;
-  t->tw = c.take<double2>((size_t)std::max(t->L, 1));
+  t->tw = c.take<double2>(t->L ? (size_t)fft_twiddle_len(next_log2(t->L)) : 1);
   t->spec = c.take<double>((size_t)std::max(t->L, 1));
   t->fb_cap = (int)std::min<long long>((long long)H * W * S / 8 + 1024, 1LL << 26);
   t->fb0 = c.take<int>((size_t)FB_HEADER + t->fb_cap);
@@ -1103,12 +1112,12 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
   } else {
     std::vector<double2> htw;
     fft_twiddles(t.L, &htw);
-    CK(cudaMemcpyAsync(t.tw, htw.data(), sizeof(double2) * t.L, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(t.tw, htw.data(), sizeof(double2) * htw.size(), cudaMemcpyHostToDevice, st));
     const int lg = next_log2(t.L);
     const FftPlan plan{lg, t.L, t.tw, t.spec, fft_error_constant(lg)};
     void* f0 = fft_kernel_ptr<0, 0>(lg);
     void* f1 = fft_kernel_ptr<1, 1>(lg);
-    const size_t smem = (sizeof(double2) + sizeof(float)) * (size_t)t.L;
+    const size_t smem = fft_smem_bytes(t.L);
     CK(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nt = fft_threads(t.L);
