@@ -58,6 +58,7 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true")
+    p.add_argument("--no-smoothness", action="store_true")
     return p.parse_args(argv)
 
 
@@ -301,6 +302,48 @@ def ncu_traffic(prefixes=("pass_kernel", "tile_pass_kernel")):
         return None
 
 
+def run_smoothness(feats, perm_np, side, device, peak, steps=5):
+    """Smoothness-loss fwd+bwd (smoothness.py:57-97) on the sorted grid, default
+    SmoothnessParams (opacity 0.09, rotation 0.91: C_w = 5 channels), fp64 as the
+    reference; planes resident in HBM, CUDA events.  Algorithmic bytes: each
+    weighted plane element read once and its gradient written once (16 B fp64)."""
+    import torch
+    import paper_2312_13299_b200 as plas
+    from paper_2312_13299_b200 import synthetic
+    planes_np = synthetic.smoothness_planes(feats[perm_np], side)
+    planes = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device) for k, v in planes_np.items()}
+    stack = plas.GridStack(plas.GridLayout(side), planes)
+    params = plas.SmoothnessParams()
+    for _ in range(3):
+        plas.smoothness_loss(stack, params, return_device=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        loss, _ = plas.smoothness_loss(stack, params, return_device=True)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    cw = sum(v.shape[-1] for k, v in planes_np.items() if params.weights.get(k, 0.0) > 0)
+    alg = side * side * cw * 16
+    out = {"what": "smoothness_loss fwd+bwd, default SmoothnessParams, fp64, sorted C2 grid",
+           "ms": round(ms, 3), "loss": loss, "weighted_channels": cw,
+           "algorithmic_bytes": alg, "achieved_GBps": round(alg / ms / 1e6, 1),
+           "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
+    rp = _reference_module()
+    if rp is not None:
+        import sogs.smoothness as rs
+        from sogs.splats import GridLayout as RL, GridStack as RS
+        rstack = RS(RL(side), planes_np)
+        rs.smoothness_loss(rstack, rs.SmoothnessParams())
+        t0 = time.perf_counter()
+        rl, _ = rs.smoothness_loss(rstack, rs.SmoothnessParams())
+        out["reference_cpu_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        out["reference_loss"] = rl
+        out["loss_rel_diff"] = abs(loss - rl) / max(abs(rl), 1e-300)
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_2312_13299_b200 as plas
@@ -406,15 +449,22 @@ def run_ours(args):
         b_avg = (prof.ms_blur0 + prof.ms_blur1) / max(1, prof.n_blur0 + prof.n_blur1) / 1e3
         roofline["blur_hbm_frac"] = round(alg_blur / b_avg / 1e9 / peak, 4) if b_avg else None
 
+    smooth = None
+    if args.config == "C2" and not args.no_smoothness:
+        smooth = run_smoothness(feats, perm_np, side, device, measured_peak()[0])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_sample(feats, WORKLOADS[args.config]["cfg"], args.cpu_budget,
                                    [len(t) - 1 for _, t in rep["radius_trace"]], "this GPU run's")
 
-    # kernels launched per sort by our library (graph mode): 6 init + 5 final +
-    # 8 per level + 2 per pass (see plas_b200.cu); parity mode adds 3 per pass
+    # kernels launched per sort by our library (graph mode, plas_b200.cu): 6 init
+    # + 5 final; per level: begin, 2 border, 4 blur (direct fold + fallback per
+    # axis) or 5 (spectrum + FFT + fallback per axis, h >= 64), stats, end; per
+    # pass: K3 + statistics/controller (parity mode adds 3 per pass)
     per_pass = 2 if args.mode == "device" else 5
-    launches = sum(11 + 8 * L + per_pass * P for L, P in zip(levels, passes))
+    fft_levels = sum(1 for r, _ in rep["radius_trace"] if math.ceil(r) >= 64)
+    launches = sum(11 + 8 * L + fft_levels + per_pass * P for L, P in zip(levels, passes))
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
@@ -425,7 +475,7 @@ def run_ours(args):
                    "sort_config": WORKLOADS[args.config]["cfg"] or "SortConfig defaults",
                    "l2": "256 MiB buffer written before every timed step (outside the events)",
                    "parallelism": f"{world} independent grid(s), one per rank"},
-        "quality": quality, "e2e": e2e, "roofline": roofline, "kernel_ms": kernel_ms,
+        "quality": quality, "e2e": e2e, "roofline": roofline, "kernel_ms": kernel_ms, "smoothness": smooth,
         "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
     }
     if rank == 0:
