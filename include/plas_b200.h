@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PLAS_ABI_VERSION 1
+#define PLAS_ABI_VERSION 2
 
 enum plas_status {
   PLAS_OK = 0,
@@ -77,6 +77,28 @@ typedef struct plas_sort_args {
    * kernels, same work; DEVICE mode then syncs once per pass instead of
    * running as one graph).  Used by bench.py for per-kernel roofline data. */
   void* profile;
+  /* Multi-GPU sharding (world > 1; 0 or 1 = single GPU).  Every rank runs
+   * plas_sort on its own device with identical arguments and keeps a full
+   * replica of the grid; each pass's groups are split into contiguous,
+   * balanced per-rank ranges.  After each pass the library writes this
+   * rank's (fp64 distance change, moved-cell count) to xchg_part[0..1] and
+   * its (cell, element) int32 pairs to xchg_send, then calls
+   * exchange(exchange_ctx), which must all-gather xchg_part into
+   * xchg_part_all[2 * world] (rank order) and the first m pairs of every
+   * rank's xchg_send into xchg_recv (rank r's pairs at r * m), with m >= the
+   * largest moved-cell count, and return m (< 0 = error).  Collectives must be
+   * ordered after the work already enqueued on `stream` and before work
+   * enqueued after the call returns (torch.distributed over NCCL does this).
+   * Every rank then applies the others' updates and runs the identical
+   * controller on the partials summed in rank order. */
+  int rank;
+  int world;
+  int (*exchange)(void* exchange_ctx);
+  void* exchange_ctx;
+  void* xchg_send;        /* device int32 [2 * n] */
+  void* xchg_recv;        /* device int32 [2 * n * world] */
+  double* xchg_part;      /* device [2] */
+  double* xchg_part_all;  /* device [2 * world] */
 } plas_sort_args;
 
 /* Per-kernel device time (CUDA events, ms) summed over all launches. */
@@ -116,6 +138,9 @@ int plas_num_levels(int64_t n, double radius_decay, double initial_radius);
 /* Workspace for plas_sort; ws must be 256-byte aligned device memory. */
 size_t plas_sort_workspace_bytes(int64_t n, int dim, int num_levels, int64_t weights_len,
                                  int64_t trace_capacity, int rng_mode);
+/* Same for a sharded sort on `world` ranks (adds the element-order f32 copy). */
+size_t plas_sort_workspace_bytes_sharded(int64_t n, int dim, int num_levels, int64_t weights_len,
+                                         int64_t trace_capacity, int rng_mode, int world);
 
 /* sort_grid / sort_grid_report (plas.py:226-301). */
 int plas_sort(const plas_sort_args* args, plas_sort_result* result, void* ws, size_t ws_bytes);

@@ -30,6 +30,9 @@ PLAS_BLUR_SEPARABLE, PLAS_BLUR_RENORMALIZED, PLAS_BLUR_BORDER_WEIGHT = 0, 1, 2
 P = ctypes.c_void_p
 i32, i64, u64, f64, sz = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_size_t
 
+# int (*exchange)(void* ctx) of plas_sort_args (multi-GPU sharding)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+
 
 class SortArgs(ctypes.Structure):
     _fields_ = [
@@ -38,6 +41,8 @@ class SortArgs(ctypes.Structure):
         ("min_block_size", i32), ("seed", u64), ("rng_mode", i32), ("num_levels", i32),
         ("radii", P), ("weights", P), ("weight_offsets", P), ("initial_perm", P),
         ("trace_capacity", i64), ("stream", P), ("profile", P),
+        ("rank", i32), ("world", i32), ("exchange", EXCHANGE_FN), ("exchange_ctx", P),
+        ("xchg_send", P), ("xchg_recv", P), ("xchg_part", P), ("xchg_part_all", P),
     ]
 
 
@@ -64,6 +69,7 @@ SIGNATURES = {
     "plas_last_error": (ctypes.c_char_p, []),
     "plas_num_levels": (i32, [i64, f64, f64]),
     "plas_sort_workspace_bytes": (sz, [i64, i32, i32, i64, i64, i32]),
+    "plas_sort_workspace_bytes_sharded": (sz, [i64, i32, i32, i64, i64, i32, i32]),
     "plas_sort": (i32, [ctypes.POINTER(SortArgs), ctypes.POINTER(SortResult), P, sz]),
     "plas_assign_groups": (i32, [P, P, P, i32, i32, P, i64, i32, P]),
     "plas_aux_workspace_bytes": (sz, [i32, i32, i32]),

@@ -412,13 +412,13 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
   const unsigned cap = (unsigned)ctrl->cap;
-  const unsigned total = (unsigned)ctrl->total_groups;
+  const unsigned g_lo = (unsigned)ctrl->g_lo, total = (unsigned)ctrl->g_hi;  // this rank's groups
   const unsigned cap_m = ctrl->cap_m, nbx_m = ctrl->nbx_m;
   const int cap_l = ctrl->cap_l, nbx_l = ctrl->nbx_l;
   const int nch = S >> 2;
   const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
   int exact = 0;
-  for (unsigned base = blockIdx.x * 64u; base < total; base += gridDim.x * 64u) {
+  for (unsigned base = g_lo + blockIdx.x * 64u; base < total; base += gridDim.x * 64u) {
     const unsigned g = base + gl;
     int k = 0, cell = 0;
     if (g < total) {
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
   const int beta = ctrl->beta;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
-  const int nblocks = nby * nbx;
+  const int b_lo = ctrl->b_lo, nblocks = ctrl->b_hi;  // this rank's blocks
   const int nch = S >> 2;
   const long long mmax = (long long)beta * beta;
   const size_t stage_floats = (size_t)(tile_stage_bytes(beta, S) / 4);
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
   };
 
   int exact = 0;
-  int b = blockIdx.x, st = 0;
+  int b = b_lo + blockIdx.x, st = 0;
   prefetch(b, 0);
   for (; b < nblocks; b += gridDim.x, st ^= 1) {
     prefetch(b + gridDim.x, st ^ 1);

@@ -52,6 +52,10 @@ struct Ctrl {
   int tile;                        // this pass runs the shared-memory tile kernel
   int fft_min_h;                   // levels with h >= fft_min_h (> 0) blur by FFT
   int fft_L;                       // FFT length (0 = no FFT tier)
+  // multi-GPU sharding (world > 1): this rank's share of the pass
+  int rank, world;
+  long long g_lo, g_hi;            // gather kernel: groups [g_lo, g_hi)
+  int b_lo, b_hi;                  // tile kernel: blocks [b_lo, b_hi)
 };
 
 // Blocks whose feature + target rows fit in TILE_SMEM_MAX bytes of shared
@@ -278,6 +282,13 @@ __host__ __device__ __forceinline__ void set_pass_geometry_base(Ctrl* c, int dy,
   segment(c->nbx - 1, c->first_x, c->beta, c->side, &lo, &hi);
   c->seg_w[2] = hi - lo;
   c->tile = use_tile(c->beta, c->S) ? 1 : 0;
+  // contiguous, balanced shares of the pass's groups / blocks (whole pass when world == 1)
+  const long long nb = (long long)c->nby * c->nbx;
+  const int W = c->world > 0 ? c->world : 1;
+  c->g_lo = c->total_groups * c->rank / W;
+  c->g_hi = c->total_groups * (c->rank + 1) / W;
+  c->b_lo = (int)(nb * c->rank / W);
+  c->b_hi = (int)(nb * (c->rank + 1) / W);
   make_fastdiv((unsigned)c->cap, &c->cap_m, &c->cap_l);
   make_fastdiv((unsigned)c->nbx, &c->nbx_m, &c->nbx_l);
 }

@@ -32,6 +32,17 @@ __global__ void gather_init_kernel(const Tin* __restrict__ features, const int* 
   if (__any_sync(PLAS_FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
 
+// f32 working copy of the features in element order (sharding: rows of
+// other ranks' moved elements are re-read from it)
+template <typename Tin>
+__global__ void orig32_kernel(const Tin* __restrict__ features, float* __restrict__ out, long long n, int D, int S) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n * S; t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / S;
+    const int d = (int)(t - i * S);
+    out[t] = d < D ? (float)features[i * D + d] : 0.f;
+  }
+}
+
 // DEVICE-mode initial permutation: keyed bijection on [0, n)
 __global__ void init_perm_device_kernel(int* __restrict__ idx, long long n, unsigned long long key0,
                                         unsigned long long key1) {
@@ -205,15 +216,51 @@ __global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
   }
 }
 
+// Strike logic of one finished pass (plas.py:266-272) given the summed fp64
+// distance change `tot` of its moved cells: current = (level-start sum +
+// changes) / n, trace append, strikes, level end.  Thread 0 only; returns
+// whether the level continues.
+__device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, long long n,
+                                                unsigned long long inner) {
+  c->dist_sum += tot;
+  const double current = c->dist_sum / (double)n;
+  const double previous = c->previous;
+  c->current = current;
+  c->reorders++;
+  c->pass++;
+  if (c->trace_pos >= c->trace_cap) {
+    c->status = 1;
+    c->level_done = 1;
+    set_cond(inner, 0);
+    return false;
+  }
+  s.trace[c->trace_pos++] = current;
+  if (previous <= 0.0 || (previous - current) / previous < c->threshold)
+    c->strikes++;
+  else
+    c->strikes = 0;
+  c->previous = current;
+  if (c->strikes >= 2) {
+    c->level_done = 1;
+    set_cond(inner, 0);
+    return false;
+  }
+  return true;
+}
+
 // After a pass: exact fp64 distance change of the moved cells (cells that
 // keep their element keep their cached distance), so current =
 // (level-start sum + deltas) / n equals grid_distance(feat, target)
 // (plas.py:266) up to fp64 summation order; then the strike logic
 // (plas.py:267-272) and the next pass's geometry.
+// Sharded (world > 1): the last CTA only publishes this rank's partial
+// (change, moved count) to xpart; shard_control_kernel runs the controller
+// once every rank's partial has been exchanged.
 __global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
-    double* partials, int* done, long long n, unsigned long long inner, unsigned long long tile_cond) {
+    double* partials, int* done, long long n, unsigned long long inner, unsigned long long tile_cond,
+    double* xpart) {
   __shared__ double sh[32];
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
@@ -240,39 +287,81 @@ __global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
     }
   }
   if (!last_cta_reduce(sum, partials, done, &s_tot, sh)) return;
+  if (c->world > 1) {
+    if (threadIdx.x == 0) {
+      xpart[0] = s_tot;
+      xpart[1] = (double)count;
+    }
+    return;
+  }
   bool more = false;
   if (threadIdx.x == 0) {
     counters[0] += count;
     counters[2] = 0;
-    c->dist_sum += s_tot;
-    const double current = c->dist_sum / (double)n;
-    const double previous = c->previous;
-    c->current = current;
-    c->reorders++;
-    c->pass++;
-    if (c->trace_pos >= c->trace_cap) {
-      c->status = 1;
-      c->level_done = 1;
-      set_cond(inner, 0);
-    } else {
-      s.trace[c->trace_pos++] = current;
-      if (previous <= 0.0 || (previous - current) / previous < c->threshold)
-        c->strikes++;
-      else
-        c->strikes = 0;
-      c->previous = current;
-      if (c->strikes >= 2) {
-        c->level_done = 1;
-        set_cond(inner, 0);
-      } else {
-        more = true;
-      }
-    }
+    more = controller_step(c, s, s_tot, n, inner);
   }
   more = __syncthreads_or(more);
   if (!more || c->rng_mode != 1) return;
   prepare_device_pass_cta(c, &s_gkey);
   if (threadIdx.x == 0) set_cond(tile_cond, c->tile);
+}
+
+// ---------------------------------------------------------------- sharding
+// This rank's moved cells -> (cell, element) pairs for the exchange.
+__global__ void shard_pack_kernel(const int* __restrict__ list, const int* __restrict__ counters,
+                                  const int* __restrict__ idx, int2* __restrict__ send) {
+  const int count = counters[2];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
+    const int cell = list[e];
+    send[e] = make_int2(cell, idx[cell]);
+  }
+}
+
+// Every other rank's updates: element idx now sits in cell -> its f32 row
+// (orig32, the working copy in element order), the index and the cached
+// distance to the cell's target.  recv holds world segments of `stride`
+// pairs; counts come with the exchanged partials (xall[2 s + 1]).
+__global__ void shard_apply_kernel(const int2* __restrict__ recv, long long stride, const double* __restrict__ xall,
+                                   int world, int rank, const float* __restrict__ orig32, float* __restrict__ feat,
+                                   int* __restrict__ idx, const float* __restrict__ target,
+                                   double* __restrict__ dcache, int D, int S) {
+  const int nch = S >> 2;
+  for (int r = 0; r < world; r++) {
+    if (r == rank) continue;
+    const long long cnt = (long long)xall[2 * r + 1];
+    const int2* seg = recv + (long long)r * stride;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cnt;
+         e += (long long)gridDim.x * blockDim.x) {
+      const int2 u = seg[e];
+      const long long cell = u.x, el = u.y;
+      for (int c = 0; c < nch; c++)
+        reinterpret_cast<float4*>(feat + cell * S)[c] = reinterpret_cast<const float4*>(orig32 + el * S)[c];
+      idx[cell] = (int)el;
+      dcache[cell] = sqrt(cell_dist2(feat + cell * S, target + cell * S, D, S));
+    }
+  }
+}
+
+// The controller on the exchanged partials, summed in rank order (identical on
+// every rank), then the next pass's draws and geometry.
+__global__ void __launch_bounds__(RED_THREADS) shard_control_kernel(Ctrl* c, Sched s, const double* __restrict__ xall,
+                                                                    int world, int* counters, long long n) {
+  __shared__ unsigned long long s_gkey;
+  bool more = false;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    long long moved = 0;
+    for (int r = 0; r < world; r++) {
+      tot += xall[2 * r];
+      moved += (long long)xall[2 * r + 1];
+    }
+    counters[0] += (int)moved;
+    counters[2] = 0;
+    more = controller_step(c, s, tot, n, 0ull);
+  }
+  more = __syncthreads_or(more);
+  if (!more || c->rng_mode != 1) return;
+  prepare_device_pass_cta(c, &s_gkey);
 }
 
 // level bookkeeping (plas.py:273-274); radius decay is the schedule table

@@ -177,6 +177,7 @@ struct SortWs {
   long long sel_stride;
   int* list;      // moved-cell list of the current pass
   double* spart;  // statistic-kernel partials
+  float* orig32;      // sharding: f32 features in element order
   double2* fft_tw;   // [fft_L] twiddles (large-radius FFT blur)
   double* fft_spec;  // [fft_L] spectrum of the current level
   int fft_L;
@@ -260,7 +261,7 @@ void fft_twiddles(int L, std::vector<double2>* tw) {
 int blur_pad(int side) { return (int)ceil(std::max(side / 2.0 - 1.0, 2.0)) + BLUR_R + 1; }
 
 size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long long tcap,
-                  int rng_mode, int side, long long list_cap, SortWs* w) {
+                  int rng_mode, int side, long long list_cap, SortWs* w, int world = 1) {
   Carver c{base};
   const int S = row_stride(dim);
   const int P = blur_pad(side);
@@ -296,6 +297,7 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->sel = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(9 * b0 * b0) : 1);
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS);
+  w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
   w->fft_L = fft_alloc_length(side);
   w->fft_tw = c.take<double2>(w->fft_L ? (size_t)fft_twiddle_len(next_log2(w->fft_L)) : 1);
   w->fft_spec = c.take<double>((size_t)std::max(w->fft_L, 1));
@@ -428,6 +430,15 @@ size_t plas_sort_workspace_bytes(int64_t n, int dim, int num_levels, int64_t wei
   return carve_sort(nullptr, n, dim, num_levels, weights_len, trace_capacity, rng_mode, side, lc, &w);
 }
 
+size_t plas_sort_workspace_bytes_sharded(int64_t n, int dim, int num_levels, int64_t weights_len,
+                                         int64_t trace_capacity, int rng_mode, int world) {
+  SortWs w;
+  const int side = (int)llround(sqrt((double)n));
+  const long long lc = list_capacity(n);
+  return carve_sort(nullptr, n, dim, num_levels, weights_len, trace_capacity, rng_mode, side, lc, &w,
+                    std::max(world, 1));
+}
+
 void plas_seed_key(uint64_t seed, uint64_t key[2]) { host::seed_key(seed, key); }
 
 int plas_host_permutation(uint64_t seed, int64_t n, int64_t* out) {
@@ -460,10 +471,14 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   SortWs w;
   const int S = row_stride(D);
   const long long lcap = list_capacity(n);
-  size_t need = carve_sort(nullptr, n, D, L, (long long)sch.weights.size(), tcap, mode, side, lcap, &w);
+  const int world = std::max(a->world, 1);
+  if (world > 1 && (a->rank < 0 || a->rank >= world || !a->exchange || !a->xchg_send || !a->xchg_recv ||
+                    !a->xchg_part || !a->xchg_part_all))
+    return fail(PLAS_ERR_INVALID, "sharded sort needs rank < world, an exchange callback and its buffers");
+  size_t need = carve_sort(nullptr, n, D, L, (long long)sch.weights.size(), tcap, mode, side, lcap, &w, world);
   if (!wsp || ws_bytes < need)
     return fail(PLAS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
-  carve_sort((char*)wsp, n, D, L, (long long)sch.weights.size(), tcap, mode, side, lcap, &w);
+  carve_sort((char*)wsp, n, D, L, (long long)sch.weights.size(), tcap, mode, side, lcap, &w, world);
 
   // ---- upload schedule + controller
   if (L > 0) {
@@ -489,6 +504,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.key1 = key[1];
   hc.fft_min_h = fft_min_h();
   hc.fft_L = w.fft_L;
+  hc.rank = world > 1 ? a->rank : 0;
+  hc.world = world;
   CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
   // zero halos of the padded blur buffers, pad channels, fallback counters
@@ -534,6 +551,13 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     gather_init_kernel<double><<<gi, 256, 0, st>>>((const double*)a->features, w.idx, w.feat, n, D,
                                                    S, w.flags);
   CKL();
+  if (world > 1) {
+    if (a->features_dtype == PLAS_F32)
+      orig32_kernel<float><<<gi, 256, 0, st>>>((const float*)a->features, w.orig32, n, D, S);
+    else
+      orig32_kernel<double><<<gi, 256, 0, st>>>((const double*)a->features, w.orig32, n, D, S);
+    CKL();
+  }
   int hflags = 0;
   CK(cudaMemcpyAsync(&hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -592,7 +616,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   int* counters = w.flags + 2;  // [0] moved cells, [1] exact decisions, [2] moved-list length
   MoveOut ml{w.list, counters + 2};
   int* done = w.flags + 6;      // last-CTA ticket of the statistic kernels
-  if (mode == PLAS_RNG_DEVICE && !a->profile) {
+  if (mode == PLAS_RNG_DEVICE && !a->profile && world == 1) {
     // ------------------------------------------------------------ graph
     // outer WHILE (levels): level_begin, border weight, blur axis 0, blur axis 1,
     //   level statistics, inner WHILE (passes): IF(tile){tile}ELSE{gather},
@@ -718,7 +742,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(add_kernel(&pn[2], ibody, &if_node, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl,
                   lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, D, S,
                   (const int*)w.list, counters, w.spart, done, n, (unsigned long long)inner_h,
-                  (unsigned long long)tile_h));
+                  (unsigned long long)tile_h, (double*)nullptr));
     cudaGraphExec_t ge;
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
@@ -870,9 +894,24 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         }
         timed(K_CTRL, [&] {
           pass_stats_kernel<<<sgrid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, D, S,
-                                                           w.list, counters, w.spart, done, n, 0, 0);
+                                                           w.list, counters, w.spart, done, n, 0, 0, a->xchg_part);
         });
         CKL();
+        if (world > 1) {
+          // exchange this rank's updates + partial, apply the others', run the controller
+          shard_pack_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(w.list, counters, w.idx, (int2*)a->xchg_send);
+          CKL();
+          const int m = a->exchange(a->exchange_ctx);
+          if (m < 0) {
+            cleanup();
+            return fail(PLAS_ERR_CUDA, "exchange callback failed");
+          }
+          shard_apply_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>((const int2*)a->xchg_recv, m, a->xchg_part_all,
+                                                                  world, a->rank, w.orig32, w.feat, w.idx, w.target,
+                                                                  w.dcache, D, S);
+          shard_control_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, a->xchg_part_all, world, counters, n);
+          CKL();
+        }
         CK(cudaMemcpyAsync(hflag, &w.ctrl->level_done, sizeof(int), cudaMemcpyDeviceToHost, st));
         // speculative draws for the next pass while the GPU runs this one
         host::NumpyPhilox saved = rng;

@@ -203,18 +203,36 @@ class SortPlan:
                                  config.initial_radius)
         self.trace_capacity = max(64 * max(self.schedule.num_levels, 1), 4096)
 
-    def run(self, features_dev, perm_out, initial_perm=None, profile=None):
+    def run(self, features_dev, perm_out, initial_perm=None, profile=None, shard=None):
         """features_dev: CUDA f32/f64 (n, dim); perm_out: CUDA int64 (n,). Returns report fields.
 
         profile: optional _lib.SortProfile filled with per-kernel CUDA-event times
-        (host-stepped execution of the same kernels)."""
+        (host-stepped execution of the same kernels).
+        shard: optional sharded.ShardSpec (rank, world, exchange) for a multi-GPU sort;
+        every rank calls run() with identical arguments."""
         import torch
         L = _lib.lib()
         sch = self.schedule
+        world = shard.world if shard is not None else 1
+        xb = None
+        if world > 1:
+            dev = features_dev.device
+            xb = {"send": torch.zeros(2 * self.n, dtype=torch.int32, device=dev),
+                  "recv": torch.zeros(2 * self.n * world, dtype=torch.int32, device=dev),
+                  "part": torch.zeros(2, dtype=torch.float64, device=dev),
+                  "part_all": torch.zeros(2 * world, dtype=torch.float64, device=dev)}
+
+            def _cb(_ctx):
+                try:
+                    return int(shard.exchange(xb["send"], xb["recv"], xb["part"], xb["part_all"]))
+                except Exception as exc:  # never raise through the C ABI
+                    xb["error"] = exc
+                    return -1
+            xb["cb"] = _lib.EXCHANGE_FN(_cb)
         while True:
-            wsb = L.plas_sort_workspace_bytes(self.n, self.dim, sch.num_levels, len(sch.weights),
-                                              self.trace_capacity, self.mode)
-            ws = _lib.workspace(wsb, "sort")
+            wsb = L.plas_sort_workspace_bytes_sharded(self.n, self.dim, sch.num_levels, len(sch.weights),
+                                                      self.trace_capacity, self.mode, world)
+            ws = _lib.workspace(wsb, "sort" if world == 1 else f"sort{shard.rank}")
             args = _lib.SortArgs()
             args.features = _lib.ptr(features_dev)
             args.features_dtype = _lib.PLAS_F32 if features_dev.dtype == torch.float32 else _lib.PLAS_F64
@@ -235,6 +253,11 @@ class SortPlan:
             args.trace_capacity = self.trace_capacity
             args.stream = _lib.stream_handle()
             args.profile = None if profile is None else ctypes.cast(ctypes.pointer(profile), ctypes.c_void_p)
+            if world > 1:
+                args.rank, args.world = shard.rank, world
+                args.exchange = xb["cb"]
+                args.xchg_send, args.xchg_recv = _lib.ptr(xb["send"]), _lib.ptr(xb["recv"])
+                args.xchg_part, args.xchg_part_all = _lib.ptr(xb["part"]), _lib.ptr(xb["part_all"])
             counts = np.zeros(max(sch.num_levels, 1), dtype=np.int64)
             trace = np.zeros(self.trace_capacity, dtype=np.float64)
             res = _lib.SortResult()
@@ -245,6 +268,8 @@ class SortPlan:
             if code == _lib.PLAS_ERR_CAPACITY:
                 self.trace_capacity *= 4
                 continue
+            if xb is not None and "error" in xb:
+                raise RuntimeError(f"exchange failed on rank {shard.rank}") from xb["error"]
             _lib.check(code, "plas_sort")
             break
         traces = []

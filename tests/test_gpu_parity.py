@@ -384,3 +384,47 @@ def test_blur_fft_tier_top_level_c2_shape():
     got, fb = gblur.blur_target_tiers(g, 511.0, 1)
     np.testing.assert_array_equal(got, O.blur_target(g, 511.0))
     print("fallbacks", fb, "of", g.size)
+
+
+# ------------------------------------------------------------------ multi-GPU sharding (emulated ranks)
+@pytest.mark.parametrize("mode,world", [("parity", 2), ("parity", 3), ("device", 2), ("device", 4)])
+def test_sharded_sort_matches_single_gpu(mode, world):
+    """The sharded protocol (per-rank group ranges + exchange of moved cells and
+    partials, sharded.py) reproduces the single-GPU sort: same permutation on every
+    rank, same pass count, trace equal up to fp64 summation order."""
+    from paper_2312_13299_b200 import sharded
+    f = synthetic.c1(0, side=96)
+    cfg = plas.SortConfig(rng_seed=3, rng_mode=mode)
+    p1, r1 = plas.sort_grid_report(f, cfg)
+    outs = sharded.sort_emulated(f, cfg, world)
+    for perm, rep in outs:
+        np.testing.assert_array_equal(perm, p1)
+        assert rep["reorders"] == r1.reorders
+        np.testing.assert_allclose([v for _, t in rep["radius_trace"] for v in t],
+                                   [v for _, t in r1.radius_trace for v in t], rtol=1e-12)
+
+
+def test_sharded_sort_c0_parity_golden():
+    """BASELINE configs[0] sharded over 4 emulated ranks: bit-exact with the reference."""
+    from paper_2312_13299_b200 import sharded
+    z = golden_npz("c0.npz")
+    feats = synthetic.c0(0)
+    case = golden_json("c0.json")[0]
+    cfg = plas.SortConfig(initial_radius=case.get("initial_radius"), **case["cfg"])
+    for perm, rep in sharded.sort_emulated(feats, cfg, 4):
+        key = ("s%d" if case["initial_radius"] is None else "r32_s%d") % case["cfg"]["rng_seed"]
+        np.testing.assert_array_equal(perm, z[key].astype(np.int64))
+        assert rep["reorders"] == case["reorders"]
+
+
+@pytest.mark.parametrize("side,dim", [(48, 21), (40, 59)])
+def test_sort_wide_rows_parity_vs_oracle(side, dim):
+    """Rows wider than 16 floats (the WIDE kernels; configs[3] has D = 59): PARITY
+    sort bit-exact with the C oracle (itself pinned to the reference goldens)."""
+    f = np.random.default_rng(side * dim).normal(0, 1, (side * side, dim))
+    perm, rep = plas.sort_grid_report(f, plas.SortConfig(rng_seed=2))
+    want, wrep = O.sort_grid_report(f, rng_seed=2)
+    np.testing.assert_array_equal(perm, want)
+    assert rep.reorders == wrep["reorders"]
+    np.testing.assert_allclose([v for _, t in rep.radius_trace for v in t],
+                               [v for _, t in wrep["radius_trace"] for v in t], rtol=1e-12)

@@ -1,0 +1,81 @@
+"""Host-side logic of the multi-GPU sort on CPU: partition ranges and the
+exchange protocol over a real 2-process gloo group (sharded.DistExchange)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2312_13299_b200 import sharded
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_ranges_partition(world):
+    rng = np.random.default_rng(world)
+    for _ in range(50):
+        total, nblocks = int(rng.integers(0, 300000)), int(rng.integers(1, 5000))
+        rs = [sharded.shard_ranges(total, nblocks, r, world) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == total and rs[0][2] == 0 and rs[-1][3] == nblocks
+        for a, b in zip(rs, rs[1:]):
+            assert a[1] == b[0] and a[3] == b[2]
+        sizes = [r[1] - r[0] for r in rs]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ex = sharded.DistExchange()
+        n = 64
+        res = []
+        for step, counts in enumerate([(3, 5), (0, 0), (7, 2)]):
+            cnt = counts[rank]
+            send = torch.zeros(2 * n, dtype=torch.int32)
+            for e in range(cnt):
+                send[2 * e] = 100 * rank + e          # cell
+                send[2 * e + 1] = 1000 * rank + step  # element
+            recv = torch.full((2 * n * world,), -1, dtype=torch.int32)
+            part = torch.tensor([0.25 * (rank + 1) + step, float(cnt)], dtype=torch.float64)
+            part_all = torch.zeros(2 * world, dtype=torch.float64)
+            m = ex(send, recv, part, part_all)
+            res.append((m, part_all.tolist(), recv[: 2 * m * world].tolist()))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_exchange_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for step, counts in enumerate([(3, 5), (0, 0), (7, 2)]):
+        m = max(counts)
+        for rank in range(world):
+            got_m, part_all, recv = out[rank][step]
+            assert got_m == m
+            assert part_all == [0.25 * 1 + step, float(counts[0]), 0.25 * 2 + step, float(counts[1])]
+            for r in range(world):
+                seg = recv[2 * m * r: 2 * m * (r + 1)]
+                for e in range(counts[r]):
+                    assert seg[2 * e] == 100 * r + e and seg[2 * e + 1] == 1000 * r + step
+        assert out[0][step] == out[1][step]  # identical on every rank
