@@ -59,6 +59,9 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--no-smoothness", action="store_true")
+    p.add_argument("--sharded", action="store_true",
+                   help="N > 1: shard ONE grid over the ranks (strong scaling; sharded.py) instead of "
+                        "one independent grid per rank")
     return p.parse_args(argv)
 
 
@@ -354,12 +357,20 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dist = init_dist(world, "nccl")
     device = torch.device("cuda", local)
-    feats = synthetic.make(args.config, data_seed=rank, side=args.side)
+    sharded_run = args.sharded and world > 1
+    # independent grids: data seed = rank; sharded: every rank holds the same grid
+    feats = synthetic.make(args.config, data_seed=0 if sharded_run else rank, side=args.side)
     n, D = feats.shape
     side = math.isqrt(n)
     cfg = plas.SortConfig(rng_seed=0, rng_mode=args.mode, **WORKLOADS[args.config]["cfg"])
     dev = torch.from_numpy(feats).to(device)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
+    if sharded_run:
+        from paper_2312_13299_b200 import sharded
+        exchange = sharded.DistExchange()
+
+        def sort_on_device(x, c):  # noqa: F811 -- this rank's share of one sharded sort
+            return sharded.sort_on_device_sharded(x, c, rank, world, exchange)
 
     for _ in range(args.warmup):
         sort_on_device(dev, cfg)
@@ -386,7 +397,10 @@ def run_ours(args):
     if dist:
         dist.barrier()
     clocks = sampler.stop()
-    units, secs = combine(n * sum(passes), sum(step_ms) / 1e3, dist, device)
+    if sharded_run:  # one grid for the whole job: count its units once
+        units, secs = combine(n * sum(passes) / world, sum(step_ms) / 1e3, dist, device)
+    else:
+        units, secs = combine(n * sum(passes), sum(step_ms) / 1e3, dist, device)
     value = units / secs
     ms_per_step = secs * 1e3 / args.steps
 
@@ -398,7 +412,7 @@ def run_ours(args):
 
     # ---- e2e through the public API, pinned host features, perm back to host
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not sharded_run:
         host = torch.from_numpy(feats).pin_memory()
         plas.sort_grid(host, cfg)
         torch.cuda.synchronize()
@@ -419,7 +433,7 @@ def run_ours(args):
     # ---- per-kernel CUDA-event times (host-stepped replay of one sort)
     roofline = None
     kernel_ms = None
-    if not args.no_profile:
+    if not args.no_profile and not sharded_run:
         prof = _lib.SortProfile()
         perm_p = torch.empty(n, dtype=torch.int64, device=device)
         SortPlan(n, D, cfg).run(dev, perm_p, None, prof)
@@ -468,13 +482,16 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 data, f64 accumulate", "data": "synthetic",
+        "scaling": "strong" if sharded_run else "weak", "vs_baseline": None,
+        "dtype": "f32 data, f64 accumulate", "data": "synthetic",
         "config": {"workload": f"{args.config} {side}x{side}x{D} PLAS sort to convergence "
                                f"(BASELINE.json configs[{args.config[1]}])",
                    "side": side, "dim": D, "rng_mode": args.mode, "seed": 0,
                    "sort_config": WORKLOADS[args.config]["cfg"] or "SortConfig defaults",
                    "l2": "256 MiB buffer written before every timed step (outside the events)",
-                   "parallelism": f"{world} independent grid(s), one per rank"},
+                   "parallelism": (f"one grid sharded over {world} ranks (per-rank group ranges, NCCL "
+                                   "all-gather of moved cells + fp64 partials per pass)") if sharded_run
+                   else f"{world} independent grid(s), one per rank"},
         "quality": quality, "e2e": e2e, "roofline": roofline, "kernel_ms": kernel_ms, "smoothness": smooth,
         "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
     }

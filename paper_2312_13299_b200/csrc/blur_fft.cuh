@@ -135,6 +135,11 @@ __host__ __device__ constexpr int fft_twiddle_len(int lg) {
 __host__ __device__ constexpr int fft_pad(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int fft_buf_len(int L) { return L + L / 8; }
 
+// Large FFTs (L = 8192: two padded buffers would exceed shared memory) run
+// every pass in place in one buffer: all threads read their butterflies'
+// inputs, the CTA syncs, then all write.
+template <int LOG2L> __host__ __device__ constexpr bool fft_inplace() { return LOG2L >= 13; }
+
 // Stockham pass p of radix R: butterfly j reads v[r] = src[j + r L/R], applies
 // twiddles W_{Ns R}^{r k} (k = j mod Ns), runs the radix-R DFT and writes to
 // dst[(j - k) R + k + r Ns] (natural order after the last pass).
@@ -169,6 +174,10 @@ struct FftPass {
   template <bool SPEC>
   __device__ __forceinline__ static void run(const double2* src, double2* dst, int tid_, const double2* tw,
                                              const double* spec) {
+    if constexpr (fft_inplace<LOG2L>()) {
+      run_inplace<SPEC>(dst, tw, spec);
+      return;
+    }
     // the thread index is re-read per pass so no pass's (thread-only) twiddle
     // loads and addresses are hoisted into an earlier pass
     unsigned tid;
@@ -192,6 +201,42 @@ struct FftPass {
             o = make_double2(o.x * sp, -(o.y * sp));
           }
           dst[fft_pad(d)] = o;
+        }
+      }
+    }
+  }
+  // in place (src == dst): every thread reads, the CTA syncs, every thread writes
+  template <bool SPEC>
+  __device__ __forceinline__ static void run_inplace(double2* buf, const double2* tw, const double* spec) {
+    unsigned tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    double2 v[NB][R];
+#pragma unroll
+    for (int t = 0; t < NB; t++) {
+      const int j = (int)tid + t * T;
+      if (j < L / R) {
+        double2 wv[R];
+        load_twiddles(wv, j, tw);
+#pragma unroll
+        for (int r = 0; r < R; r++) v[t][r] = buf[fft_pad(j + r * (L / R))];
+        twiddle(v[t], wv);
+        dft_small<R>(v[t]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NB; t++) {
+      const int j = (int)tid + t * T;
+      if (j < L / R) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const int d = dest(j, r);
+          double2 o = v[t][r];
+          if (SPEC) {
+            const double sp = ld_ordered(spec + d);
+            o = make_double2(o.x * sp, -(o.y * sp));
+          }
+          buf[fft_pad(d)] = o;
         }
       }
     }
@@ -246,8 +291,8 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
   constexpr int NP = fft_npasses(LOG2L);
   extern __shared__ double2 fbuf[];
   double2* bufA = fbuf;
-  double2* bufB = fbuf + fft_buf_len(L);
-  float* raw = reinterpret_cast<float*>(fbuf + 2 * fft_buf_len(L));  // [2][n] input lines
+  double2* bufB = fft_inplace<LOG2L>() ? fbuf : fbuf + fft_buf_len(L);
+  float* raw = reinterpret_cast<float*>(fbuf + (fft_inplace<LOG2L>() ? 1 : 2) * fft_buf_len(L));  // [2][n] lines
   __shared__ double red[64];
   __shared__ int flist[FB_LOCAL];
   __shared__ int nflag;
@@ -426,7 +471,10 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
 }
 
 // shared memory of blur_fft_kernel for an L-point FFT
-inline size_t fft_smem_bytes(int L) { return sizeof(double2) * 2 * (size_t)fft_buf_len(L) + sizeof(float) * (size_t)L; }
+inline size_t fft_smem_bytes(int L) {
+  const size_t nbuf = L >= 8192 ? 1 : 2;  // fft_inplace
+  return sizeof(double2) * nbuf * (size_t)fft_buf_len(L) + sizeof(float) * (size_t)L;
+}
 
 // Real spectrum of the current level's symmetric kernel on L points:
 // K[m] = w0 + 2 sum_{j=1..h} w_j cos(2 pi j m / L), cosines from the twiddle

@@ -428,3 +428,12 @@ def test_sort_wide_rows_parity_vs_oracle(side, dim):
     assert rep.reorders == wrep["reorders"]
     np.testing.assert_allclose([v for _, t in rep.radius_trace for v in t],
                                [v for _, t in wrep["radius_trace"] for v in t], rtol=1e-12)
+
+
+def test_blur_fft_tier_in_place_8192():
+    """L = 8192 (4096-wide lines, configs[4]): the single-buffer in-place FFT variant."""
+    rng = np.random.default_rng(29)
+    g = rng.normal(0, 1, (8, 4096, 3)).astype(np.float32)
+    for r in (300.0, 2047.0):
+        got, fb = gblur.blur_target_tiers(g, r, 1)
+        np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"r={r} fb={fb}")
