@@ -1256,6 +1256,35 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
   const long long cells = (long long)H * W, tot = cells * C;
   const int eg = grid_for(tot, 256, 8);
   const double scale = coeff / (double)tot;
+  if (half_width <= 4) {  // fused single-kernel path (kernel_size <= 9)
+    if (half_width > 0 && !weights) return fail(PLAS_ERR_INVALID, "weights required");
+    const double one = 1.0;
+    CK(cudaMemcpyAsync(a.w, half_width > 0 ? weights : &one, sizeof(double) * (half_width + 1),
+                       cudaMemcpyHostToDevice, st));
+    const dim3 grid((W + SM_TS - 1) / SM_TS, (H + SM_TS - 1) / SM_TS);
+    const int nparts = (int)(grid.x * grid.y);
+    void* fn = nullptr;
+    size_t smem = 0;
+    switch (half_width) {
+      case 0: fn = (void*)smooth_fused_kernel<0>; smem = SmoothTile<0>::smem_doubles * 8; break;
+      case 1: fn = (void*)smooth_fused_kernel<1>; smem = SmoothTile<1>::smem_doubles * 8; break;
+      case 2: fn = (void*)smooth_fused_kernel<2>; smem = SmoothTile<2>::smem_doubles * 8; break;
+      case 3: fn = (void*)smooth_fused_kernel<3>; smem = SmoothTile<3>::smem_doubles * 8; break;
+      default: fn = (void*)smooth_fused_kernel<4>; smem = SmoothTile<4>::smem_doubles * 8; break;
+    }
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const double* pl = plane;
+    double* gr = grad;
+    const double* wd = a.w;
+    int Hh = H, Ww = W, Cc = C, det = detach_target;
+    double dl = huber_delta, sc = scale;
+    double* parts = a.t0;
+    void* args[] = {&pl, &gr, &Hh, &Ww, &Cc, &wd, &dl, &sc, &det, &parts};
+    CK(cudaLaunchKernel(fn, grid, dim3(256), args, smem, st));
+    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(a.t0, nparts, (double)tot, loss_dev);
+    CKL();
+    return PLAS_OK;
+  }
   if (half_width > 0) {
     if (!weights) return fail(PLAS_ERR_INVALID, "weights required");
     CK(cudaMemcpyAsync(a.w, weights, sizeof(double) * (half_width + 1), cudaMemcpyHostToDevice, st));

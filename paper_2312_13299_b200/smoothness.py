@@ -89,6 +89,7 @@ def smoothness_loss(stack, params=None, return_device=False):
     params = params or SmoothnessParams()
     loss = 0.0
     gradients = {}
+    means = []  # (coeff, device mean): one host sync at the end
     for name, plane in stack.planes.items():
         weight = params.weights.get(name, 0.0)
         coeff = params.overall_multiplier * weight
@@ -96,11 +97,15 @@ def smoothness_loss(stack, params=None, return_device=False):
         shape = tuple(plane.shape)
         size = int(np.prod(shape))
         if coeff == 0.0 or size == 0:
-            z = np.zeros(shape)
-            gradients[name] = torch.zeros(shape, dtype=torch.float64, device="cuda") if return_device else z
+            gradients[name] = (torch.zeros(shape, dtype=torch.float64, device="cuda") if return_device
+                               else np.zeros(shape))
             continue
         dev = _lib.to_device(plane if is_t else np.asarray(plane, dtype=np.float64), torch.float64)
         mean, grad = smoothness_plane_device(dev, coeff, params)
-        loss += coeff * float(mean.item())
+        means.append((coeff, mean))
         gradients[name] = grad if return_device else grad.cpu().numpy()
+    if means:
+        vals = torch.cat([m for _, m in means]).cpu().tolist()
+        for (coeff, _), v in zip(means, vals):
+            loss += coeff * float(v)  # smoothness.py:88, plane order
     return loss, gradients
