@@ -33,6 +33,7 @@
 // cache and the running sum for exactly those cells.
 #pragma once
 #include "common.cuh"
+#include "control.cuh"
 
 namespace plas {
 
@@ -302,10 +303,10 @@ template <bool PARITY>
 __device__ __forceinline__ unsigned group_local(const int* __restrict__ sel, long long sel_stride, int cls,
                                                 const unsigned (&keys)[6], int lb, int rb, unsigned m,
                                                 unsigned q, int s) {
-  if (PARITY) return (unsigned)__ldg(sel + (long long)cls * sel_stride + 4 * q + s);
-  Feistel fe;
-  fe.init_keys(keys, lb, rb, m);
-  return fe(4 * q + s);
+  // PARITY: host-exact master permutation filtered per class (class_select_kernel);
+  // DEVICE: the keyed bijections tabulated by gen_class_tables (the caller passes
+  // the buffer of this pass's parity)
+  return (unsigned)__ldg(sel + (long long)cls * sel_stride + 4 * q + s);
 }
 
 // l -> (ly, lx) = (l / ww, l % ww) with a float reciprocal (l < 2^24) and a +-1 fix
@@ -405,6 +406,9 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
   __shared__ PassShared ps;
   __shared__ int s_list[8 * WARP_LIST];
   load_pass_shared(ps, ctrl);
+  // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
+  const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
+  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
   int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
   int wcnt = 0;
   const int side = ctrl->side;
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
         k = rem >= 4 ? 4 : rem;
         if (s < k) {
           const int cls = ty * 3 + tx;
-          const unsigned l = group_local<PARITY>(sel, sel_stride, cls, ps.keys[cls], ps.bits[cls][0],
+          const unsigned l = group_local<PARITY>(selp, sel_stride, cls, ps.keys[cls], ps.bits[cls][0],
                                                  ps.bits[cls][1], m, q, s);
           int ly, lx;
           split_local(l, ww, __frcp_rn((float)ww), &ly, &lx);
@@ -545,6 +549,9 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
   __shared__ PassShared ps;
   __shared__ int s_list[8 * WARP_LIST];
   load_pass_shared(ps, ctrl);
+  // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
+  const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
+  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
   int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
   int wcnt = 0;
   const int side = ctrl->side;
@@ -601,7 +608,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
         const int rem = m - 4 * q;
         if (rem >= 2) k = rem >= 4 ? 4 : rem;
         if (s < k)
-          l = (int)group_local<PARITY>(sel, sel_stride, g.cls, ps.keys[g.cls], ps.bits[g.cls][0],
+          l = (int)group_local<PARITY>(selp, sel_stride, g.cls, ps.keys[g.cls], ps.bits[g.cls][0],
                                        ps.bits[g.cls][1], (unsigned)m, (unsigned)q, s);
       }
       int rowj[4];

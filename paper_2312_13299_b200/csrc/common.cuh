@@ -56,7 +56,17 @@ struct Ctrl {
   int rank, world;
   long long g_lo, g_hi;            // gather kernel: groups [g_lo, g_hi)
   int b_lo, b_hi;                  // tile kernel: blocks [b_lo, b_hi)
+  // DEVICE mode: this level's per-pass draws (dy, dx, grouping key), filled by
+  // pass_draws_kernel at level start for passes < PDRAW_MAX
+  const int4* pdraw;
+  const int* prec;                 // per-pass grouping records (PREC_INTS each), same level
+  int pdraw_level;                 // level the table holds (-1: none)
+  int gen_pass;                    // pass whose grouping tables gen_tables_kernel builds
 };
+
+constexpr int PDRAW_MAX = 1024;  // passes per level with precomputed draws (beyond: computed on the fly)
+// per-pass grouping record: m[9], lbits[9], rbits[9], keys[9][6]
+constexpr int PREC_INTS = 96;
 
 // Blocks whose feature + target rows fit in TILE_SMEM_MAX bytes of shared
 // memory are processed by the tile kernel (coalesced staging), larger blocks
@@ -315,8 +325,26 @@ __host__ __device__ __forceinline__ void set_pass_geometry(Ctrl* c, int dy, int 
 // DEVICE-mode per-pass draws: dy, dx and the grouping key come from the
 // Philox4x64-10 stream keyed like NumPy's (SeedSequence state), at counter
 // (block, pass, level, purpose) -- stateless, identical on every GPU.
+__host__ __device__ __forceinline__ void device_pass_draws_at(const Ctrl* c, int level, int pass, int* dy,
+                                                              int* dx, unsigned long long* gkey) {
+  DeviceDraw d;
+  d.init(c->key0, c->key1, (unsigned long long)pass, (unsigned long long)level, 0x504153535ull /* "PASS" */);
+  *dy = (int)d.bounded((unsigned)c->beta);
+  *dx = (int)d.bounded((unsigned)c->beta);
+  *gkey = d.next64();
+}
+
 __host__ __device__ __forceinline__ void device_pass_draws(const Ctrl* c, int* dy, int* dx,
                                                            unsigned long long* gkey) {
+#ifdef __CUDA_ARCH__
+  if (c->pdraw && c->pdraw_level == c->level && c->pass < PDRAW_MAX) {  // precomputed at level start
+    const int4 v = c->pdraw[c->pass];
+    *dy = v.x;
+    *dx = v.y;
+    *gkey = ((unsigned long long)(unsigned)v.w << 32) | (unsigned)v.z;
+    return;
+  }
+#endif
   DeviceDraw d;
   d.init(c->key0, c->key1, (unsigned long long)c->pass, (unsigned long long)c->level,
          0x504153535ull /* "PASS" */);

@@ -91,6 +91,42 @@ __device__ __forceinline__ double cell_dist2(const float* __restrict__ a, const 
   return (p[0] + p[1]) + (p[2] + p[3]);
 }
 
+// cell_dist2 for rows of exactly NCH float4 chunks with every load issued
+// before the first use (same evaluation order, same value).
+template <int NCH>
+__device__ __forceinline__ double cell_dist2_fixed(const float* __restrict__ a, const float* __restrict__ b, int D) {
+  float4 x[NCH], y[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    x[c] = __ldg(reinterpret_cast<const float4*>(a) + c);
+    y[c] = __ldg(reinterpret_cast<const float4*>(b) + c);
+  }
+  double p[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int c = 0; c < NCH; c++) {
+    const float xs[4] = {x[c].x, x[c].y, x[c].z, x[c].w}, ys[4] = {y[c].x, y[c].y, y[c].z, y[c].w};
+    double acc = p[c & 3];
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+      if (4 * c + e < D) {
+        const double df = (double)xs[e] - (double)ys[e];
+        acc = fma(df, df, acc);
+      }
+    p[c & 3] = acc;
+  }
+  return (p[0] + p[1]) + (p[2] + p[3]);
+}
+
+__device__ __forceinline__ double cell_dist2_any(const float* a, const float* b, int D, int S) {
+  switch (S) {
+    case 4: return cell_dist2_fixed<1>(a, b, D);
+    case 8: return cell_dist2_fixed<2>(a, b, D);
+    case 12: return cell_dist2_fixed<3>(a, b, D);
+    case 16: return cell_dist2_fixed<4>(a, b, D);
+    default: return cell_dist2(a, b, D, S);
+  }
+}
+
 // fixed-order fp64 reduction of `nparts` partials by one CTA (thread 0 result)
 __device__ __forceinline__ double reduce_partials(const double* partials, int nparts, double* sh) {
   double s = 0.0;
@@ -139,6 +175,49 @@ __device__ __host__ __forceinline__ bool level_uses_fft(int h, int side, int fft
   return fft_min_h > 0 && fft_L > 0 && h >= fft_min_h && side + h <= fft_L;
 }
 
+// DEVICE mode, level start: every pass's draws of this level (stateless in
+// (level, pass)), so no kernel on the per-pass critical path runs Philox.
+__global__ void pass_draws_kernel(Ctrl* c, int4* __restrict__ pdraw, int* __restrict__ prec) {
+  // one thread per (pass, class) item (item 9 stores the draws): every chain is
+  // one Philox block plus at most one Feistel key setup
+  const int level = c->level;
+  const int beta = c->beta, side = c->side;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < PDRAW_MAX * 16; t += gridDim.x * blockDim.x) {
+    const int p = t >> 4, item = t & 15;
+    if (item > 9) continue;
+    int dy, dx;
+    unsigned long long gk;
+    device_pass_draws_at(c, level, p, &dy, &dx, &gk);
+    if (item == 9) {
+      pdraw[p] = make_int4(dy, dx, (int)(unsigned)gk, (int)(unsigned)(gk >> 32));
+      continue;
+    }
+    // class `item`: its shape (set_pass_geometry_base) and keys (set_class_keys)
+    const int cls = item, ty = cls / 3, tx = cls % 3;
+    const int fy = dy > 0 ? dy : beta, fx = dx > 0 ? dx : beta;
+    const int nby = num_segments(fy, beta, side), nbx = num_segments(fx, beta, side);
+    int lo, hi, hh, ww;
+    if (ty == 1) hh = beta;
+    else { segment(ty == 0 ? 0 : nby - 1, fy, beta, side, &lo, &hi); hh = hi - lo; }
+    if (tx == 1) ww = beta;
+    else { segment(tx == 0 ? 0 : nbx - 1, fx, beta, side, &lo, &hi); ww = hi - lo; }
+    auto exists = [](int tt, int nn) { return tt == 0 || (tt == 2 && nn >= 2) || (tt == 1 && nn >= 3); };
+    const unsigned m = (unsigned)(hh * ww);
+    Feistel fe;
+    fe.init(class_key(gk, hh, ww), m);
+    int* r = prec + (long long)p * PREC_INTS;
+    r[cls] = (exists(ty, nby) && exists(tx, nbx)) ? (int)m : 0;
+    r[9 + cls] = fe.lbits;
+    r[18 + cls] = fe.rbits;
+    for (int k = 0; k < 6; k++) r[27 + 6 * cls + k] = (int)fe.keys[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c->pdraw = pdraw;
+    c->prec = prec;
+    c->pdraw_level = level;
+  }
+}
+
 __global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_cond) {
   if (threadIdx.x) return;
   const int lv = c->level;
@@ -150,19 +229,108 @@ __global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_con
   c->level_done = 0;
 }
 
+// The controller's serial tail works on a shared-memory copy of Ctrl: one
+// coalesced copy in and out instead of a chain of dependent global accesses.
+__device__ __forceinline__ void ctrl_to_smem(Ctrl* dst, const Ctrl* src) {
+  static_assert(sizeof(Ctrl) % 4 == 0, "Ctrl is copied as 32-bit words");
+  const int* s = reinterpret_cast<const int*>(src);
+  int* d = reinterpret_cast<int*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += blockDim.x) d[i] = s[i];
+  __syncthreads();
+}
+__device__ __forceinline__ void ctrl_from_smem(Ctrl* dst, const Ctrl* src) {
+  __syncthreads();
+  const int* s = reinterpret_cast<const int*>(src);
+  int* d = reinterpret_cast<int*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += blockDim.x) d[i] = s[i];
+}
+
+// DEVICE mode: the class groupings of pass `pass` of the current level as
+// tables tab[cls * stride + l] = Feistel_cls(l), l < m_cls (the keyed
+// bijections of common.cuh).  Draws are stateless in (level, pass), so every
+// CTA derives the pass's geometry and keys itself and fills its slice of the
+// tables; the pass kernel then looks groupings up instead of evaluating the
+// Feistel network (and its cycle walk) per lane.  Called by all threads.
+__device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* __restrict__ tab0, long long stride,
+                                                 int worker = -1, int nworkers = 0) {
+  if (worker < 0) {
+    worker = blockIdx.x;
+    nworkers = gridDim.x;
+  }
+  int* __restrict__ tab = tab0 + (long long)(pass & 1) * 9 * stride;  // double-buffered by pass parity
+  {
+    // fast path: the pass's record precomputed at level start (pass_draws_kernel)
+    const int* prec = cg->prec;
+    const bool ok = prec && cg->pdraw_level == cg->level && pass < PDRAW_MAX;
+    if (ok) {
+      __shared__ int rec[PREC_INTS];
+      for (int i = threadIdx.x; i < PREC_INTS; i += blockDim.x) rec[i] = prec[(long long)pass * PREC_INTS + i];
+      __syncthreads();
+      const long long per = (long long)blockDim.x * nworkers;
+      for (int cls = 0; cls < 9; cls++) {
+        const unsigned m = (unsigned)rec[cls];
+        if (!m) continue;
+        Feistel fe;
+        fe.init_keys(reinterpret_cast<const unsigned*>(rec + 27 + 6 * cls), rec[9 + cls], rec[18 + cls], m);
+        for (long long l = worker * (long long)blockDim.x + threadIdx.x; l < m; l += per)
+          tab[cls * stride + l] = (int)fe((unsigned)l);
+      }
+      return;
+    }
+  }
+  __shared__ Ctrl nx;
+  __shared__ unsigned long long gk;
+  __shared__ int mcls[10];
+  ctrl_to_smem(&nx, cg);
+  if (threadIdx.x == 0) {
+    nx.pass = pass;
+    int dy, dx;
+    device_pass_draws(&nx, &dy, &dx, &gk);
+    set_pass_geometry_base(&nx, dy, dx);
+  }
+  __syncthreads();
+  if (threadIdx.x < 9) {
+    set_class_keys(&nx, threadIdx.x, gk);
+    // classes that do not exist in this pass get m = 0
+    const int ty = threadIdx.x / 3, tx = threadIdx.x % 3;
+    auto exists = [](int t, int n) { return t == 0 || (t == 2 && n >= 2) || (t == 1 && n >= 3); };
+    mcls[threadIdx.x] = (exists(ty, nx.nby) && exists(tx, nx.nbx)) ? nx.seg_h[ty] * nx.seg_w[tx] : 0;
+  }
+  __syncthreads();
+  const long long per = (long long)blockDim.x * nworkers;
+  for (int cls = 0; cls < 9; cls++) {
+    const unsigned m = (unsigned)mcls[cls];
+    if (!m) continue;
+    Feistel fe;
+    fe.init_keys(nx.fe_keys[cls], nx.fe_lbits[cls], nx.fe_rbits[cls], m);
+    for (long long l = worker * (long long)blockDim.x + threadIdx.x; l < m; l += per)
+      tab[cls * stride + l] = (int)fe((unsigned)l);
+  }
+}
+
+// DEVICE mode: tables of the next pass, built concurrently with the pass
+// statistics (the graph runs this kernel and pass_stats_kernel in parallel;
+// gen_pass was set by the pass kernel, so the controller's update of pass
+// does not race with it).
+__global__ void __launch_bounds__(256) gen_tables_kernel(const Ctrl* c, int* tab, long long stride) {
+  gen_class_tables(c, c->gen_pass, tab, stride);
+}
+
 // Last-CTA-done protocol: every CTA writes its partial, fences and takes a
 // ticket; the CTA with the last ticket sees all partials, reduces them in a
 // fixed order (deterministic) and runs the controller.  Returns true there.
 __device__ __forceinline__ bool last_cta_reduce(double v, double* partials, int* done, double* total,
-                                                double* sh) {
-  __shared__ int s_last;
+                                                double* sh, int* ticket = nullptr) {
+  __shared__ int s_last, s_ticket;
   const double blk = block_sum<RED_THREADS>(v, sh);
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = blk;
     __threadfence();
-    s_last = atomicAdd(done, 1) == (int)gridDim.x - 1;
+    s_ticket = atomicAdd(done, 1);
+    s_last = s_ticket == (int)gridDim.x - 1;
   }
   __syncthreads();
+  if (ticket) *ticket = s_ticket;
   if (!s_last) return false;
   __threadfence();
   double t = 0.0;
@@ -181,7 +349,7 @@ __device__ __forceinline__ bool last_cta_reduce(double v, double* partials, int*
 __global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, long long n, int D, int S, double* partials, int* done,
-    unsigned long long inner, unsigned long long tile_cond) {
+    unsigned long long inner, unsigned long long tile_cond, int* tab, long long tab_stride) {
   __shared__ double sh[32];
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
@@ -192,7 +360,17 @@ __global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
     dcache[i] = d;
     sum += d;
   }
-  if (!last_cta_reduce(sum, partials, done, &s_tot, sh)) return;
+  const bool gen = tab && c->rng_mode == 1;
+  int ticket = 0;
+  if (!last_cta_reduce(sum, partials, done, &s_tot, sh, &ticket)) {
+    // pass 0's tables, built by the other CTAs (ticket order) while the last one finishes
+    if (gen) gen_class_tables(c, 0, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
+    return;
+  }
+  __shared__ Ctrl sc;
+  Ctrl* const cg = c;
+  ctrl_to_smem(&sc, cg);
+  c = &sc;
   bool go = false;
   if (threadIdx.x == 0) {
     const double tot = s_tot;
@@ -208,12 +386,15 @@ __global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
     }
   }
   go = __syncthreads_or(go);
-  if (!go) return;
-  if (c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
-  if (threadIdx.x == 0) {
-    if (c->rng_mode == 1) set_cond(tile_cond, c->tile);
-    set_cond(inner, 1);
+  if (go) {
+    if (c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
+    if (threadIdx.x == 0) {
+      if (c->rng_mode == 1) set_cond(tile_cond, c->tile);
+      set_cond(inner, 1);
+    }
   }
+  ctrl_from_smem(cg, &sc);
+  if (gen && gridDim.x == 1) gen_class_tables(&sc, 0, tab, tab_stride, 0, 1);
 }
 
 // Strike logic of one finished pass (plas.py:266-272) given the summed fp64
@@ -260,33 +441,73 @@ __global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
     double* partials, int* done, long long n, unsigned long long inner, unsigned long long tile_cond,
-    double* xpart) {
+    double* xpart, int* tab, long long tab_stride) {
   __shared__ double sh[32];
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
   const int count = counters[2];
   double sum = 0.0;
   const int stride = gridDim.x * blockDim.x;
-  // four independent cells per thread in flight
-  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < count; e0 += 4 * stride) {
-    long long cell[4];
-    double old[4];
+  // two independent cells per thread in flight, every row load issued first
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < count; e0 += 2 * stride) {
+    long long cell[2];
+    double old[2];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < 2; u++) {
       const int e = e0 + u * stride;
       cell[u] = e < count ? list[e] : -1;
       old[u] = cell[u] >= 0 ? dcache[cell[u]] : 0.0;
     }
+    if (S == 16 && cell[1] >= 0) {  // the common case: both rows sets in flight together
+      float4 x[2][4], y[2][4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      if (cell[u] >= 0) {
-        const double d = sqrt(cell_dist2(feat + cell[u] * S, target + cell[u] * S, D, S));
+      for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          x[u][c] = __ldg(reinterpret_cast<const float4*>(feat + cell[u] * 16) + c);
+          y[u][c] = __ldg(reinterpret_cast<const float4*>(target + cell[u] * 16) + c);
+        }
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        double p[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+          const float xs[4] = {x[u][c].x, x[u][c].y, x[u][c].z, x[u][c].w};
+          const float ys[4] = {y[u][c].x, y[u][c].y, y[u][c].z, y[u][c].w};
+          double acc = 0.0;
+#pragma unroll
+          for (int e = 0; e < 4; e++)
+            if (4 * c + e < D) {
+              const double df = (double)xs[e] - (double)ys[e];
+              acc = fma(df, df, acc);
+            }
+          p[c] = acc;
+        }
+        const double d = sqrt((p[0] + p[1]) + (p[2] + p[3]));
         sum += d - old[u];
         dcache[cell[u]] = d;
       }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        if (cell[u] >= 0) {
+          const double d = sqrt(cell_dist2_any(feat + cell[u] * S, target + cell[u] * S, D, S));
+          sum += d - old[u];
+          dcache[cell[u]] = d;
+        }
+      }
     }
   }
-  if (!last_cta_reduce(sum, partials, done, &s_tot, sh)) return;
+  // DEVICE mode: every CTA builds its slice of the next pass's grouping tables
+  // AFTER taking its ticket, so the slices are built while the last CTA runs
+  // the controller instead of delaying it (gen_pass was set by the pass kernel;
+  // the controller's writes to Ctrl leave the fields read here unchanged)
+  const bool gen = tab && c->rng_mode == 1;
+  int ticket = 0;
+  if (!last_cta_reduce(sum, partials, done, &s_tot, sh, &ticket)) {
+    if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
+    return;
+  }
   if (c->world > 1) {
     if (threadIdx.x == 0) {
       xpart[0] = s_tot;
@@ -294,6 +515,10 @@ __global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
     }
     return;
   }
+  __shared__ Ctrl sc;
+  Ctrl* const cg = c;
+  ctrl_to_smem(&sc, cg);
+  c = &sc;
   bool more = false;
   if (threadIdx.x == 0) {
     counters[0] += count;
@@ -301,9 +526,12 @@ __global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
     more = controller_step(c, s, s_tot, n, inner);
   }
   more = __syncthreads_or(more);
-  if (!more || c->rng_mode != 1) return;
-  prepare_device_pass_cta(c, &s_gkey);
-  if (threadIdx.x == 0) set_cond(tile_cond, c->tile);
+  if (more && c->rng_mode == 1) {
+    prepare_device_pass_cta(c, &s_gkey);
+    if (threadIdx.x == 0) set_cond(tile_cond, c->tile);
+  }
+  ctrl_from_smem(cg, &sc);
+  if (gen && gridDim.x == 1) gen_class_tables(&sc, sc.pass, tab, tab_stride, 0, 1);
 }
 
 // ---------------------------------------------------------------- sharding

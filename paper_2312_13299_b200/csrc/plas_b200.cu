@@ -172,6 +172,8 @@ struct SortWs {
   double* weights;
   long long* level_counts;
   double* trace;
+  int4* pdraw;  // DEVICE: per-pass draws of the current level
+  int* prec;    // DEVICE: per-pass grouping records (class shapes + Feistel keys)
   int* mp;   // parity: master permutation (beta0^2)
   int* sel;  // parity: 9 class selections
   long long sel_stride;
@@ -292,9 +294,13 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->level_counts = c.take<long long>(std::max(L, 1));
   w->trace = c.take<double>(std::max(tcap, 1LL));
   long long b0 = side;  // beta0 <= side
-  w->sel_stride = rng_mode == PLAS_RNG_PARITY ? b0 * b0 : 0;
+  // per-class grouping tables: PARITY (class_select_kernel) and DEVICE (gen_class_tables)
+  w->sel_stride = b0 * b0;
   w->mp = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(b0 * b0) : 1);
-  w->sel = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(9 * b0 * b0) : 1);
+  // two buffers in DEVICE mode (pass parity: pass p reads one while building p + 1's)
+  w->sel = c.take<int>((size_t)((rng_mode == PLAS_RNG_PARITY ? 9 : 18) * b0 * b0));
+  w->pdraw = c.take<int4>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX);
+  w->prec = c.take<int>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX * PREC_INTS);
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS);
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
@@ -397,7 +403,15 @@ int tile_grid_size(int S) {
 // Capacity of the moved-cell list: every cell changes element at most once per pass.
 long long list_capacity(long long n) { return n; }
 
-int stats_grid_size() { return std::min(num_sms() * 4, MAX_PARTS); }
+int stats_grid_size() {
+  static int g = 0;
+  if (!g) {
+    const char* e = getenv("PLAS_STATS_CTAS_PER_SM");
+    const int per = e ? std::max(1, atoi(e)) : 4;
+    g = std::min(num_sms() * per, MAX_PARTS);
+  }
+  return g;
+}
 
 }  // namespace
 
@@ -506,6 +520,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.fft_L = w.fft_L;
   hc.rank = world > 1 ? a->rank : 0;
   hc.world = world;
+  hc.pdraw = nullptr;
+  hc.prec = nullptr;
+  hc.pdraw_level = -1;
   CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
   // zero halos of the padded blur buffers, pad channels, fallback counters
@@ -635,7 +652,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     cudaGraphNode_t nd[8];
     CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
                   (unsigned long long)blur_h));
-    CK(add_kernel(&nd[1], obody, &nd[0], 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
+    cudaGraphNode_t nd_draws;
+    CK(add_kernel(&nd_draws, obody, &nd[0], 1, pass_draws_kernel, dim3(PDRAW_MAX * 16 / 256), dim3(256), w.ctrl,
+                  w.pdraw, w.prec));
+    CK(add_kernel(&nd[1], obody, &nd_draws, 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
                   w.rowweight, side, lc.lvl));
     CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight_kernel, dim3(lc.den_grid), dim3(256),
                   (const double*)w.rowweight, w.den32, (double*)nullptr, side, side, lc.lvl));
@@ -699,13 +719,13 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     nd[4] = blur_if;
     CK(add_kernel(&nd[5], obody, &nd[4], 1, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
                   w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
-                  w.spart, done, (unsigned long long)inner_h, (unsigned long long)tile_h));
+                  w.spart, done, (unsigned long long)inner_h, (unsigned long long)tile_h, w.sel, w.sel_stride));
     cudaGraphNode_t inner_node;
     cudaGraph_t ibody;
     CK(add_while(&inner_node, obody, &nd[5], 1, inner_h, &ibody));
     CK(add_kernel(&nd[6], obody, &inner_node, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl,
                   lc.sched, (unsigned long long)outer_h));
-    cudaGraphNode_t if_node, pn[3];
+    cudaGraphNode_t if_node, pn[3];  // [0] tile, [1] gather, [2] statistics
     cudaGraph_t if_bodies[2];
     {
       cudaGraphNodeParams p{};
@@ -722,8 +742,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       int* idx = w.idx;
       const float* target = w.target;
       const Ctrl* ctrl = w.ctrl;
-      const int* sel = nullptr;
-      long long sstride = 0;
+      const int* sel = w.sel;  // DEVICE-mode tables (gen_class_tables)
+      long long sstride = w.sel_stride;
       int Dv = D, Sv = S;
       void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &ml, &counters};
       cudaKernelNodeParams kp{};
@@ -742,7 +762,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(add_kernel(&pn[2], ibody, &if_node, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl,
                   lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, D, S,
                   (const int*)w.list, counters, w.spart, done, n, (unsigned long long)inner_h,
-                  (unsigned long long)tile_h, (double*)nullptr));
+                  (unsigned long long)tile_h, (double*)nullptr, w.sel, w.sel_stride));  // + next pass's tables
     cudaGraphExec_t ge;
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
@@ -799,7 +819,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     for (int lv = 0; lv < L; lv++) {
       const int beta = sch.betas[lv];
       const long long bsq = (long long)beta * beta;
-      timed(K_CTRL, [&] { level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull); });
+      timed(K_CTRL, [&] {
+        level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull);
+        if (!parity) pass_draws_kernel<<<PDRAW_MAX * 16 / 256, 256, 0, st>>>(w.ctrl, w.pdraw, w.prec);
+      });
       const bool use_fft = level_uses_fft(sch.hs[lv], side, hc.fft_min_h, hc.fft_L);
       timed(K_BORDER, [&] {
         border_rows_kernel<<<lc.rows_grid, 128, 0, st>>>(w.rowweight, side, lc.lvl);
@@ -853,7 +876,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       }
       timed(K_DIST, [&] {
         level_stats_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, n,
-                                                                 D, S, w.spart, done, 0, 0);
+                                                                 D, S, w.spart, done, 0, 0,
+                                                                 parity ? nullptr : w.sel, w.sel_stride);
       });
       CKL();
       int dy = 0, dx = 0;
@@ -875,8 +899,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           int* idx = w.idx;
           const float* target = w.target;
           const Ctrl* ctrl = w.ctrl;
-          const int* sel = parity ? w.sel : nullptr;
-          long long sstride = parity ? w.sel_stride : 0;
+          const int* sel = w.sel;  // PARITY: class_select_kernel; DEVICE: gen_class_tables
+          long long sstride = w.sel_stride;
           int Dv = D, Sv = S;
           void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &ml, &counters};
           cudaError_t le = cudaSuccess;
@@ -894,7 +918,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         }
         timed(K_CTRL, [&] {
           pass_stats_kernel<<<sgrid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, D, S,
-                                                           w.list, counters, w.spart, done, n, 0, 0, a->xchg_part);
+                                                           w.list, counters, w.spart, done, n, 0, 0, a->xchg_part,
+                                                           parity || world > 1 ? nullptr : w.sel, w.sel_stride);
+          if (!parity && world > 1) gen_tables_kernel<<<num_sms(), 256, 0, st>>>(w.ctrl, w.sel, w.sel_stride);
         });
         CKL();
         if (world > 1) {
