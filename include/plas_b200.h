@@ -162,7 +162,8 @@ int plas_blur(const void* in, void* out, int dtype, int H, int W, int C, const d
               int half_width, int op, void* ws, size_t ws_bytes, void* stream);
 
 /* blur_target (plas.py:64-68) of an (H, W, C) f32 grid through the SORT's
- * level-blur tiers: tier 0 = direct fast fold, tier 1 = FFT convolution; both
+ * level-blur tiers: tier 0 = direct fast fold, tier 1 = FFT convolution,
+ * tier 2 = one-kernel tile blur (half_width <= 16); all
  * certify every output against the SciPy fold and recompute the uncertain
  * ones exactly, so the result is bit-identical to the reference.  weights:
  * host [half_width + 1], centre first.  fallbacks: optional host [2] out, the

@@ -240,3 +240,142 @@ __global__ void fb_reset_kernel(int* fb) {
 }
 
 }  // namespace plas
+
+namespace plas {
+
+// ---------------------------------------------------------------------------
+// Small-radius tier (h <= TB_HMAX): the whole level blur in one kernel.  A CTA
+// owns a TB_T x TB_T tile of target cells and, per float4 channel group,
+//   stages the input tile + h halo in shared memory,
+//   axis 0: fast fold + certificate (fp32(acc - B) == fp32(acc + B)); the
+//           uncertain outputs take the exact SciPy fold inline (blur.cuh),
+//   axis 1: the same on the staged axis-0 rows, then / den32.
+// Bit-identical to blur_pad_kernel + blur_pad_fallback_kernel (same
+// certificate bound with M = the tile's max |x|, same exact fold), with one
+// read of the grid and one write of the target, and no fallback kernels.
+constexpr int TB_T = 32;
+constexpr int TB_HMAX = 16;
+constexpr int TB_THREADS = 256;
+
+__host__ __device__ constexpr size_t tile_blur_smem_bytes(int h) {
+  return sizeof(double2) * ((size_t)(TB_T + 2 * h) * (TB_T + 2 * h) + (size_t)TB_T * (TB_T + 2 * h));
+}
+
+// exact SciPy fold of one staged channel at stride `st` doubles (centre x)
+__device__ __forceinline__ double tb_exact(const double* x, int st, const double* w, int h) {
+  double acc = __dmul_rn(x[0], w[0]);
+  for (int j = h; j >= 1; j--) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(x[-j * st], x[j * st]), w[j]));
+  return acc;
+}
+
+// Channels are processed in pairs staged as double2 (each input converted to
+// fp64 once; the folds then read fp64 from shared memory).
+__global__ void __launch_bounds__(TB_THREADS) blur_tile_kernel(const float* __restrict__ feat, float* __restrict__ target,
+                                                               PadGeom pg, BlurLevelRef lvl,
+                                                               const float* __restrict__ den32) {
+  extern __shared__ double2 tsm2[];
+  __shared__ double w[TB_HMAX + 1];
+  __shared__ float red[TB_THREADS / 32];
+  int h;
+  const double* wg;
+  lvl.get(&h, &wg);
+  if (threadIdx.x <= h) w[threadIdx.x] = wg[threadIdx.x];
+  const int H = pg.H, W = pg.W, C = pg.C, S = pg.S;
+  const int NI = TB_T + 2 * h;   // staged side
+  double2* in = tsm2;            // [NI][NI]
+  double2* tmp = tsm2 + NI * NI;  // [TB_T][NI] (fp32-rounded axis-0 values)
+  const int y0 = blockIdx.y * TB_T, x0 = blockIdx.x * TB_T;
+  const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int cp = 0; cp < (C + 1) / 2; cp++) {
+    const bool has_b = 2 * cp + 1 < C;
+    // ---- stage the input tile (rows outside [0, H) are feat's zero halo rows)
+    float mx = 0.f;
+    for (int e = threadIdx.x; e < NI * NI; e += TB_THREADS) {
+      const int r = e / NI, cc = e - r * NI;
+      const int y = y0 - h + r, x = x0 - h + cc;
+      float2 v = make_float2(0.f, 0.f);
+      if (x >= 0 && x < W && y < H + pg.pad)
+        v = __ldg(reinterpret_cast<const float2*>(feat + ((long long)y * W + x) * S) + cp);
+      in[e] = make_double2((double)v.x, (double)v.y);
+      mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(PLAS_FULL_MASK, mx, o));
+    if (lane == 0) red[wid] = mx;
+    __syncthreads();
+    float M0 = 0.f;
+    for (int i = 0; i < TB_THREADS / 32; i++) M0 = fmaxf(M0, red[i]);
+    const double B0 = bscale * (double)M0;
+    // ---- axis 0: rows [h, h + T) of the stage, every staged column
+    float mx1 = 0.f;
+    for (int e = threadIdx.x; e < TB_T * NI; e += TB_THREADS) {
+      const int r = e / NI, cc = e - r * NI;
+      const int x = x0 - h + cc;
+      double2 o = make_double2(0.0, 0.0);
+      if (x >= 0 && x < W && y0 + r < H) {
+        const double2* colp = in + (r + h) * NI + cc;
+        const double2 xc = colp[0];
+        double a0 = __dmul_rn(xc.x, w[0]), a1 = __dmul_rn(xc.y, w[0]);
+        for (int j = h; j >= 1; j--) {
+          const double2 lo = colp[-j * NI], hi = colp[j * NI];
+          const double wj = w[j];
+          a0 = fma(__dadd_rn(lo.x, hi.x), wj, a0);
+          a1 = fma(__dadd_rn(lo.y, hi.y), wj, a1);
+        }
+        float r0 = __double2float_rn(a0), r1 = 0.f;
+        if (__double2float_rn(__dsub_rn(a0, B0)) != __double2float_rn(__dadd_rn(a0, B0)))
+          r0 = __double2float_rn(tb_exact(reinterpret_cast<const double*>(colp), 2 * NI, w, h));
+        if (has_b) {
+          r1 = __double2float_rn(a1);
+          if (__double2float_rn(__dsub_rn(a1, B0)) != __double2float_rn(__dadd_rn(a1, B0)))
+            r1 = __double2float_rn(tb_exact(reinterpret_cast<const double*>(colp) + 1, 2 * NI, w, h));
+        }
+        o = make_double2((double)r0, (double)r1);
+        mx1 = fmaxf(mx1, fmaxf(fabsf(r0), fabsf(r1)));
+      }
+      tmp[e] = o;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx1 = fmaxf(mx1, __shfl_xor_sync(PLAS_FULL_MASK, mx1, o));
+    __syncthreads();  // red[] reuse + tmp complete
+    if (lane == 0) red[wid] = mx1;
+    __syncthreads();
+    float M1 = 0.f;
+    for (int i = 0; i < TB_THREADS / 32; i++) M1 = fmaxf(M1, red[i]);
+    const double B1 = bscale * (double)M1;
+    // ---- axis 1 on the staged rows, / den32, store
+    for (int e = threadIdx.x; e < TB_T * TB_T; e += TB_THREADS) {
+      const int r = e / TB_T, cc = e - r * TB_T;
+      const int y = y0 + r, x = x0 + cc;
+      if (y >= H || x >= W) continue;
+      const double2* rowp = tmp + r * NI + cc + h;
+      const float dn = den32[(long long)y * W + x];
+      const double2 xc = rowp[0];
+      double a0 = __dmul_rn(xc.x, w[0]), a1 = __dmul_rn(xc.y, w[0]);
+      for (int j = h; j >= 1; j--) {
+        const double2 lo = rowp[-j], hi = rowp[j];
+        const double wj = w[j];
+        a0 = fma(__dadd_rn(lo.x, hi.x), wj, a0);
+        a1 = fma(__dadd_rn(lo.y, hi.y), wj, a1);
+      }
+      float r0 = __double2float_rn(a0), r1 = 0.f;
+      if (__double2float_rn(__dsub_rn(a0, B1)) != __double2float_rn(__dadd_rn(a0, B1)))
+        r0 = __double2float_rn(tb_exact(reinterpret_cast<const double*>(rowp), 2, w, h));
+      r0 = __fdiv_rn(r0, dn);
+      float* dst = target + ((long long)y * W + x) * S + 2 * cp;
+      if (has_b) {
+        r1 = __double2float_rn(a1);
+        if (__double2float_rn(__dsub_rn(a1, B1)) != __double2float_rn(__dadd_rn(a1, B1)))
+          r1 = __double2float_rn(tb_exact(reinterpret_cast<const double*>(rowp) + 1, 2, w, h));
+        r1 = __fdiv_rn(r1, dn);
+        *reinterpret_cast<float2*>(dst) = make_float2(r0, r1);
+      } else {
+        dst[0] = r0;
+      }
+    }
+    __syncthreads();  // stage / tmp reuse by the next channel pair
+  }
+}
+
+}  // namespace plas

@@ -52,6 +52,7 @@ struct Ctrl {
   int tile;                        // this pass runs the shared-memory tile kernel
   int fft_min_h;                   // levels with h >= fft_min_h (> 0) blur by FFT
   int fft_L;                       // FFT length (0 = no FFT tier)
+  int tile_blur_hmax;              // levels with h <= this (and not FFT) blur in one tile kernel
   // multi-GPU sharding (world > 1): this rank's share of the pass
   int rank, world;
   long long g_lo, g_hi;            // gather kernel: groups [g_lo, g_hi)

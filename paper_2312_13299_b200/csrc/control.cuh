@@ -218,12 +218,18 @@ __global__ void pass_draws_kernel(Ctrl* c, int4* __restrict__ pdraw, int* __rest
   }
 }
 
-__global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_cond) {
+__device__ __host__ __forceinline__ bool level_uses_tile_blur(int h, int side, int fft_min_h, int fft_L,
+                                                              int tile_hmax) {
+  return !level_uses_fft(h, side, fft_min_h, fft_L) && h <= tile_hmax;
+}
+
+__global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_cond, unsigned long long tblur_cond) {
   if (threadIdx.x) return;
   const int lv = c->level;
   c->beta = s.betas[lv];
   c->h = s.hs[lv];
   set_cond(blur_cond, level_uses_fft(c->h, c->side, c->fft_min_h, c->fft_L) ? 1u : 0u);
+  set_cond(tblur_cond, level_uses_tile_blur(c->h, c->side, c->fft_min_h, c->fft_L, c->tile_blur_hmax) ? 1u : 0u);
   c->pass = 0;
   c->strikes = 0;
   c->level_done = 0;

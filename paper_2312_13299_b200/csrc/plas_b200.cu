@@ -229,6 +229,16 @@ int fft_min_h() {
   return v;
 }
 
+// largest half-width of the one-kernel tile blur (0 = off); PLAS_TILE_BLUR_HMAX overrides
+int tile_blur_hmax() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PLAS_TILE_BLUR_HMAX");
+    v = e ? std::min(std::max(atoi(e), 0), TB_HMAX) : 4;  // measured best at C2 (tile kernel is latency-bound above)
+  }
+  return v;
+}
+
 // relative error constant of the FFT convolution (blur_fft.cuh), x2 safety
 double fft_error_constant(int log2L) {
   const double u = ldexp(1.0, -53);
@@ -347,6 +357,7 @@ struct Launch {
   int S, D, side;
   long long n;
   int blur_grid, fb_grid, den_grid, rows_grid, dist_grid, pass_grid, tile_grid, vad_grid;
+  dim3 tb_grid;
   PadGeom pg;
   BlurLevelRef lvl;
   Sched sched;
@@ -518,6 +529,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.key1 = key[1];
   hc.fft_min_h = fft_min_h();
   hc.fft_L = w.fft_L;
+  hc.tile_blur_hmax = tile_blur_hmax();
   hc.rank = world > 1 ? a->rank : 0;
   hc.world = world;
   hc.pdraw = nullptr;
@@ -615,6 +627,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     fft_grid = side * ((D + 1) / 2);  // one CTA per line pair
   }
   const int spec_grid = std::max(1, w.fft_L / 128);
+  lc.tb_grid = dim3((side + TB_T - 1) / TB_T, (side + TB_T - 1) / TB_T);
+  if (hc.tile_blur_hmax > 0)
+    CK(cudaFuncSetAttribute(blur_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tile_blur_smem_bytes(hc.tile_blur_hmax)));
   lc.sched = Sched{w.radii, w.betas, w.hs, w.level_counts, w.trace};
 
   auto vad_launch = [&](double* out) -> int {
@@ -647,11 +663,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(add_while(&outer_node, g, nullptr, 0, outer_h, &obody));
     CK(cudaGraphConditionalHandleCreate(&inner_h, obody, 0, 0));
     CK(cudaGraphConditionalHandleCreate(&tile_h, obody, 0, 0));
-    cudaGraphConditionalHandle blur_h;
+    cudaGraphConditionalHandle blur_h, tblur_h;
     CK(cudaGraphConditionalHandleCreate(&blur_h, obody, 0, 0));
+    CK(cudaGraphConditionalHandleCreate(&tblur_h, obody, 0, 0));
     cudaGraphNode_t nd[8];
     CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
-                  (unsigned long long)blur_h));
+                  (unsigned long long)blur_h, (unsigned long long)tblur_h));
     cudaGraphNode_t nd_draws;
     CK(add_kernel(&nd_draws, obody, &nd[0], 1, pass_draws_kernel, dim3(PDRAW_MAX * 16 / 256), dim3(256), w.ctrl,
                   w.pdraw, w.prec));
@@ -706,14 +723,43 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         CK(add_kernel(&fn[4], bbody[0], &fn[3], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
                       (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
       }
+      // ELSE: IF (h <= tile_blur_hmax) { one tile kernel } ELSE { direct fold + fallbacks }
+      cudaGraphNode_t tb_if;
+      cudaGraph_t tbody[2];
+      {
+        cudaGraphNodeParams p{};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = tblur_h;
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 2;
+        CK(cudaGraphAddNode(&tb_if, bbody[1], nullptr, 0, &p));
+        tbody[0] = p.conditional.phGraph_out[0];
+        tbody[1] = p.conditional.phGraph_out[1];
+      }
+      {
+        const float* fin = w.feat;
+        float* tout = w.target;
+        PadGeom pg = lc.pg;
+        BlurLevelRef lv = lc.lvl;
+        const float* den = w.den32;
+        void* ta[] = {&fin, &tout, &pg, &lv, &den};
+        cudaKernelNodeParams kp{};
+        kp.func = (void*)blur_tile_kernel;
+        kp.gridDim = lc.tb_grid;
+        kp.blockDim = dim3(TB_THREADS);
+        kp.sharedMemBytes = (unsigned)tile_blur_smem_bytes(hc.tile_blur_hmax);
+        kp.kernelParams = ta;
+        cudaGraphNode_t tn;
+        CK(cudaGraphAddKernelNode(&tn, tbody[0], nullptr, 0, &kp));
+      }
       cudaGraphNode_t bn[4];
-      CK(add_kernel(&bn[0], bbody[1], nullptr, 0, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
+      CK(add_kernel(&bn[0], tbody[1], nullptr, 0, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
-      CK(add_kernel(&bn[1], bbody[1], &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
+      CK(add_kernel(&bn[1], tbody[1], &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
-      CK(add_kernel(&bn[2], bbody[1], &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
+      CK(add_kernel(&bn[2], tbody[1], &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
-      CK(add_kernel(&bn[3], bbody[1], &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
+      CK(add_kernel(&bn[3], tbody[1], &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
     }
     nd[4] = blur_if;
@@ -820,7 +866,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       const int beta = sch.betas[lv];
       const long long bsq = (long long)beta * beta;
       timed(K_CTRL, [&] {
-        level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull);
+        level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull, 0ull);
         if (!parity) pass_draws_kernel<<<PDRAW_MAX * 16 / 256, 256, 0, st>>>(w.ctrl, w.pdraw, w.prec);
       });
       const bool use_fft = level_uses_fft(sch.hs[lv], side, hc.fft_min_h, hc.fft_L);
@@ -859,6 +905,11 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           }
           blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
                                                                      w.fb_cap);
+        });
+      } else if (level_uses_tile_blur(sch.hs[lv], side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax)) {
+        timed(K_BLUR0, [&] {
+          blur_tile_kernel<<<lc.tb_grid, TB_THREADS, tile_blur_smem_bytes(hc.tile_blur_hmax), st>>>(
+              w.feat, w.target, lc.pg, lc.lvl, w.den32);
         });
       } else {
         timed(K_BLUR0, [&] {
@@ -1142,8 +1193,9 @@ size_t plas_blur_tiers_workspace_bytes(int H, int W, int C, int half_width) {
 
 int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, const double* weights, int half_width,
                            int tier, int64_t* fallbacks, void* ws, size_t ws_bytes, void* stream) {
-  if (H < 1 || W < 1 || C < 1 || half_width < 1 || !weights || tier < 0 || tier > 1)
+  if (H < 1 || W < 1 || C < 1 || half_width < 1 || !weights || tier < 0 || tier > 2)
     return fail(PLAS_ERR_INVALID, "bad blur tier arguments");
+  if (tier == 2 && half_width > TB_HMAX) return fail(PLAS_ERR_INVALID, "tile tier needs half_width <= 16");
   TierWs t;
   if (!ws || ws_bytes < carve_tiers(nullptr, H, W, C, half_width, &t))
     return fail(PLAS_ERR_WORKSPACE, "tier workspace");
@@ -1166,7 +1218,13 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
   const int fbg = num_sms() * 2;
   int64_t counts[2] = {0, 0};
   int hc[2];
-  if (tier == 0) {
+  if (tier == 2) {
+    const size_t smem = tile_blur_smem_bytes(half_width);
+    CK(cudaFuncSetAttribute(blur_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    hc[0] = hc[1] = 0;
+    blur_tile_kernel<<<dim3((W + TB_T - 1) / TB_T, (H + TB_T - 1) / TB_T), TB_THREADS, smem, st>>>(t.feat, t.target, pg,
+                                                                                                  lv, t.den32);
+  } else if (tier == 0) {
     const int g0 = grid_for((long long)W * S * ((H + BLUR_R - 1) / BLUR_R), 256, 8);
     blur_pad_kernel<0, 0><<<g0, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap, t.fb1);
     CK(cudaMemcpyAsync(&hc[0], t.fb0, sizeof(int), cudaMemcpyDeviceToHost, st));

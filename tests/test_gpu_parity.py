@@ -361,7 +361,7 @@ def test_device_mode_paired_protocol(config_name, fixture):
 
 
 # ------------------------------------------------------------------ sort-path blur tiers
-@pytest.mark.parametrize("tier", [0, 1])
+@pytest.mark.parametrize("tier", [0, 1, 2])
 def test_blur_tiers_bit_exact_vs_oracle(tier):
     """The sort's level blur (direct fast fold / FFT convolution, each certified against
     the SciPy fold with exact fallback) is bit-identical to blur_target at every radius."""
@@ -372,6 +372,8 @@ def test_blur_tiers_bit_exact_vs_oracle(tier):
     for shape, radii in cases:
         g = rng.normal(0, 1, shape).astype(np.float32)
         for r in radii:
+            if tier == 2 and math.ceil(r) > 16:
+                continue
             got, fb = gblur.blur_target_tiers(g, r, tier)
             np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"tier {tier} {shape} r={r} fb={fb}")
             assert fb[0] + fb[1] < 0.05 * g.size, fb
