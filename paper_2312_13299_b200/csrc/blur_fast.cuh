@@ -71,34 +71,41 @@ __global__ void __launch_bounds__(256, 3) blur_pad_kernel(const float* __restric
   const int nchunks = (n + R - 1) / R;
   const double w0 = __ldg(w);
   const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
-  const long long nstrips = (WS + 31) / 32;
-  const long long ncg = (nchunks + 7) / 8;
-  const long long total = AXIS == 0 ? nstrips * ncg * 256 : (long long)S * nchunks * H;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
+  // 32-bit index math with multiply-shift division (every count < 2^31)
+  const unsigned nstrips = (unsigned)((WS + 31) / 32);
+  const unsigned ncg = (unsigned)((nchunks + 7) / 8);
+  const unsigned total = AXIS == 0 ? nstrips * ncg * 256u : (unsigned)S * (unsigned)nchunks * (unsigned)H;
+  unsigned ns_m, s_m, nc_m;
+  int ns_l, s_l, nc_l;
+  make_fastdiv(nstrips, &ns_m, &ns_l);
+  make_fastdiv((unsigned)S, &s_m, &s_l);
+  make_fastdiv((unsigned)nchunks, &nc_m, &nc_l);
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     long long in_base, out_base, cellbase = 0;
     int chunk, c;
     if (AXIS == 0) {
       // a CTA takes one 32-float column strip and 8 consecutive chunks, so its
       // warps share input rows in L1
-      const long long item = t >> 8;
+      const unsigned item = t >> 8;
       const int lt = (int)(t & 255);
-      const long long strip = item % nstrips;
-      chunk = (int)((item / nstrips) * 8 + (lt >> 5));
-      const long long f = strip * 32 + (lt & 31);
-      if (f >= WS || chunk >= nchunks) continue;
-      c = (int)(f % S);
+      const unsigned q = fastdiv(item, ns_m, ns_l);
+      const unsigned strip = item - q * nstrips;
+      chunk = (int)(q * 8 + (lt >> 5));
+      const unsigned f = strip * 32 + (lt & 31);
+      if ((long long)f >= WS || chunk >= nchunks) continue;
+      const unsigned cell = fastdiv(f, s_m, s_l);
+      c = (int)(f - cell * (unsigned)S);
       in_base = f;
-      out_base = (f / S) * S + c;  // same column of the tmp interior (row offset added per i)
-      cellbase = f / S;
+      out_base = f;  // same column of the tmp interior (row offset added per i)
+      cellbase = cell;
     } else {
-      c = (int)(t % S);
-      const long long rest = t / S;
-      chunk = (int)(rest % nchunks);
-      const long long y = rest / nchunks;
-      in_base = y * WSP + c;
-      out_base = y * WS + c;
-      cellbase = y * W;
+      const unsigned rest = fastdiv(t, s_m, s_l);
+      c = (int)(t - rest * (unsigned)S);
+      const unsigned y = fastdiv(rest, nc_m, nc_l);
+      chunk = (int)(rest - y * (unsigned)nchunks);
+      in_base = (long long)y * WSP + c;
+      out_base = (long long)y * WS + c;
+      cellbase = (long long)y * W;
     }
     if (c >= C) continue;
     const int i0 = chunk * R;
