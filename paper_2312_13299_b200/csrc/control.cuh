@@ -127,6 +127,31 @@ __device__ __forceinline__ double cell_dist2_any(const float* a, const float* b,
   }
 }
 
+// cell_dist2 for 16-float rows with all eight loads issued first (same order,
+// same value): the level-start statistic streams every row once
+__device__ __forceinline__ double cell_dist2_s16(const float* __restrict__ a, const float* __restrict__ b, int D) {
+  float4 x[4], y[4];
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    x[c] = __ldg(reinterpret_cast<const float4*>(a) + c);
+    y[c] = __ldg(reinterpret_cast<const float4*>(b) + c);
+  }
+  double p[4];
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const float xs[4] = {x[c].x, x[c].y, x[c].z, x[c].w}, ys[4] = {y[c].x, y[c].y, y[c].z, y[c].w};
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; e++)
+      if (4 * c + e < D) {
+        const double df = (double)xs[e] - (double)ys[e];
+        acc = fma(df, df, acc);
+      }
+    p[c] = acc;
+  }
+  return (p[0] + p[1]) + (p[2] + p[3]);
+}
+
 // fixed-order fp64 reduction of `nparts` partials by one CTA (thread 0 result)
 __device__ __forceinline__ double reduce_partials(const double* partials, int nparts, double* sh) {
   double s = 0.0;
@@ -362,7 +387,8 @@ __global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
   double sum = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const double d = sqrt(cell_dist2(feat + i * S, target + i * S, D, S));
+    const double d = sqrt(S == 16 ? cell_dist2_s16(feat + i * 16, target + i * 16, D)
+                                   : cell_dist2(feat + i * S, target + i * S, D, S));
     dcache[i] = d;
     sum += d;
   }
