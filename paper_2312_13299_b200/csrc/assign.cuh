@@ -44,6 +44,28 @@ __device__ __forceinline__ float f4get(const float4& v, int e) {
   return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
 __device__ __forceinline__ float4 f4zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// packed f32x2 arithmetic (sm_100: FADD2 / FFMA2, two fp32 lanes per instruction)
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long sqacc2(unsigned long long d, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(d), "l"(c));
+  return r;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
   float r;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -184,11 +206,11 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
   const int s = lane & 3;
   const int gbase = lane & ~3;
   const int nch = S >> 2;
-  float part[4][4];
+  // fast-tier partial squared distances, packed (j, j+1) per f32x2 register;
+  // pad channels (>= D) are zero in both rows and contribute nothing
+  unsigned long long acc2[4][2];
 #pragma unroll
-  for (int i = 0; i < 4; i++)
-#pragma unroll
-    for (int j = 0; j < 4; j++) part[i][j] = 0.f;
+  for (int i = 0; i < 4; i++) acc2[i][0] = acc2[i][1] = 0ull;
   const int rounds = WIDE ? (nch + 3) >> 2 : 1;
   for (int r = 0; r < rounds; r++) {
     const int c = 4 * r + s;
@@ -202,16 +224,24 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
     }
 #pragma unroll
     for (int e = 0; e < 4; e++) {
-      if (4 * c + e < D) {
+      const unsigned long long t01 = pk2(f4get(Tc[0], e), f4get(Tc[1], e));
+      const unsigned long long t23 = pk2(f4get(Tc[2], e), f4get(Tc[3], e));
 #pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const float df = f4get(Fc[i], e) - f4get(Tc[j], e);
-            part[i][j] = fmaf(df, df, part[i][j]);
-          }
+      for (int i = 0; i < 4; i++) {
+        const unsigned long long ff = pk2(f4get(Fc[i], e), f4get(Fc[i], e));
+        acc2[i][0] = sqacc2(sub2(ff, t01), acc2[i][0]);
+        acc2[i][1] = sqacc2(sub2(ff, t23), acc2[i][1]);
       }
     }
+  }
+  float part[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const float2 a = upk2(acc2[i][0]), b = upk2(acc2[i][1]);
+    part[i][0] = a.x;
+    part[i][1] = a.y;
+    part[i][2] = b.x;
+    part[i][3] = b.y;
   }
   // reduce-scatter over the 4 lanes: lane s ends with row i = s
   const bool hi2 = (s & 2) != 0, hi1 = (s & 1) != 0;
@@ -301,7 +331,6 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
 // PARITY: the filtered master permutation; DEVICE: the keyed bijection.
 template <bool PARITY>
 __device__ __forceinline__ unsigned group_local(const int* __restrict__ sel, long long sel_stride, int cls,
-                                                const unsigned (&keys)[6], int lb, int rb, unsigned m,
                                                 unsigned q, int s) {
   // PARITY: host-exact master permutation filtered per class (class_select_kernel);
   // DEVICE: the keyed bijections tabulated by gen_class_tables (the caller passes
@@ -372,19 +401,12 @@ __device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int 
 
 // per-pass class tables in shared memory
 struct PassShared {
-  unsigned keys[9][6];
-  int bits[9][2];
   int seg[6];
   int wcnt[32];
   int base;
 };
 
 __device__ __forceinline__ void load_pass_shared(PassShared& ps, const Ctrl* __restrict__ ctrl) {
-  for (int t = threadIdx.x; t < 54; t += blockDim.x) ps.keys[t / 6][t % 6] = ctrl->fe_keys[t / 6][t % 6];
-  if (threadIdx.x < 9) {
-    ps.bits[threadIdx.x][0] = ctrl->fe_lbits[threadIdx.x];
-    ps.bits[threadIdx.x][1] = ctrl->fe_rbits[threadIdx.x];
-  }
   if (threadIdx.x < 3) {
     ps.seg[threadIdx.x] = ctrl->seg_h[threadIdx.x];
     ps.seg[3 + threadIdx.x] = ctrl->seg_w[threadIdx.x];
@@ -439,8 +461,7 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
         k = rem >= 4 ? 4 : rem;
         if (s < k) {
           const int cls = ty * 3 + tx;
-          const unsigned l = group_local<PARITY>(selp, sel_stride, cls, ps.keys[cls], ps.bits[cls][0],
-                                                 ps.bits[cls][1], m, q, s);
+          const unsigned l = group_local<PARITY>(selp, sel_stride, cls, q, s);
           int ly, lx;
           split_local(l, ww, __frcp_rn((float)ww), &ly, &lx);
           const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
@@ -608,8 +629,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
         const int rem = m - 4 * q;
         if (rem >= 2) k = rem >= 4 ? 4 : rem;
         if (s < k)
-          l = (int)group_local<PARITY>(selp, sel_stride, g.cls, ps.keys[g.cls], ps.bits[g.cls][0],
-                                       ps.bits[g.cls][1], (unsigned)m, (unsigned)q, s);
+          l = (int)group_local<PARITY>(selp, sel_stride, g.cls, (unsigned)q, s);
       }
       int rowj[4];
 #pragma unroll
