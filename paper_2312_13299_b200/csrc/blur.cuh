@@ -179,4 +179,48 @@ __global__ void border_weight_kernel(const double* __restrict__ row_weight, floa
   }
 }
 
+// The sort only needs den32 = fp32(den).  den(y, x) is A(y) folded along x
+// over the in-range taps, which in exact arithmetic is A(y) * B(x) with
+// B(x) = sum of the in-range weights.  Both SciPy's fp64 fold and this
+// product lie within (2h + 4) 2^-53 A(y) of the exact product (weights sum to
+// 1, non-negative terms), so when fp32(p - bound) == fp32(p + bound) the fp32
+// value equals fp32 of the reference fold; otherwise the cell is folded
+// exactly.  O(H W) instead of O(H W h) -- the border plane is data-independent
+// but per level.
+// row_weight[y] = A(y) (border_rows_kernel); col_weight[x] = B(x).
+__global__ void border_cols_kernel(double* __restrict__ col_weight, int W, BlurLevelRef lvl) {
+  int h;
+  const double* w;
+  lvl.get(&h, &w);
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+    double b = __ldg(w);
+    for (int j = h; j >= 1; j--) b += ((x - j >= 0) ? __ldg(w + j) : 0.0) + ((x + j < W) ? __ldg(w + j) : 0.0);
+    col_weight[x] = b;
+  }
+}
+
+__global__ void border_weight32_kernel(const double* __restrict__ row_weight, const double* __restrict__ col_weight,
+                                       float* __restrict__ den32, int H, int W, BlurLevelRef lvl) {
+  int h;
+  const double* w;
+  lvl.get(&h, &w);
+  const double scale = (2.0 * h + 8.0) * 1.1102230246251565e-16 * 2.0;  // x2 safety
+  // one row per CTA iteration: no per-element division
+  for (int y = blockIdx.x; y < H; y += gridDim.x)
+  for (int x = threadIdx.x; x < W; x += blockDim.x) {
+    const long long t = (long long)y * W + x;
+    const double a = row_weight[y];
+    const double p = a * col_weight[x];
+    const double bnd = scale * a;
+    float r = __double2float_rn(p);
+    if (__double2float_rn(p - bnd) != __double2float_rn(p + bnd)) {  // exact fold (blur.py:13-15)
+      double acc = __dmul_rn(a, __ldg(w));
+      for (int j = h; j >= 1; j--)
+        acc = __dadd_rn(acc, __dmul_rn(__dadd_rn((x - j >= 0) ? a : 0.0, (x + j < W) ? a : 0.0), __ldg(w + j)));
+      r = __double2float_rn(acc);
+    }
+    den32[t] = r;
+  }
+}
+
 }  // namespace plas
