@@ -365,13 +365,14 @@ constexpr int WARP_LIST = 512;  // shared staging entries per warp
 // Append this lane's moved cell (if mv) to its warp's staging segment; the
 // warp-uniform fill level lives in *wcnt (a register in every lane).  A full
 // segment is flushed by the warp with one global reservation.
+template <int CAP = WARP_LIST>
 __device__ __forceinline__ void stage_move(bool mv, int cell, int* wlist, int* wcnt, const MoveOut& mo) {
   const unsigned bal = __ballot_sync(PLAS_FULL_MASK, mv);
   if (!bal) return;
   const int lane = threadIdx.x & 31;
   if (mv) wlist[*wcnt + __popc(bal & ((1u << lane) - 1u))] = cell;
   *wcnt += __popc(bal);
-  if (*wcnt > WARP_LIST - 32) {
+  if (*wcnt > CAP - 32) {
     __syncwarp();
     int base = 0;
     if (lane == 0) base = atomicAdd(mo.count, *wcnt);
@@ -383,6 +384,7 @@ __device__ __forceinline__ void stage_move(bool mv, int cell, int* wlist, int* w
 }
 
 // CTA-wide: append every warp's remaining entries with one reservation
+template <int CAP = WARP_LIST>
 __device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int wcnt, int* s_wcnt,
                                             int* s_base) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -396,7 +398,7 @@ __device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int 
   __syncthreads();
   int off = *s_base;
   for (int w = 0; w < wid; w++) off += s_wcnt[w];
-  for (int i = lane; i < wcnt; i += 32) mo.list[off + i] = s_list[wid * WARP_LIST + i];
+  for (int i = lane; i < wcnt; i += 32) mo.list[off + i] = s_list[wid * CAP + i];
 }
 
 // per-pass class tables in shared memory
@@ -522,6 +524,7 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
 // moved rows are written back, from the staged copy, so in-place swaps need
 // no ordering.  Same decisions as pass_kernel.
 constexpr int TILE_THREADS = 256;
+constexpr int TILE_WARP_LIST = 128;  // moved-cell staging per warp in the tile kernel
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -547,10 +550,10 @@ struct TileGeom {
   int y0, x0, hh, ww, cls;
 };
 
-__device__ __forceinline__ TileGeom tile_geom(int b, int nbx, int nby, int fy, int fx, int beta,
-                                              const int* seg) {
+__device__ __forceinline__ TileGeom tile_geom(int b, int nbx, unsigned nbx_m, int nbx_l, int nby, int fy, int fx,
+                                              int beta, const int* seg) {
   TileGeom g;
-  const int by = b / nbx, bx = b - by * nbx;
+  const int by = (int)fastdiv((unsigned)b, nbx_m, nbx_l), bx = b - by * nbx;
   const int ty = by == 0 ? 0 : (by == nby - 1 ? 2 : 1);
   const int tx = bx == 0 ? 0 : (bx == nbx - 1 ? 2 : 1);
   g.hh = seg[ty];
@@ -568,17 +571,19 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
     int* __restrict__ counters) {
   extern __shared__ float4 smem4[];
   __shared__ PassShared ps;
-  __shared__ int s_list[8 * WARP_LIST];
+  __shared__ int s_list[8 * TILE_WARP_LIST];  // small lists: 3 CTAs per SM fit in shared memory
   load_pass_shared(ps, ctrl);
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
   if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
-  int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
+  int* wlist = s_list + (threadIdx.x >> 5) * TILE_WARP_LIST;
   int wcnt = 0;
   const int side = ctrl->side;
   const int beta = ctrl->beta;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
+  const unsigned nbx_m = ctrl->nbx_m;
+  const int nbx_l = ctrl->nbx_l;
   const int b_lo = ctrl->b_lo, nblocks = ctrl->b_hi;  // this rank's blocks
   const int nch = S >> 2;
   const long long mmax = (long long)beta * beta;
@@ -589,19 +594,22 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
   // issue the copies of block b into stage st
   auto prefetch = [&](int b, int st) {
     if (b < nblocks) {
-      const TileGeom g = tile_geom(b, nbx, nby, fy, fx, beta, ps.seg);
+      const TileGeom g = tile_geom(b, nbx, nbx_m, nbx_l, nby, fy, fx, beta, ps.seg);
       float* sF = stage_base + st * stage_floats;
       float* sT = sF + mmax * S;
       int* sI = reinterpret_cast<int*>(sT + mmax * S);
       const int row4 = g.ww * nch;
+      const float rr4 = __frcp_rn((float)row4), rw = __frcp_rn((float)g.ww);
       for (int e = threadIdx.x; e < g.hh * row4; e += blockDim.x) {
-        const int r = e / row4, c = e - r * row4;
+        int r, c;
+        split_local((unsigned)e, row4, rr4, &r, &c);
         const long long go = ((long long)(g.y0 + r) * side + g.x0) * S + 4 * c;
         cp_async16(sF + 4 * e, feat + go);
         cp_async16(sT + 4 * e, target + go);
       }
       for (int e = threadIdx.x; e < g.hh * g.ww; e += blockDim.x) {
-        const int r = e / g.ww, c = e - r * g.ww;
+        int r, c;
+        split_local((unsigned)e, g.ww, rw, &r, &c);
         cp_async4(sI + e, idx + (long long)(g.y0 + r) * side + g.x0 + c);
       }
     }
@@ -615,7 +623,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
     prefetch(b + gridDim.x, st ^ 1);
     cp_async_wait<1>();  // block b's stage has landed
     __syncthreads();
-    const TileGeom g = tile_geom(b, nbx, nby, fy, fx, beta, ps.seg);
+    const TileGeom g = tile_geom(b, nbx, nbx_m, nbx_l, nby, fy, fx, beta, ps.seg);
     const float* sF = stage_base + st * stage_floats;
     const float* sT = sF + mmax * S;
     const int* sI = reinterpret_cast<const int*>(sT + mmax * S);
@@ -666,12 +674,12 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
       const bool my_mv = pick4(mv, s);
       const long long dcell = pick4(gcell, pick4(dst, s));
       if (my_mv) idx[dcell] = sI[pick4(rowj, s)];
-      stage_move(my_mv, (int)dcell, wlist, &wcnt, mo);
+      stage_move<TILE_WARP_LIST>(my_mv, (int)dcell, wlist, &wcnt, mo);
     }
     __syncthreads();  // stage st is refilled by the prefetch two iterations on
   }
   cp_async_wait<0>();
-  flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  flush_moves<TILE_WARP_LIST>(mo, s_list, wcnt, ps.wcnt, &ps.base);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
 }
