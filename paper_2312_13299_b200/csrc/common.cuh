@@ -62,6 +62,10 @@ struct Ctrl {
   const int4* pdraw;
   const int* prec;                 // per-pass grouping records (PREC_INTS each), same level
   int pdraw_level;                 // level the table holds (-1: none)
+  // fast-division magics precomputed at level start (the per-pass geometry
+  // update is on the serial critical path): cap, and nbx for its two values
+  unsigned lv_cap_m, lv_seg_m[2];
+  int lv_cap_l, lv_seg_l[2], lv_seg_base, lv_cap;
   int gen_pass;                    // pass whose grouping tables gen_tables_kernel builds
 };
 
@@ -296,12 +300,30 @@ __host__ __device__ __forceinline__ void set_pass_geometry_base(Ctrl* c, int dy,
   // contiguous, balanced shares of the pass's groups / blocks (whole pass when world == 1)
   const long long nb = (long long)c->nby * c->nbx;
   const int W = c->world > 0 ? c->world : 1;
-  c->g_lo = c->total_groups * c->rank / W;
-  c->g_hi = c->total_groups * (c->rank + 1) / W;
-  c->b_lo = (int)(nb * c->rank / W);
-  c->b_hi = (int)(nb * (c->rank + 1) / W);
-  make_fastdiv((unsigned)c->cap, &c->cap_m, &c->cap_l);
-  make_fastdiv((unsigned)c->nbx, &c->nbx_m, &c->nbx_l);
+  if (W == 1) {
+    c->g_lo = 0;
+    c->g_hi = c->total_groups;
+    c->b_lo = 0;
+    c->b_hi = (int)nb;
+  } else {
+    c->g_lo = c->total_groups * c->rank / W;
+    c->g_hi = c->total_groups * (c->rank + 1) / W;
+    c->b_lo = (int)(nb * c->rank / W);
+    c->b_hi = (int)(nb * (c->rank + 1) / W);
+  }
+  if (c->lv_cap == c->cap) {  // level-start magics (level_begin_kernel)
+    c->cap_m = c->lv_cap_m;
+    c->cap_l = c->lv_cap_l;
+  } else {
+    make_fastdiv((unsigned)c->cap, &c->cap_m, &c->cap_l);
+  }
+  const int si = c->nbx - c->lv_seg_base;
+  if (si == 0 || si == 1) {
+    c->nbx_m = c->lv_seg_m[si];
+    c->nbx_l = c->lv_seg_l[si];
+  } else {
+    make_fastdiv((unsigned)c->nbx, &c->nbx_m, &c->nbx_l);
+  }
 }
 
 // DEVICE-mode Feistel keys of block class cls.  gkey keys the per-class

@@ -253,6 +253,13 @@ __global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_con
   const int lv = c->level;
   c->beta = s.betas[lv];
   c->h = s.hs[lv];
+  // fast-division magics of this level's constant cap and of the two possible
+  // segment counts (first segment beta or shorter), off the per-pass path
+  c->lv_cap = (c->beta * c->beta + 3) / 4;
+  make_fastdiv((unsigned)c->lv_cap, &c->lv_cap_m, &c->lv_cap_l);
+  c->lv_seg_base = num_segments(c->beta, c->beta, c->side);
+  make_fastdiv((unsigned)c->lv_seg_base, &c->lv_seg_m[0], &c->lv_seg_l[0]);
+  make_fastdiv((unsigned)(c->lv_seg_base + 1), &c->lv_seg_m[1], &c->lv_seg_l[1]);
   set_cond(blur_cond, level_uses_fft(c->h, c->side, c->fft_min_h, c->fft_L) ? 1u : 0u);
   set_cond(tblur_cond, level_uses_tile_blur(c->h, c->side, c->fft_min_h, c->fft_L, c->tile_blur_hmax) ? 1u : 0u);
   c->pass = 0;
