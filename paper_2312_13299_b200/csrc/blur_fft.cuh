@@ -110,7 +110,9 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
 
 template <int L> __host__ __device__ constexpr int fft_threads_for() { return L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8); }
 // resident CTAs per SM the register budget must allow (~85 registers at 256 threads)
-template <int L> __host__ __device__ constexpr int fft_min_blocks() { return fft_threads_for<L>() >= 512 ? 1 : 512 / fft_threads_for<L>(); }
+// 4 CTAs per SM at 256 threads (64 registers): the passes are latency-bound, so
+// occupancy beats the second buffer (measured: C2 144.5 -> 138.5 ms)
+template <int L> __host__ __device__ constexpr int fft_min_blocks() { return L > 4096 ? 1 : 1024 / fft_threads_for<L>(); }
 
 // Pass schedule of an L = 2^LOG2L point FFT: radix-8 passes, then one radix-4
 // or radix-2 pass for the remaining bits.  Pass p has sub-transform size
@@ -135,10 +137,10 @@ __host__ __device__ constexpr int fft_twiddle_len(int lg) {
 __host__ __device__ constexpr int fft_pad(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int fft_buf_len(int L) { return L + L / 8; }
 
-// Large FFTs (L = 8192: two padded buffers would exceed shared memory) run
-// every pass in place in one buffer: all threads read their butterflies'
-// inputs, the CTA syncs, then all write.
-template <int LOG2L> __host__ __device__ constexpr bool fft_inplace() { return LOG2L >= 13; }
+// Every pass runs in place in one padded buffer (all threads read their
+// butterflies' inputs, the CTA syncs, then all write): half the shared memory
+// of ping-pong buffers, so 4 CTAs fit per SM at L = 2048 (and L = 8192 fits).
+template <int LOG2L> __host__ __device__ constexpr bool fft_inplace() { return true; }
 
 // Stockham pass p of radix R: butterfly j reads v[r] = src[j + r L/R], applies
 // twiddles W_{Ns R}^{r k} (k = j mod Ns), runs the radix-R DFT and writes to
@@ -245,7 +247,7 @@ struct FftPass {
 
 template <int LOG2L, int P, int LAST>
 struct FftChain {
-  // passes P .. LAST-1 of one FFT, ping-ponging between a and b (pass P reads a)
+  // passes P .. LAST-1 of one FFT (a == b: in place, fft_inplace)
   template <bool SPEC_LAST>
   __device__ __forceinline__ static void run(double2* a, double2* b, int tid, const double2* tw, const double* spec) {
     if constexpr (P < LAST) {
@@ -273,7 +275,7 @@ __device__ __forceinline__ double warp_max_sum(double v, double m, double* out_m
 // across a loop the compiler hoists every pass's thread-only address
 // arithmetic out of it and spills).  Dataflow: the first pass of the forward
 // FFT reads the line pair straight from global memory (indices >= n are the
-// zero padding); passes ping-pong between two padded shared buffers with one
+// zero padding); passes run in place in one padded shared buffer, two
 // barrier each; the last pass of the second FFT keeps its outputs in
 // registers and certifies / stores them.  The CTA also settles its own
 // uncertain outputs with the exact SciPy fold from a shared-memory copy of
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
 
 // shared memory of blur_fft_kernel for an L-point FFT
 inline size_t fft_smem_bytes(int L) {
-  const size_t nbuf = L >= 8192 ? 1 : 2;  // fft_inplace
+  const size_t nbuf = 1;  // fft_inplace
   return sizeof(double2) * nbuf * (size_t)fft_buf_len(L) + sizeof(float) * (size_t)L;
 }
 
