@@ -275,8 +275,8 @@ __device__ __forceinline__ double warp_max_sum(double v, double m, double* out_m
 // across a loop the compiler hoists every pass's thread-only address
 // arithmetic out of it and spills).  Dataflow: the first pass of the forward
 // FFT reads the line pair straight from global memory (indices >= n are the
-// zero padding); passes run in place in one padded shared buffer, two
-// barrier each; the last pass of the second FFT keeps its outputs in
+// zero padding); passes run in place in one padded shared buffer (two
+// barriers each); the last pass of the second FFT keeps its outputs in
 // registers and certifies / stores them.  The CTA also settles its own
 // uncertain outputs with the exact SciPy fold from a shared-memory copy of
 // the two input lines (FB_LOCAL of them; any excess goes to the global list).
