@@ -51,7 +51,7 @@ struct PadGeom {
 //         out = tmp interior (row stride (W + 2 pad) * S).
 // AXIS 1: in = tmp interior, out = target (row stride W*S), EPI 1 divides by den32.
 template <int AXIS, int EPI>
-__global__ void __launch_bounds__(256, 3) blur_pad_kernel(const float* __restrict__ in, float* __restrict__ out,
+__global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                        PadGeom pg, BlurLevelRef lvl,
                                                        const float* __restrict__ den32,
                                                        int* __restrict__ fb, int fb_cap,

@@ -4,6 +4,12 @@
 #include <stdint.h>
 
 #define PLAS_FULL_MASK 0xffffffffu
+#ifndef STATS_MINB
+#define STATS_MINB 4
+#endif
+#ifndef BPAD_MINB
+#define BPAD_MINB 3
+#endif
 
 namespace plas {
 

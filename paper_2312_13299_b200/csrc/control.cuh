@@ -384,7 +384,7 @@ __device__ __forceinline__ bool last_cta_reduce(double v, double* partials, int*
 
 // Level start (plas.py:256-258): fp64 distance of every cell to the fresh
 // target into the cache, sum -> previous, trace, open the pass loop.
-__global__ void __launch_bounds__(RED_THREADS) level_stats_kernel(
+__global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, long long n, int D, int S, double* partials, int* done,
     unsigned long long inner, unsigned long long tile_cond, int* tab, long long tab_stride) {
@@ -476,7 +476,7 @@ __device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, lo
 // Sharded (world > 1): the last CTA only publishes this rank's partial
 // (change, moved count) to xpart; shard_control_kernel runs the controller
 // once every rank's partial has been exchanged.
-__global__ void __launch_bounds__(RED_THREADS) pass_stats_kernel(
+__global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
     double* partials, int* done, long long n, unsigned long long inner, unsigned long long tile_cond,
