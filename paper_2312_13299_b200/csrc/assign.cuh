@@ -91,6 +91,25 @@ __device__ __forceinline__ int perm_dest(int k, int p, int i) {
   if (k == 2) return p == 0 ? i : 1 - i;
   return i;
 }
+// all four destinations of arrangement p of k slots, 2 bits per slot
+__device__ __forceinline__ unsigned perm_dest_code(int k, int p) {
+  unsigned long long w;
+  int sh;
+  if (k == 4) {
+    w = p < 8 ? 0xb1e16c9c78d8b4e4ull : (p < 16 ? 0x36c672d22d8d39c9ull : 0x1b4b278763931e4eull);
+    sh = 8 * (p & 7);
+  } else if (k == 3) {
+    w = 0x61209211824ull | 0xc0c0c0c0c0c0ull;  // slot 3 stays
+    sh = 8 * p;
+  } else if (k == 2) {
+    w = 0xe1e4ull;
+    sh = 8 * p;
+  } else {
+    w = 0xe4ull;
+    sh = 0;
+  }
+  return (unsigned)((w >> sh) & 0xffull);
+}
 
 struct CostMat {
   float v[4][4];  // v[i][j] = cost of slot i's element in slot j's target
@@ -145,21 +164,15 @@ __device__ __forceinline__ void lane_best_exact(const CostMat& C, int k, int s, 
   *best_p = bp;
 }
 
-// fast tier: fp32 sums; this lane's best (b1, p1) and second best b2
-__device__ __forceinline__ void lane_best_fast(const CostMat& C, int k, int s, float* b1, int* p1,
-                                               float* b2) {
+// fast tier from the lane's column view: c0 = C[0][s], x[i][q] = C[i][o_q]
+// (o = the other targets in increasing order); same sums as lane_best_fast
+__device__ __forceinline__ void lane_best_fast_cols(float c0, const float (&x)[4][3], int k, int s, float* b1,
+                                                    int* p1, float* b2) {
   const float INF = __int_as_float(0x7f800000);
   float v1 = INF, v2 = INF;
   int q1 = 0x7fffffff;
   if (s < k) {
-    const float c0 = sel4(C.v[0], s);
     if (k == 4) {
-      const int o[3] = {s == 0 ? 1 : 0, s <= 1 ? 2 : 1, s <= 2 ? 3 : 2};
-      float x[4][3];
-#pragma unroll
-      for (int i = 1; i < 4; i++)
-#pragma unroll
-        for (int q = 0; q < 3; q++) x[i][q] = sel4(C.v[i], o[q]);
       const int A[6] = {0, 0, 1, 1, 2, 2}, B[6] = {1, 2, 0, 2, 0, 1}, E[6] = {2, 1, 2, 0, 1, 0};
 #pragma unroll
       for (int l = 0; l < 6; l++) {
@@ -172,10 +185,9 @@ __device__ __forceinline__ void lane_best_fast(const CostMat& C, int k, int s, f
           v2 = c;
         }
       }
-    } else if (k == 3) {
-      const int o0 = s == 0 ? 1 : 0, o1 = s == 2 ? 1 : 2;
-      const float ca = (c0 + sel4(C.v[1], o0)) + sel4(C.v[2], o1);
-      const float cb = (c0 + sel4(C.v[1], o1)) + sel4(C.v[2], o0);
+    } else if (k == 3) {  // the other targets of {0, 1, 2} are o_0 < o_1
+      const float ca = (c0 + x[1][0]) + x[2][1];
+      const float cb = (c0 + x[1][1]) + x[2][0];
       if (cb < ca) {
         v1 = cb;
         q1 = 2 * s + 1;
@@ -186,7 +198,7 @@ __device__ __forceinline__ void lane_best_fast(const CostMat& C, int k, int s, f
         v2 = cb;
       }
     } else if (k == 2) {
-      v1 = c0 + sel4(C.v[1], 1 - s);
+      v1 = c0 + x[1][0];
       q1 = s;
     }
   }
@@ -206,69 +218,76 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
   const int s = lane & 3;
   const int gbase = lane & ~3;
   const int nch = S >> 2;
-  // fast-tier partial squared distances, packed (j, j+1) per f32x2 register;
-  // pad channels (>= D) are zero in both rows and contribute nothing
-  unsigned long long acc2[4][2];
+  // fast-tier partial squared distances: acc[i][j] holds the (even, odd)
+  // channel halves as one f32x2 register, fed straight from the 8-byte halves
+  // of the loaded chunks; pad channels (>= D) are zero in both rows
+  unsigned long long acc[4][4];
 #pragma unroll
-  for (int i = 0; i < 4; i++) acc2[i][0] = acc2[i][1] = 0ull;
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
   const int rounds = WIDE ? (nch + 3) >> 2 : 1;
   for (int r = 0; r < rounds; r++) {
     const int c = 4 * r + s;
     const bool valid = c < nch;
+    // no data selects: slots >= k read row rowj = 0 (their pairs are never
+    // used); a lane past the row reads chunk 0 of the quad's first feature row
+    // as every operand, so all its differences are exactly zero
+    const float* Tv = valid ? Tb : Fb;
     float4 Tc[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      const long long off = (long long)rowj[i] * S + 4 * c;
-      Fc[i] = (valid && i < k) ? ld4v(Fb + off) : f4zero();
-      Tc[i] = (valid && i < k) ? (TNC ? ld4g(Tb + off) : ld4v(Tb + off)) : f4zero();
+      const long long off = valid ? (long long)rowj[i] * S + 4 * c : (long long)rowj[0] * S;
+      Fc[i] = ld4v(Fb + off);
+      Tc[i] = (TNC && valid) ? ld4g(Tv + off) : ld4v(Tv + off);
     }
 #pragma unroll
-    for (int e = 0; e < 4; e++) {
-      const unsigned long long t01 = pk2(f4get(Tc[0], e), f4get(Tc[1], e));
-      const unsigned long long t23 = pk2(f4get(Tc[2], e), f4get(Tc[3], e));
+    for (int i = 0; i < 4; i++)
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const unsigned long long ff = pk2(f4get(Fc[i], e), f4get(Fc[i], e));
-        acc2[i][0] = sqacc2(sub2(ff, t01), acc2[i][0]);
-        acc2[i][1] = sqacc2(sub2(ff, t23), acc2[i][1]);
+      for (int j = 0; j < 4; j++) {
+        acc[i][j] = sqacc2(sub2(pk2(Fc[i].x, Fc[i].y), pk2(Tc[j].x, Tc[j].y)), acc[i][j]);
+        acc[i][j] = sqacc2(sub2(pk2(Fc[i].z, Fc[i].w), pk2(Tc[j].z, Tc[j].w)), acc[i][j]);
       }
-    }
   }
   float part[4][4];
 #pragma unroll
-  for (int i = 0; i < 4; i++) {
-    const float2 a = upk2(acc2[i][0]), b = upk2(acc2[i][1]);
-    part[i][0] = a.x;
-    part[i][1] = a.y;
-    part[i][2] = b.x;
-    part[i][3] = b.y;
-  }
-  // reduce-scatter over the 4 lanes: lane s ends with row i = s
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const float2 h = upk2(acc[i][j]);
+      part[i][j] = h.x + h.y;
+    }
+  // reduce-scatter over the 4 lanes by column: lane s ends with column j = s
+  // of the cost matrix, col[i] = C[i][s]
   const bool hi2 = (s & 2) != 0, hi1 = (s & 1) != 0;
   float half[2][4];
 #pragma unroll
   for (int t = 0; t < 2; t++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const float send = hi2 ? part[t][j] : part[2 + t][j];
-      const float keep = hi2 ? part[2 + t][j] : part[t][j];
-      half[t][j] = keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 2);
+    for (int i = 0; i < 4; i++) {
+      const float send = hi2 ? part[i][t] : part[i][2 + t];
+      const float keep = hi2 ? part[i][2 + t] : part[i][t];
+      half[t][i] = keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 2);
     }
-  float cst[4];
+  float col[4];
 #pragma unroll
-  for (int j = 0; j < 4; j++) {
-    const float send = hi1 ? half[0][j] : half[1][j];
-    const float keep = hi1 ? half[1][j] : half[0][j];
-    cst[j] = sqrt_approx(keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 1));
+  for (int i = 0; i < 4; i++) {
+    const float send = hi1 ? half[0][i] : half[1][i];
+    const float keep = hi1 ? half[1][i] : half[0][i];
+    col[i] = sqrt_approx(keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 1));
   }
-  CostMat C;
+  // lane s takes the arrangements that put slot 0's element in target s: it
+  // needs C[i][o_q] for the other targets o_0 < o_1 < o_2, i.e. column o_q's
+  // entry i, shuffled from lane o_q (a per-lane source, no selects)
+  const int o3[3] = {s == 0 ? 1 : 0, s <= 1 ? 2 : 1, s <= 2 ? 3 : 2};
+  float x[4][3];
 #pragma unroll
-  for (int i = 0; i < 4; i++)
+  for (int i = 1; i < 4; i++)
 #pragma unroll
-    for (int j = 0; j < 4; j++) C.v[i][j] = __shfl_sync(PLAS_FULL_MASK, cst[j], gbase + i);
+    for (int q = 0; q < 3; q++) x[i][q] = __shfl_sync(PLAS_FULL_MASK, col[i], gbase + o3[q]);
   float b1, b2;
   int bp;
-  lane_best_fast(C, k, s, &b1, &bp, &b2);
+  lane_best_fast_cols(col[0], x, k, s, &b1, &bp, &b2);
 #pragma unroll
   for (int o = 1; o <= 2; o <<= 1) {
     const float ob1 = __shfl_xor_sync(PLAS_FULL_MASK, b1, o);
@@ -289,6 +308,7 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
     // ---- exact tier for the whole warp (same decision wherever the fast one was
     // certain): lane s recomputes row s with the reference arithmetic
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    float cst[4];
     const long long fo = (long long)pick4(rowj, s) * S;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -307,6 +327,7 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
       }
       cst[j] = __double2float_rn(__dsqrt_rn(acc[j]));
     }
+    CostMat C;
 #pragma unroll
     for (int i = 0; i < 4; i++)
 #pragma unroll
@@ -446,9 +467,13 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
   const int nch = S >> 2;
   const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
   int exact = 0;
-  for (unsigned base = g_lo + blockIdx.x * 64u; base < total; base += gridDim.x * 64u) {
-    const unsigned g = base + gl;
-    int k = 0, cell = 0;
+  // geometry of group g for lane slot s; the table entry load is issued here
+  // and consumed one iteration later (prefetch)
+  struct Geo {
+    int k, ww, y0, x0, l;
+  };
+  auto geo = [&](unsigned g) {
+    Geo o{0, 1, 0, 0, 0};
     if (g < total) {
       const unsigned b = fastdiv(g, cap_m, cap_l);
       const unsigned q = g - b * cap;
@@ -457,41 +482,53 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
       const int ty = by == 0 ? 0 : (by == (unsigned)nby - 1 ? 2 : 1);
       const int tx = bx == 0 ? 0 : (bx == (unsigned)nbx - 1 ? 2 : 1);
       const int hh = ps.seg[ty], ww = ps.seg[3 + tx];
-      const unsigned m = (unsigned)(hh * ww);
-      const int rem = (int)m - 4 * (int)q;
+      const int rem = hh * ww - 4 * (int)q;
       if (rem >= 2) {  // a single leftover cell never moves
-        k = rem >= 4 ? 4 : rem;
-        if (s < k) {
-          const int cls = ty * 3 + tx;
-          const unsigned l = group_local<PARITY>(selp, sel_stride, cls, q, s);
-          int ly, lx;
-          split_local(l, ww, __frcp_rn((float)ww), &ly, &lx);
-          const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
-          const int x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
-          cell = (y0 + ly) * side + x0 + lx;
-        }
+        o.k = rem >= 4 ? 4 : rem;
+        o.ww = ww;
+        o.y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
+        o.x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
+        if (s < o.k) o.l = (int)group_local<PARITY>(selp, sel_stride, ty * 3 + tx, q, s);
       }
     }
+    return o;
+  };
+  Geo gnext = geo(g_lo + blockIdx.x * 64u + gl);
+  for (unsigned base = g_lo + blockIdx.x * 64u; base < total; base += gridDim.x * 64u) {
+    const Geo gc = gnext;
+    gnext = geo(base + gridDim.x * 64u + gl);
+    const int k = gc.k;
+    int cell = 0;
+    if (s < k) {
+      int ly, lx;
+      split_local((unsigned)gc.l, gc.ww, __frcp_rn((float)gc.ww), &ly, &lx);
+      cell = (gc.y0 + ly) * side + gc.x0 + lx;
+    }
+    // this lane's element index, needed only if its cell moves (loaded with the rows)
+    const int my_idx0 = s < k ? idx[cell] : 0;
     int rowj[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
     float4 Fc[4];
     const int bp = decide4<WIDE, true>(feat, target, rowj, D, S, k, Fc, &exact);
-    int dst[4];
+    const unsigned code = perm_dest_code(k, bp);
+    int dst[4], dcl[4];
     bool mv[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-      dst[i] = i < k ? perm_dest(k, bp, i) : i;
-      mv[i] = bp != 0 && i < k && dst[i] != i;
+      dst[i] = (int)((code >> (2 * i)) & 3u);
+      mv[i] = dst[i] != i;
+      dcl[i] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + dst[i]);  // destination cell of slot i
     }
-    const bool my_mv = pick4(mv, s);
-    const int my_idx = my_mv ? idx[cell] : 0;
+    const int my_dst = (int)((code >> (2 * s)) & 3u);
+    const bool my_mv = my_dst != s;
+    const int my_idx = my_idx0;
     __syncwarp();
     if (!WIDE) {
       if (s < nch) {
 #pragma unroll
         for (int i = 0; i < 4; i++)
-          if (mv[i]) st4(feat + (long long)pick4(rowj, dst[i]) * S + 4 * s, Fc[i]);
+          if (mv[i]) st4(feat + (long long)dcl[i] * S + 4 * s, Fc[i]);
       }
     } else {
       // chunk columns: every read of a column precedes its writes
@@ -507,7 +544,7 @@ __global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, 
         __syncwarp();
       }
     }
-    const int dcell = pick4(rowj, pick4(dst, s));
+    const int dcell = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + my_dst);
     if (my_mv) idx[dcell] = my_idx;
     stage_move(my_mv, dcell, wlist, &wcnt, mo);
   }
@@ -630,26 +667,34 @@ __global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
     const int m = g.hh * g.ww;
     const int ngroups = (m + 3) >> 2;
     const float rw = __frcp_rn((float)g.ww);
-    for (int q0 = 0; q0 < ngroups; q0 += TILE_THREADS / 4) {
-      const int q = q0 + gl;
-      int k = 0, l = 0;
+    // slot count and table entry of group q (the entry of the next group is
+    // loaded one iteration ahead)
+    auto group_at = [&](int q, int* k, int* l) {
+      *k = 0;
+      *l = 0;
       if (q < ngroups) {
         const int rem = m - 4 * q;
-        if (rem >= 2) k = rem >= 4 ? 4 : rem;
-        if (s < k)
-          l = (int)group_local<PARITY>(selp, sel_stride, g.cls, (unsigned)q, s);
+        if (rem >= 2) *k = rem >= 4 ? 4 : rem;
+        if (s < *k) *l = (int)group_local<PARITY>(selp, sel_stride, g.cls, (unsigned)q, s);
       }
+    };
+    int knext, lnext;
+    group_at(gl, &knext, &lnext);
+    for (int q0 = 0; q0 < ngroups; q0 += TILE_THREADS / 4) {
+      const int k = knext, l = lnext;
+      group_at(q0 + TILE_THREADS / 4 + gl, &knext, &lnext);
       int rowj[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, l, (lane & ~3) + j);
       float4 Fc[4];
       const int bp = decide4<WIDE, false>(sF, sT, rowj, D, S, k, Fc, &exact);
+      const unsigned code = perm_dest_code(k, bp);
       int dst[4];
       bool mv[4];
 #pragma unroll
       for (int i = 0; i < 4; i++) {
-        dst[i] = i < k ? perm_dest(k, bp, i) : i;
-        mv[i] = bp != 0 && i < k && dst[i] != i;
+        dst[i] = (int)((code >> (2 * i)) & 3u);
+        mv[i] = dst[i] != i;
       }
       long long gcell[4];
 #pragma unroll

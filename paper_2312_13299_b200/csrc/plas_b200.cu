@@ -307,10 +307,10 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->trace = c.take<double>(std::max(tcap, 1LL));
   long long b0 = side;  // beta0 <= side
   // per-class grouping tables: PARITY (class_select_kernel) and DEVICE (gen_class_tables)
-  w->sel_stride = b0 * b0;
+  w->sel_stride = (b0 * b0 + 3) / 4 * 4;  // every class row 16-byte aligned
   w->mp = c.take<int>(rng_mode == PLAS_RNG_PARITY ? (size_t)(b0 * b0) : 1);
   // two buffers in DEVICE mode (pass parity: pass p reads one while building p + 1's)
-  w->sel = c.take<int>((size_t)((rng_mode == PLAS_RNG_PARITY ? 9 : 18) * b0 * b0));
+  w->sel = c.take<int>((size_t)((rng_mode == PLAS_RNG_PARITY ? 9 : 18) * w->sel_stride));
   w->pdraw = c.take<int4>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX);
   w->prec = c.take<int>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX * PREC_INTS);
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
@@ -381,6 +381,17 @@ int pass_grid_size(int S) {
     cached[which] = std::min(num_sms() * occ, MAX_PARTS);
   }
   return cached[which];
+}
+
+// K3 launch configuration (gather regime)
+struct PassCfg {
+  void* fn;
+  int grid, block;
+  unsigned smem;
+};
+template <bool PARITY>
+PassCfg pass_cfg(int S) {
+  return {pass_kernel_ptr<PARITY>(S), pass_grid_size(S), 256, 0u};
 }
 
 template <bool PARITY>
@@ -804,10 +815,11 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       kp.sharedMemBytes = (unsigned)tile_smem_bytes(S);
       kp.kernelParams = args;
       CK(cudaGraphAddKernelNode(&pn[0], if_bodies[0], nullptr, 0, &kp));
-      kp.func = pass_kernel_ptr<false>(S);
-      kp.gridDim = dim3(lc.pass_grid);
-      kp.blockDim = dim3(256);
-      kp.sharedMemBytes = 0;
+      const PassCfg pc = pass_cfg<false>(S);
+      kp.func = pc.fn;
+      kp.gridDim = dim3(pc.grid);
+      kp.blockDim = dim3(pc.block);
+      kp.sharedMemBytes = pc.smem;
       CK(cudaGraphAddKernelNode(&pn[1], if_bodies[1], nullptr, 0, &kp));
     }
     CK(add_kernel(&pn[2], ibody, &if_node, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl,
@@ -844,11 +856,17 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaEventRecord(evs[e0 + 1], st);
       pend.push_back({kind, e0});
     };
+    // PLAS_LEVEL_TRACE=1 (with a profile): one stderr line per level, diagnostics only
+    const bool level_trace = prof && getenv("PLAS_LEVEL_TRACE") && atoi(getenv("PLAS_LEVEL_TRACE"));
+    double lvl_ms[7] = {0, 0, 0, 0, 0, 0, 0};
+    int lvl_n[7] = {0, 0, 0, 0, 0, 0, 0};
     auto flush_profile = [&]() {
       if (!prof) return;
       for (auto& pe : pend) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, evs[pe.e0], evs[pe.e0 + 1]);
+        lvl_ms[pe.kind] += ms;
+        lvl_n[pe.kind] += 1;
         double* slot = &prof->ms_pass + 2 * pe.kind;  // {ms, n} pairs in declaration order
         slot[0] += ms;
         reinterpret_cast<int64_t*>(slot)[1] += 1;
@@ -865,7 +883,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       for (auto e : evs) cudaEventDestroy(e);
     };
     int pp = 0;
-    void* kfn = parity ? pass_kernel_ptr<true>(S) : pass_kernel_ptr<false>(S);
+    const PassCfg kpc = parity ? pass_cfg<true>(S) : pass_cfg<false>(S);
     void* tfn = parity ? tile_kernel_ptr<true>(S) : tile_kernel_ptr<false>(S);
     for (int lv = 0; lv < L; lv++) {
       const int beta = sch.betas[lv];
@@ -967,7 +985,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                                     (size_t)(2 * tile_stage_bytes(beta, S)), st);
             });
           else
-            timed(K_PASS, [&] { le = cudaLaunchKernel(kfn, dim3(lc.pass_grid), dim3(256), args, 0, st); });
+            timed(K_PASS, [&] { le = cudaLaunchKernel(kpc.fn, dim3(kpc.grid), dim3(kpc.block), args, kpc.smem, st); });
           if (le != cudaSuccess) {
             cleanup();
             return fail(PLAS_ERR_CUDA, std::string("pass launch: ") + cudaGetErrorString(le));
@@ -1020,6 +1038,18 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       }
       timed(K_CTRL, [&] { level_end_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0); });
       CKL();
+      if (level_trace) {
+        CK(cudaStreamSynchronize(st));
+        flush_profile();
+        fprintf(stderr, "level %3d h %4d beta %4d %s passes %3d pass %7.1f us blur0 %7.1f blur1 %7.1f border %6.1f "
+                "dist %6.1f ctrl %7.1f us (%d)\n", lv, sch.hs[lv], beta,
+                use_fft ? "fft " : (level_uses_tile_blur(sch.hs[lv], side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax)
+                                        ? "tile" : "dir "),
+                lvl_n[K_PASS], 1e3 * lvl_ms[K_PASS] / (lvl_n[K_PASS] ? lvl_n[K_PASS] : 1), 1e3 * lvl_ms[K_BLUR0],
+                1e3 * lvl_ms[K_BLUR1], 1e3 * lvl_ms[K_BORDER], 1e3 * lvl_ms[K_DIST], 1e3 * lvl_ms[K_CTRL],
+                lvl_n[K_CTRL]);
+        for (int k = 0; k < 7; k++) lvl_ms[k] = 0, lvl_n[k] = 0;
+      }
     }
     CK(cudaStreamSynchronize(st));
     flush_profile();
