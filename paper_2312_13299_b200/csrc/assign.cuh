@@ -443,7 +443,7 @@ __device__ __forceinline__ void load_pass_shared(PassShared& ps, const Ctrl* __r
 //   sel[cls][...] (plas.py:209, built by class_select_kernel).
 // DEVICE: the class grouping is a keyed bijection on [0, m) (Ctrl.fe_*).
 template <bool WIDE, bool PARITY>
-__global__ void __launch_bounds__(256, 4) pass_kernel(float* __restrict__ feat, int* __restrict__ idx,
+__global__ void __launch_bounds__(256, WIDE ? 2 : 4) pass_kernel(float* __restrict__ feat, int* __restrict__ idx,
                                                        const float* __restrict__ target, int D, int S,
                                                        const Ctrl* __restrict__ ctrl,
                                                        const int* __restrict__ sel, long long sel_stride,
@@ -602,7 +602,7 @@ __device__ __forceinline__ TileGeom tile_geom(int b, int nbx, unsigned nbx_m, in
 }
 
 template <bool WIDE, bool PARITY>
-__global__ void __launch_bounds__(TILE_THREADS, 3) tile_pass_kernel(
+__global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
     float* __restrict__ feat, int* __restrict__ idx, const float* __restrict__ target, int D, int S,
     const Ctrl* __restrict__ ctrl, const int* __restrict__ sel, long long sel_stride, MoveOut mo,
     int* __restrict__ counters) {
