@@ -59,6 +59,7 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--no-smoothness", action="store_true")
+    p.add_argument("--no-prep", action="store_true", help="skip the feature-prep (SURVEY 8(f) #1) line")
     p.add_argument("--sharded", action="store_true",
                    help="N > 1: shard ONE grid over the ranks (strong scaling; sharded.py) instead of "
                         "one independent grid per rank")
@@ -347,6 +348,87 @@ def run_smoothness(feats, perm_np, side, device, peak, steps=5):
     return out
 
 
+def run_prep(device, peak, steps=5, n=1_100_000, side=1024, seed=0):
+    """SURVEY 8(f) #1 on the GPU: prune_to_grid -> select (every attribute row
+    gathered) -> normalize_for_sorting -> the post-sort permutation apply of every
+    attribute (bundle.py:134-160), on a seeded degree-3 cloud of n Gaussians
+    pruned to side^2; device-resident, CUDA events.  Algorithmic bytes per
+    kept Gaussian: select and apply each read + write all 59 fp64 channels
+    (2 x 944 B), normalize reads the 9 weighted raw channels and writes 9
+    features (144 B), the logit is read once (8 B).  Next to the reference's
+    own prune_to_grid + normalize_for_sorting + values[perm] on the host."""
+    import torch
+    from paper_2312_13299_b200 import splats as ps
+    g = np.random.default_rng(seed)
+    cl = {"positions": g.normal(0, 3, (n, 3)), "sh_dc": g.normal(0, 0.5, (n, 3)),
+          "sh_rest": g.normal(0, 0.1, (n, 45)), "opacity_logit": g.normal(0, 2, n),
+          "scale_log": g.normal(-4, 1, (n, 3)), "rotation": g.normal(0, 1, (n, 4))}
+    fields = ("positions", "sh_dc", "sh_rest", "opacity_logit", "scale_log", "rotation")
+    attr_of = dict(zip(ps.ATTRIBUTES, fields))
+    dev = {f: torch.from_numpy(np.ascontiguousarray(cl[f])).to(device) for f in fields}
+    keep = side * side
+    perm = torch.from_numpy(np.random.default_rng(seed + 1).permutation(keep)).to(device)
+
+    def step():
+        surv = ps.prune_indices(dev["opacity_logit"], keep)
+        pr = {f: ps.gather_rows(dev[f], surv) for f in fields}
+        feats, _, _ = ps.normalize_features({a: pr[f] for a, f in attr_of.items()})
+        applied = {f: ps.gather_rows(pr[f], perm) for f in fields}
+        return surv, feats, applied
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        surv, feats, _ = step()
+    e1.record()
+    e1.synchronize()
+    ms_eager = e0.elapsed_time(e1) / steps
+    # the same step captured once in a CUDA graph: device time without the
+    # Python / ctypes launch overhead of its ~40 small launches
+    graph = torch.cuda.CUDAGraph()
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(graph, stream=stream):
+            gsurv, gfeats, _ = step()
+    torch.cuda.current_stream().wait_stream(stream)
+    graph.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        graph.replay()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if not (torch.equal(gsurv, surv) and torch.equal(gfeats, feats)):
+        raise RuntimeError("graph replay of the prep step differs from the eager step")
+    alg = keep * (2 * 944 + 144) + n * 8
+    out = {"what": f"prune_to_grid + select + normalize_for_sorting + permutation apply, {n} Gaussians "
+                   f"(degree-3, 59 channels) -> {side}x{side}, fp64, device-resident",
+           "ms": round(ms, 3), "ms_eager": round(ms_eager, 3), "algorithmic_bytes": alg, "achieved_GBps": round(alg / ms / 1e6, 1),
+           "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
+    rp = _reference_module()
+    if rp is not None:
+        from sogs import splats as rsp
+        cloud = rsp.SplatCloud(**cl)
+        layout = rsp.GridLayout(side)
+        pnp = perm.cpu().numpy()
+        t0 = time.perf_counter()
+        pruned = rsp.prune_to_grid(cloud, layout)
+        rfeat, _ = rsp.normalize_for_sorting(pruned)
+        for a in rsp.ATTRIBUTES:
+            pruned.attribute(a)[pnp]
+        out["reference_cpu_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        order = np.argsort(cloud.opacity_logit, kind="stable")
+        out["survivors_identical"] = bool(np.array_equal(surv.cpu().numpy(), np.sort(order[n - keep:])))
+        f = feats.cpu().numpy()
+        out["features_max_ulp"] = int(np.abs(f.view(np.int64) - rfeat.view(np.int64)).max())
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_2312_13299_b200 as plas
@@ -466,6 +548,9 @@ def run_ours(args):
     smooth = None
     if args.config == "C2" and not args.no_smoothness:
         smooth = run_smoothness(feats, perm_np, side, device, measured_peak()[0])
+    prep = None
+    if args.config == "C2" and not args.no_prep and rank == 0:
+        prep = run_prep(device, measured_peak()[0])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -492,7 +577,7 @@ def run_ours(args):
                    "parallelism": (f"one grid sharded over {world} ranks (per-rank group ranges, NCCL "
                                    "all-gather of moved cells + fp64 partials per pass)") if sharded_run
                    else f"{world} independent grid(s), one per rank"},
-        "quality": quality, "e2e": e2e, "roofline": roofline, "kernel_ms": kernel_ms, "smoothness": smooth,
+        "quality": quality, "e2e": e2e, "roofline": roofline, "kernel_ms": kernel_ms, "smoothness": smooth, "prep": prep,
         "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clocks,
     }
     if rank == 0:

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PLAS_ABI_VERSION 2
+#define PLAS_ABI_VERSION 3
 
 enum plas_status {
   PLAS_OK = 0,
@@ -191,6 +191,44 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
                           double huber_delta, int detach_target, const double* weights,
                           int half_width, double* loss_dev, void* ws, size_t ws_bytes,
                           void* stream);
+
+/* ---- caller-side feature preparation ---------------------- */
+
+/* prune_to_grid (splats.py:139-152): indices of the `keep` Gaussians that a
+ * stable ascending argsort of opacity_logit puts last, in increasing index
+ * order, written to survivors (device int64 [keep]).  opacity_logit: device
+ * fp64 [n], finite (SplatCloud validation, splats.py:58-60). */
+size_t plas_prune_workspace_bytes(int64_t n);
+int plas_prune_to_grid(const double* opacity_logit, int64_t n, int64_t keep, int64_t* survivors, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/* One attribute of normalize_for_sorting (splats.py:184-216): device fp64
+ * rows of `channels` values, `row_stride` values apart; activation 0 = none,
+ * 1 = sigmoid, 2 = exp (SplatCloud.activated, splats.py:86-93); weight >= 0
+ * (0: min/max only, no output columns). */
+typedef struct plas_attr {
+  const double* values;
+  int64_t row_stride;
+  int32_t channels;
+  int32_t activation;
+  double weight;
+} plas_attr;
+#define PLAS_MAX_ATTRS 8
+#define PLAS_MAX_ATTR_CHANNELS 64
+
+/* normalize_for_sorting: features (device fp64 [n, feat_cols], feat_cols =
+ * total channels of the weight > 0 attributes, in attribute order) and the
+ * per-channel mins / maxs of every attribute's activated values (device fp64
+ * [total channels], attribute order). */
+size_t plas_normalize_workspace_bytes(int64_t n, int total_channels);
+int plas_normalize_for_sorting(const plas_attr* attrs, int num_attrs, int64_t n, double* features,
+                               int feat_cols, double* mins, double* maxs, void* ws, size_t ws_bytes,
+                               void* stream);
+
+/* Row gather dst[i] = src[index[i]], i < count, rows of row_bytes bytes
+ * (values[perm], bundle.py:160; SplatCloud.select, splats.py:95-104). */
+int plas_gather_rows(const void* src, int64_t row_bytes, const int64_t* index, int64_t count, void* dst,
+                     void* stream);
 
 /* NumPy SeedSequence(seed).generate_state(2, uint64) -> key (Philox4x64 key). */
 void plas_seed_key(uint64_t seed, uint64_t key[2]);

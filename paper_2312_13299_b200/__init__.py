@@ -12,13 +12,15 @@ from .plas import (PERMUTATIONS, SortConfig, block_size, blur_target, grid_dista
                    initial_radius, partition_blocks, reassign_block, sort_grid,
                    sort_grid_report, sort_on_device)
 from .smoothness import DEFAULT_SMOOTHNESS_WEIGHTS, SmoothnessParams, huber, huber_grad, smoothness_loss
-from .splats import DEFAULT_SORT_WEIGHTS, GridLayout, GridStack
+from .splats import (DEFAULT_SORT_WEIGHTS, GridLayout, GridStack, NormalizationSpec, SplatCloud,
+                     build_grid_layout, normalize_for_sorting, prune_to_grid)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "PERMUTATIONS", "SortConfig", "SortReport", "SmoothnessParams", "GridLayout", "GridStack",
-    "DEFAULT_SORT_WEIGHTS", "DEFAULT_SMOOTHNESS_WEIGHTS", "block_size", "blur_target",
+    "DEFAULT_SORT_WEIGHTS", "DEFAULT_SMOOTHNESS_WEIGHTS", "NormalizationSpec", "SplatCloud",
+    "block_size", "blur_target", "build_grid_layout", "normalize_for_sorting", "prune_to_grid",
     "grid_distance", "huber", "huber_grad", "initial_radius", "partition_blocks", "reassign_block",
     "smoothness_loss", "sort_grid", "sort_grid_report", "sort_on_device", "vad",
 ]

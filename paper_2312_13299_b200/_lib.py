@@ -62,6 +62,12 @@ class SortResult(ctypes.Structure):
 
 # exported symbols and their ctypes signatures (restype, argtypes); the
 # CPU test checks this list against include/plas_b200.h
+class Attr(ctypes.Structure):
+    """include/plas_b200.h: plas_attr (one attribute of normalize_for_sorting)."""
+    _fields_ = [("values", ctypes.c_void_p), ("row_stride", ctypes.c_int64), ("channels", ctypes.c_int32),
+                ("activation", ctypes.c_int32), ("weight", ctypes.c_double)]
+
+
 SIGNATURES = {
     "plas_abi_version": (i32, []),
     "plas_sizeof_sort_args": (sz, []),
@@ -79,6 +85,11 @@ SIGNATURES = {
     "plas_grid_distance": (i32, [P, P, P, i64, i32, P, P, sz, P]),
     "plas_vad": (i32, [P, i32, i32, i32, i32, P, P, sz, P]),
     "plas_smoothness_plane": (i32, [P, P, i32, i32, i32, f64, f64, i32, P, i32, P, P, sz, P]),
+    "plas_prune_workspace_bytes": (sz, [i64]),
+    "plas_prune_to_grid": (i32, [P, i64, i64, P, P, sz, P]),
+    "plas_normalize_workspace_bytes": (sz, [i64, i32]),
+    "plas_normalize_for_sorting": (i32, [P, i32, i64, P, i32, P, P, P, sz, P]),
+    "plas_gather_rows": (i32, [P, i64, P, i64, P, P]),
     "plas_seed_key": (None, [u64, P]),
     "plas_host_permutation": (i32, [u64, i64, P]),
 }

@@ -26,6 +26,7 @@
 
 #include "../../include/plas_b200.h"
 #include "assign.cuh"
+#include "prep.cuh"
 #include "blur.cuh"
 #include "blur_fast.cuh"
 #include "blur_fft.cuh"
@@ -1421,6 +1422,112 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
     if (int e = launch_blur(a.t1, a.t2, PLAS_F64, H, W, C, C, half_width, a, false, st)) return e;
     sub_kernel<<<eg, 256, 0, st>>>(a.t3, a.t2, grad, tot);
   }
+  CKL();
+  return PLAS_OK;
+}
+
+// ---------------------------------------------------------------- feature prep
+size_t plas_prune_workspace_bytes(int64_t n) {
+  const long long nb = (n + PREP_CHUNK - 1) / PREP_CHUNK;
+  return 256 + 256 * sizeof(unsigned) + (size_t)std::max(nb, 1LL) * sizeof(int2) + 256;
+}
+
+int plas_prune_to_grid(const double* logit, int64_t n, int64_t keep, int64_t* survivors, void* ws,
+                       size_t ws_bytes, void* stream) {
+  if (!logit || !survivors || n < 1 || keep < 1 || keep > n || n >= (1LL << 31))
+    return fail(PLAS_ERR_INVALID, "prune_to_grid: need 1 <= keep <= n < 2^31");
+  if (!ws || ws_bytes < plas_prune_workspace_bytes(n)) return fail(PLAS_ERR_WORKSPACE, "prune workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver c{(char*)ws};
+  SelectState* s = c.take<SelectState>(1);
+  unsigned* hist = c.take<unsigned>(256);
+  const long long nb = (n + PREP_CHUNK - 1) / PREP_CHUNK;
+  int2* counts = c.take<int2>((size_t)nb);
+  const int grid = grid_for(n, SEL_THREADS, 4);
+  select_init_kernel<<<1, SEL_THREADS, 0, st>>>(s, n - keep, hist);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    select_hist_kernel<<<grid, SEL_THREADS, 0, st>>>(logit, n, s, shift, hist);
+    select_pick_kernel<<<1, SEL_THREADS, 0, st>>>(s, shift, hist);
+  }
+  prune_count_kernel<<<(unsigned)nb, SEL_THREADS, 0, st>>>(logit, n, s, counts);
+  prune_scan_kernel<<<1, 1024, 0, st>>>(counts, (int)nb);
+  prune_write_kernel<<<(unsigned)nb, SEL_THREADS, 0, st>>>(logit, n, s, counts, (long long*)survivors);
+  CKL();
+  return PLAS_OK;
+}
+
+size_t plas_normalize_workspace_bytes(int64_t n, int total_channels) {
+  const int parts = std::min(grid_for(n, 256, 4), 1024);
+  return (size_t)parts * std::max(total_channels, 1) * sizeof(double2) + 256;
+}
+
+int plas_normalize_for_sorting(const plas_attr* attrs, int num_attrs, int64_t n, double* features,
+                               int feat_cols, double* mins, double* maxs, void* ws, size_t ws_bytes,
+                               void* stream) {
+  if (!attrs || num_attrs < 1 || num_attrs > PREP_MAX_ATTRS || n < 1 || !mins || !maxs)
+    return fail(PLAS_ERR_INVALID, "normalize_for_sorting: bad arguments");
+  PrepAttrs at{};
+  int ch = 0, col = 0;
+  for (int i = 0; i < num_attrs; i++) {
+    const plas_attr& a = attrs[i];
+    if (a.channels < 0 || a.activation < 0 || a.activation > 2 || !(a.weight >= 0.0) ||
+        (a.channels > 0 && (!a.values || a.row_stride < a.channels)))
+      return fail(PLAS_ERR_INVALID, "normalize_for_sorting: bad attribute");
+    PrepAttr& p = at.a[i];
+    p.v = a.values;
+    p.stride = a.row_stride;
+    p.channels = a.channels;
+    p.act = a.activation;
+    p.weight = a.weight;
+    p.ch0 = ch;
+    p.col = (a.weight != 0.0 && a.channels > 0) ? col : -1;
+    if (p.col >= 0) col += a.channels;
+    ch += a.channels;
+  }
+  at.count = num_attrs;
+  at.total_ch = ch;
+  if (ch > PREP_MAX_CH) return fail(PLAS_ERR_INVALID, "normalize_for_sorting: too many channels");
+  if (col != feat_cols || (col > 0 && !features))
+    return fail(PLAS_ERR_INVALID, "normalize_for_sorting: feat_cols != channels of the weighted attributes");
+  if (!ws || ws_bytes < plas_normalize_workspace_bytes(n, ch)) return fail(PLAS_ERR_WORKSPACE, "normalize workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ch == 0) return PLAS_OK;
+  const int parts = std::min(grid_for(n, 256, 4), 1024);
+  double2* part = reinterpret_cast<double2*>(ws);
+  prep_minmax_kernel<<<parts, 256, 0, st>>>(at, n, part);
+  prep_minmax_final_kernel<<<1, 1024, 0, st>>>(part, parts, ch, mins, maxs);
+  if (col > 0) prep_write_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(at, n, feat_cols, mins, maxs, features);
+  CKL();
+  return PLAS_OK;
+}
+
+int plas_gather_rows(const void* src, int64_t row_bytes, const int64_t* index, int64_t count, void* dst,
+                     void* stream) {
+  if (count < 0 || row_bytes < 0 || (count > 0 && (!src || !dst || !index)))
+    return fail(PLAS_ERR_INVALID, "gather_rows: bad arguments");
+  if (count == 0 || row_bytes == 0) return PLAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uintptr_t al = (uintptr_t)src | (uintptr_t)dst | (uintptr_t)row_bytes;
+  const int vb = al % 16 == 0 ? 16 : (al % 8 == 0 ? 8 : (al % 4 == 0 ? 4 : 1));
+  const long long rv = row_bytes / vb, total = count * rv;
+  if (total >= (1LL << 32) - 1) return fail(PLAS_ERR_INVALID, "gather_rows: more than 2^32 vectors");
+  unsigned m;
+  int l;
+  make_fastdiv((unsigned)rv, &m, &l);
+  const int grid = grid_for(total, 256, 8);
+  const long long* ix = (const long long*)index;
+  if (vb == 16)
+    gather_rows_kernel<uint4><<<grid, 256, 0, st>>>((const uint4*)src, (unsigned)rv, m, l, ix, (unsigned)total,
+                                                    (uint4*)dst);
+  else if (vb == 8)
+    gather_rows_kernel<unsigned long long><<<grid, 256, 0, st>>>((const unsigned long long*)src, (unsigned)rv, m, l,
+                                                                  ix, (unsigned)total, (unsigned long long*)dst);
+  else if (vb == 4)
+    gather_rows_kernel<unsigned><<<grid, 256, 0, st>>>((const unsigned*)src, (unsigned)rv, m, l, ix, (unsigned)total,
+                                                       (unsigned*)dst);
+  else
+    gather_rows_kernel<unsigned char><<<grid, 256, 0, st>>>((const unsigned char*)src, (unsigned)rv, m, l, ix,
+                                                             (unsigned)total, (unsigned char*)dst);
   CKL();
   return PLAS_OK;
 }

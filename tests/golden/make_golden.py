@@ -393,6 +393,49 @@ def part_paired_null_c1():
     _paired_null("paired_null_c1.json", synthetic.c1(0), {}, list(range(int(os.environ.get("PAIRED_C1", "32")))))
 
 
+def _prep_cloud(seed, n, sh_rest, ties=False):
+    g = np.random.default_rng(seed)
+    logit = g.normal(0.0, 2.0, n)
+    if ties:  # heavy ties, and both signed zeros
+        logit = np.round(logit, 1)
+        logit[g.integers(0, n, n // 20)] = 0.0
+        logit[g.integers(0, n, n // 20)] = -0.0
+    return dict(positions=g.normal(0, 3, (n, 3)), sh_dc=g.normal(0, 0.5, (n, 3)),
+                sh_rest=g.normal(0, 0.1, (n, sh_rest)), opacity_logit=logit,
+                scale_log=g.normal(-4, 1, (n, 3)), rotation=g.normal(0, 1, (n, 4)))
+
+
+def part_prep():
+    """prune_to_grid + normalize_for_sorting (splats.py:139-216) on seeded clouds,
+    run by the reference; inputs and outputs to prep.npz."""
+    from sogs import splats as ref_splats
+    arrays = {}
+    cases = [("a", 0, 1500, 45, True, None), ("b", 1, 300, 0, False, {"opacity": 0.5, "rotation": 2.0}),
+             ("c", 2, 530, 45, True, {"sh_rest": 0.25, "position": 0.0}),
+             ("d", 3, 64, 0, False, {k: 0.0 for k in ("position", "sh_dc", "scale")})]
+    for name, seed, n, shr, ties, weights in cases:
+        cl = _prep_cloud(seed, n, shr, ties)
+        if name == "c":  # one constant channel
+            cl["sh_dc"][:, 1] = 0.25
+        cloud = ref_splats.SplatCloud(**cl)
+        layout = ref_splats.build_grid_layout(n)
+        pruned = ref_splats.prune_to_grid(cloud, layout)
+        order = np.argsort(cloud.opacity_logit, kind="stable")
+        survivors = np.sort(order[cloud.n - layout.cells:])
+        assert np.array_equal(pruned.positions, cloud.positions[survivors])
+        feats, spec = ref_splats.normalize_for_sorting(pruned, weights)
+        for k, v in cl.items():
+            arrays[f"{name}_in_{k}"] = v
+        arrays[f"{name}_keep"] = np.int64(layout.cells)
+        arrays[f"{name}_survivors"] = survivors.astype(np.int64)
+        arrays[f"{name}_features"] = feats
+        for k in ref_splats.ATTRIBUTES:
+            arrays[f"{name}_min_{k}"] = spec.mins[k]
+            arrays[f"{name}_max_{k}"] = spec.maxs[k]
+        arrays[f"{name}_weights"] = np.array([spec.weights[k] for k in ref_splats.ATTRIBUTES])
+    np.savez_compressed(out("prep.npz"), **arrays)
+
+
 PARTS = {k[5:]: v for k, v in globals().items() if k.startswith("part_")}
 
 if __name__ == "__main__":
