@@ -358,6 +358,7 @@ def run_prep(device, peak, steps=5, n=1_100_000, side=1024, seed=0):
     features (144 B), the logit is read once (8 B).  Next to the reference's
     own prune_to_grid + normalize_for_sorting + values[perm] on the host."""
     import torch
+    from paper_2312_13299_b200 import quantization as pq
     from paper_2312_13299_b200 import splats as ps
     g = np.random.default_rng(seed)
     cl = {"positions": g.normal(0, 3, (n, 3)), "sh_dc": g.normal(0, 0.5, (n, 3)),
@@ -369,12 +370,15 @@ def run_prep(device, peak, steps=5, n=1_100_000, side=1024, seed=0):
     keep = side * side
     perm = torch.from_numpy(np.random.default_rng(seed + 1).permutation(keep)).to(device)
 
+    qspec = pq.default_quant_spec()
+
     def step():
         surv = ps.prune_indices(dev["opacity_logit"], keep)
         pr = {f: ps.gather_rows(dev[f], surv) for f in fields}
         feats, _, _ = ps.normalize_features({a: pr[f] for a, f in attr_of.items()})
         applied = {f: ps.gather_rows(pr[f], perm) for f in fields}
-        return surv, feats, applied
+        planes = {a: pq.quantize_planes(a, applied[f], qspec[a], host_ranges=False)[0] for a, f in attr_of.items()}
+        return surv, feats, planes
 
     for _ in range(2):
         step()
@@ -405,9 +409,10 @@ def run_prep(device, peak, steps=5, n=1_100_000, side=1024, seed=0):
     ms = e0.elapsed_time(e1) / steps
     if not (torch.equal(gsurv, surv) and torch.equal(gfeats, feats)):
         raise RuntimeError("graph replay of the prep step differs from the eager step")
-    alg = keep * (2 * 944 + 144) + n * 8
-    out = {"what": f"prune_to_grid + select + normalize_for_sorting + permutation apply, {n} Gaussians "
-                   f"(degree-3, 59 channels) -> {side}x{side}, fp64, device-resident",
+    alg = keep * (2 * 944 + 144 + 472 + 59 * 2) + n * 8  # + quantize: read 59 fp64, write <= 2 B pixels
+    out = {"what": f"bundle.compress up to the PNG encode: prune_to_grid + select + normalize_for_sorting + "
+                   f"permutation apply + contract/quantize/plane packing, {n} Gaussians (degree-3, 59 channels) "
+                   f"-> {side}x{side}, fp64, device-resident (the sort itself is the main line)",
            "ms": round(ms, 3), "ms_eager": round(ms_eager, 3), "algorithmic_bytes": alg, "achieved_GBps": round(alg / ms / 1e6, 1),
            "hbm_frac": round(alg / ms / 1e6 / peak, 4)}
     rp = _reference_module()
@@ -416,12 +421,24 @@ def run_prep(device, peak, steps=5, n=1_100_000, side=1024, seed=0):
         cloud = rsp.SplatCloud(**cl)
         layout = rsp.GridLayout(side)
         pnp = perm.cpu().numpy()
+        from sogs import bundle as rbd
+        from sogs import quantization as rq
+        rspec = rq.default_quant_spec()
         t0 = time.perf_counter()
         pruned = rsp.prune_to_grid(cloud, layout)
         rfeat, _ = rsp.normalize_for_sorting(pruned)
-        for a in rsp.ATTRIBUTES:
-            pruned.attribute(a)[pnp]
+        ref_planes = {}
+        for a in rsp.ATTRIBUTES:  # bundle.py:158-176 without the PNG encode
+            vals = pruned.attribute(a)[pnp]
+            if a == "position":
+                vals = rq.contract(vals)
+            idx, _, _ = rbd._quantize_attribute(vals, rspec[a])
+            per_image = rbd.PLANE_GROUPS[a][0]
+            ref_planes[a] = [idx[:, i * per_image:(i + 1) * per_image] for i in range(vals.shape[1] // per_image)]
         out["reference_cpu_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+        _, _, gplanes = step()
+        out["planes_identical"] = bool(all(
+            np.array_equal(gplanes[a].cpu().numpy().astype(np.int64), np.stack(ref_planes[a])) for a in ref_planes))
         order = np.argsort(cloud.opacity_logit, kind="stable")
         out["survivors_identical"] = bool(np.array_equal(surv.cpu().numpy(), np.sort(order[n - keep:])))
         f = feats.cpu().numpy()

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PLAS_ABI_VERSION 3
+#define PLAS_ABI_VERSION 4
 
 enum plas_status {
   PLAS_OK = 0,
@@ -229,6 +229,20 @@ int plas_normalize_for_sorting(const plas_attr* attrs, int num_attrs, int64_t n,
  * (values[perm], bundle.py:160; SplatCloud.select, splats.py:95-104). */
 int plas_gather_rows(const void* src, int64_t row_bytes, const int64_t* index, int64_t count, void* dst,
                      void* stream);
+
+/* Quantize one attribute into its encoded image planes:
+ * _quantize_attribute (bundle.py:102-115) with contract (quantization.py:8-11)
+ * when `contract`, quantize (quantization.py:28-41) per channel, and the
+ * plane slicing of compress (bundle.py:170-176): channel c goes to image
+ * c / per_image, sample c % per_image; planes = device uint8 (bit_depth 8) or
+ * uint16 (16) [channels / per_image][n][per_image].  data_driven: per-channel
+ * lo = min, hi = max (min + 1 if constant) of the (contracted) values, else
+ * clip_min / clip_max.  lo_out / hi_out: device fp64 [channels] (manifest). */
+size_t plas_quantize_workspace_bytes(int64_t n, int channels);
+int plas_quantize_planes(const double* values, int64_t n, int channels, int64_t row_stride, int contract,
+                         int data_driven, double clip_min, double clip_max, int levels, int bit_depth,
+                         int per_image, void* planes, double* lo_out, double* hi_out, void* ws, size_t ws_bytes,
+                         void* stream);
 
 /* NumPy SeedSequence(seed).generate_state(2, uint64) -> key (Philox4x64 key). */
 void plas_seed_key(uint64_t seed, uint64_t key[2]);

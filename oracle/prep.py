@@ -65,3 +65,35 @@ def normalize_columns(attrs, weights=None):
         cols.append(out)
     feats = np.concatenate(cols, axis=1) if cols else np.zeros((n, 1))
     return feats, mins, maxs
+
+
+# ---- quantization
+PLANE_LAYOUT = {"position": (3, 1), "sh_dc": (3, 1), "opacity": (1, 1), "scale": (3, 1), "rotation": (1, 4),
+                "sh_rest": (3, 15)}  # bundle.py:25-32
+
+
+def quantize_attribute_planes(name, values, levels, clip=None):
+    """bundle.compress's per-attribute step (bundle.py:158-176): positions are
+    contracted (quantization.py:8-11); the range per channel is the clip pair or,
+    data-driven, (min, max) with max replaced by min + 1 on a constant channel
+    (bundle.py:104-109); index = floor(unit (levels - 1) + 0.5) of the clamped
+    affine position (quantization.py:28-41); channels sliced into images of
+    PLANE_LAYOUT[name][0] samples.  Returns (planes int64 (images, n, per_image), lo, hi)."""
+    v = np.asarray(values, dtype=np.float64)
+    v = v.reshape(v.shape[0], -1)
+    if name == "position":
+        v = np.sign(v) * np.log1p(np.abs(v))
+    n, C = v.shape
+    if clip is None:
+        lo = np.array([v[:, c].min() for c in range(C)])
+        hi = np.array([v[:, c].max() for c in range(C)])
+        hi = np.where(hi > lo, hi, lo + 1.0)
+    else:
+        lo, hi = np.full(C, float(clip[0])), np.full(C, float(clip[1]))
+    idx = np.empty((n, C), dtype=np.int64)
+    for c in range(C):
+        x = np.minimum(np.maximum(v[:, c], lo[c]), hi[c])
+        idx[:, c] = np.floor((x - lo[c]) / (hi[c] - lo[c]) * (levels - 1) + 0.5).astype(np.int64)
+    per_image = PLANE_LAYOUT[name][0]
+    planes = np.stack([idx[:, i * per_image:(i + 1) * per_image] for i in range(C // per_image)])
+    return planes, lo, hi

@@ -90,6 +90,8 @@ SIGNATURES = {
     "plas_normalize_workspace_bytes": (sz, [i64, i32]),
     "plas_normalize_for_sorting": (i32, [P, i32, i64, P, i32, P, P, P, sz, P]),
     "plas_gather_rows": (i32, [P, i64, P, i64, P, P]),
+    "plas_quantize_workspace_bytes": (sz, [i64, i32]),
+    "plas_quantize_planes": (i32, [P, i64, i32, i64, i32, i32, f64, f64, i32, i32, i32, P, P, P, P, sz, P]),
     "plas_seed_key": (None, [u64, P]),
     "plas_host_permutation": (i32, [u64, i64, P]),
 }

@@ -1532,4 +1532,39 @@ int plas_gather_rows(const void* src, int64_t row_bytes, const int64_t* index, i
   return PLAS_OK;
 }
 
+size_t plas_quantize_workspace_bytes(int64_t n, int channels) {
+  const int parts = std::min(grid_for(n, 256, 4), 1024);
+  return (size_t)parts * std::max(channels, 1) * sizeof(double2) + 256;
+}
+
+int plas_quantize_planes(const double* values, int64_t n, int channels, int64_t row_stride, int contract,
+                         int data_driven, double clip_min, double clip_max, int levels, int bit_depth,
+                         int per_image, void* planes, double* lo_out, double* hi_out, void* ws, size_t ws_bytes,
+                         void* stream) {
+  if (n < 1 || channels < 1 || channels > 256 || row_stride < channels || !values || !planes || !lo_out ||
+      !hi_out || levels < 2 || (bit_depth != 8 && bit_depth != 16) || per_image < 1 || channels % per_image)
+    return fail(PLAS_ERR_INVALID, "quantize_planes: bad arguments");
+  if (levels > (1 << bit_depth)) return fail(PLAS_ERR_INVALID, "quantize_planes: levels do not fit bit_depth");
+  if (!data_driven && !(clip_min < clip_max)) return fail(PLAS_ERR_INVALID, "clip_min must be below clip_max");
+  if (!ws || ws_bytes < plas_quantize_workspace_bytes(n, channels)) return fail(PLAS_ERR_WORKSPACE, "quantize workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (data_driven) {
+    const int parts = std::min(grid_for(n, 256, 4), 1024);
+    double2* part = reinterpret_cast<double2*>(ws);
+    quant_minmax_kernel<<<parts, 256, 0, st>>>(values, n, channels, row_stride, contract, part);
+    quant_range_kernel<<<1, 1024, 0, st>>>(part, parts, channels, lo_out, hi_out);
+  } else {
+    quant_fill_kernel<<<1, 256, 0, st>>>(lo_out, hi_out, channels, clip_min, clip_max);
+  }
+  const int grid = grid_for(n * channels, 256, 8);
+  if (bit_depth == 8)
+    quant_pack_kernel<unsigned char><<<grid, 256, 0, st>>>(values, n, channels, row_stride, contract, lo_out, hi_out,
+                                                           levels, per_image, (unsigned char*)planes);
+  else
+    quant_pack_kernel<unsigned short><<<grid, 256, 0, st>>>(values, n, channels, row_stride, contract, lo_out,
+                                                            hi_out, levels, per_image, (unsigned short*)planes);
+  CKL();
+  return PLAS_OK;
+}
+
 }  // extern "C"

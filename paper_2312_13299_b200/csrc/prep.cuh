@@ -345,4 +345,92 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const V* __restrict__ 
   }
 }
 
+// ---- quantization (quantization.py:8-51, bundle.py:102-115, 158-188)
+// contract(x) = sign(x) ln(1 + |x|) (quantization.py:8-11)
+__device__ __forceinline__ double contract_value(double x) {
+  const double s = x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0);  // np.sign: +0 for either zero
+  return s * log1p(fabs(x));
+}
+
+// per-CTA per-channel min / max of the (optionally contracted) values
+__global__ void __launch_bounds__(256) quant_minmax_kernel(const double* __restrict__ v, long long n, int C,
+                                                           long long stride, int contract,
+                                                           double2* __restrict__ part) {
+  __shared__ double2 red[256];
+  const int lanes = (int)blockDim.x / C;
+  const int rl = (int)threadIdx.x / C, c = (int)threadIdx.x - rl * C;
+  double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+  if (rl < lanes) {
+    for (long long i = (long long)blockIdx.x * lanes + rl; i < n; i += (long long)gridDim.x * lanes) {
+      double x = __ldg(v + i * stride + c);
+      if (contract) x = contract_value(x);
+      lo = fmin(lo, x);
+      hi = fmax(hi, x);
+    }
+  }
+  red[threadIdx.x] = make_double2(lo, hi);
+  __syncthreads();
+  if ((int)threadIdx.x < C) {
+    double2 r = red[threadIdx.x];
+    for (int t = (int)threadIdx.x + C; t < lanes * C; t += C) {
+      r.x = fmin(r.x, red[t].x);
+      r.y = fmax(r.y, red[t].y);
+    }
+    part[(long long)blockIdx.x * C + threadIdx.x] = r;
+  }
+}
+
+// data-driven range (bundle.py:106-109): lo = min, hi = max if max > min else min + 1
+__global__ void quant_range_kernel(const double2* __restrict__ part, int nparts, int C, double* __restrict__ lo_out,
+                                   double* __restrict__ hi_out) {
+  const int lane = threadIdx.x & 31;
+  for (int c = threadIdx.x >> 5; c < C; c += blockDim.x >> 5) {
+    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+    for (int p = lane; p < nparts; p += 32) {
+      lo = fmin(lo, part[(long long)p * C + c].x);
+      hi = fmax(hi, part[(long long)p * C + c].y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(PLAS_FULL_MASK, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(PLAS_FULL_MASK, hi, o));
+    }
+    if (lane == 0) {
+      lo_out[c] = lo;
+      hi_out[c] = hi > lo ? hi : lo + 1.0;
+    }
+  }
+}
+
+__global__ void quant_fill_kernel(double* __restrict__ lo_out, double* __restrict__ hi_out, int C, double lo,
+                                  double hi) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    lo_out[c] = lo;
+    hi_out[c] = hi;
+  }
+}
+
+// index = floor(((clip(v, lo, hi) - lo) / (hi - lo)) (levels - 1) + 0.5) (quantization.py:28-41),
+// written as the encoded image's pixel: image c / per_image, pixel i, sample c % per_image
+template <typename P>
+__global__ void __launch_bounds__(256) quant_pack_kernel(const double* __restrict__ v, long long n, int C,
+                                                         long long stride, int contract,
+                                                         const double* __restrict__ lo_in,
+                                                         const double* __restrict__ hi_in, int levels,
+                                                         int per_image, P* __restrict__ out) {
+  const long long total = n * C;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / C;
+    const int c = (int)(e - i * C);
+    double x = v[i * stride + c];
+    if (contract) x = contract_value(x);
+    const double lo = lo_in[c], hi = hi_in[c];
+    x = fmin(fmax(x, lo), hi);  // np.clip
+    const double unit = (x - lo) / (hi - lo);
+    const double q = floor(unit * (double)(levels - 1) + 0.5);
+    const int img = c / per_image, w = c - img * per_image;
+    out[((long long)img * n + i) * per_image + w] = (P)(long long)q;
+  }
+}
+
 }  // namespace plas

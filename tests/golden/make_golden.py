@@ -436,6 +436,43 @@ def part_prep():
     np.savez_compressed(out("prep.npz"), **arrays)
 
 
+def part_quant():
+    """bundle.compress's per-attribute quantization (bundle.py:102-115, 158-176,
+    quantization.py:8-41) by the reference on a seeded grid-ordered cloud:
+    values -> pixel planes (uint16) and manifest lo / hi, to quant.npz."""
+    from sogs import bundle as ref_bundle
+    from sogs import quantization as ref_q
+    arrays = {}
+    side = 24
+    n = side * side
+    cl = _prep_cloud(7, n, 45, ties=False)
+    cl["positions"][:5] = [[0.0, -0.0, 1e-300], [5e3, -5e3, 0.5], [1.0, 1.0, 1.0], [-1.0, 2.0, -3.0], [0, 0, 0]]
+    cl["scale_log"][:, 2] = -3.0  # a constant data-driven channel
+    cl["sh_dc"][:3] = [[-9.0, 9.0, 1.0], [4.0, -2.0, 0.0], [3.999999, -1.999999, 0.5]]  # clipping
+    cloud = ref_splats_cloud(cl)
+    spec = ref_q.default_quant_spec()
+    for name in ref_bundle.ATTRIBUTES:
+        values = cloud.attribute(name)
+        if values.shape[1] == 0:
+            continue
+        if name == "position":
+            values = ref_q.contract(values)
+        indices, lo, hi = ref_bundle._quantize_attribute(values, spec[name])
+        per_image, count = ref_bundle.PLANE_GROUPS[name]
+        needed = values.shape[1] // per_image
+        planes = np.stack([indices[:, i * per_image:(i + 1) * per_image] for i in range(needed)])
+        arrays[f"{name}_in"] = cloud.attribute(name)
+        arrays[f"{name}_planes"] = planes.astype(np.uint16)
+        arrays[f"{name}_lo"] = np.array(lo)
+        arrays[f"{name}_hi"] = np.array(hi)
+    np.savez_compressed(out("quant.npz"), **arrays)
+
+
+def ref_splats_cloud(cl):
+    from sogs import splats as ref_splats
+    return ref_splats.SplatCloud(**cl)
+
+
 PARTS = {k[5:]: v for k, v in globals().items() if k.startswith("part_")}
 
 if __name__ == "__main__":
