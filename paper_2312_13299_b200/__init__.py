@@ -11,7 +11,8 @@ from .metrics import SortReport, vad
 from .plas import (PERMUTATIONS, SortConfig, block_size, blur_target, grid_distance,
                    initial_radius, partition_blocks, reassign_block, sort_grid,
                    sort_grid_report, sort_on_device)
-from .smoothness import DEFAULT_SMOOTHNESS_WEIGHTS, SmoothnessParams, huber, huber_grad, smoothness_loss
+from .smoothness import (DEFAULT_SMOOTHNESS_WEIGHTS, SmoothnessParams, huber, huber_grad, smoothness_loss,
+                         smoothness_loss_autograd)
 from .splats import (DEFAULT_SORT_WEIGHTS, GridLayout, GridStack, NormalizationSpec, SplatCloud,
                      build_grid_layout, normalize_for_sorting, prune_to_grid)
 
@@ -22,5 +23,5 @@ __all__ = [
     "DEFAULT_SORT_WEIGHTS", "DEFAULT_SMOOTHNESS_WEIGHTS", "NormalizationSpec", "SplatCloud",
     "block_size", "blur_target", "build_grid_layout", "normalize_for_sorting", "prune_to_grid",
     "grid_distance", "huber", "huber_grad", "initial_radius", "partition_blocks", "reassign_block",
-    "smoothness_loss", "sort_grid", "sort_grid_report", "sort_on_device", "vad",
+    "smoothness_loss", "smoothness_loss_autograd", "sort_grid", "sort_grid_report", "sort_on_device", "vad",
 ]

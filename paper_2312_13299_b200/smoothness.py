@@ -109,3 +109,53 @@ def smoothness_loss(stack, params=None, return_device=False):
         for (coeff, _), v in zip(means, vals):
             loss += coeff * float(v)  # smoothness.py:88, plane order
     return loss, gradients
+
+
+# ---------------------------------------------------------------- trainer integration
+def _plane_function():
+    import torch
+
+    class SmoothnessPlane(torch.autograd.Function):
+        """coeff * mean(Huber(plane - blur(plane))) of one plane with its exact
+        gradient from the fused kernel (forward computes both; backward scales)."""
+
+        @staticmethod
+        def forward(ctx, plane, coeff, params):
+            x = plane.detach().to(dtype=torch.float64).contiguous()
+            mean, grad = smoothness_plane_device(x, coeff, params)
+            ctx.save_for_backward(grad)
+            ctx.out_dtype = plane.dtype
+            return (mean * coeff).reshape(())
+
+        @staticmethod
+        def backward(ctx, g):
+            (grad,) = ctx.saved_tensors
+            return (grad * g).to(ctx.out_dtype), None, None
+
+    return SmoothnessPlane
+
+
+_SmoothnessPlane = None
+
+
+def smoothness_loss_autograd(planes, params=None):
+    """smoothness_loss (smoothness.py:57-97) as a differentiable torch scalar for a
+    training loop: planes = {attribute: (side, side[, C]) CUDA tensor} (any float
+    dtype, requires_grad as the trainer likes); the sum over weighted planes in
+    dict order, as the reference accumulates it.  loss.backward() delivers the
+    same gradients smoothness_loss returns."""
+    import torch
+    global _SmoothnessPlane
+    if _SmoothnessPlane is None:
+        _SmoothnessPlane = _plane_function()
+    params = params or SmoothnessParams()
+    total = None
+    for name, plane in planes.items():
+        coeff = params.overall_multiplier * params.weights.get(name, 0.0)
+        if coeff == 0.0 or plane.numel() == 0:
+            continue
+        term = _SmoothnessPlane.apply(plane, coeff, params)
+        total = term if total is None else total + term
+    if total is None:
+        total = torch.zeros((), dtype=torch.float64, device="cuda")
+    return total

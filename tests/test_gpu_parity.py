@@ -439,3 +439,28 @@ def test_blur_fft_tier_in_place_8192():
     for r in (300.0, 2047.0):
         got, fb = gblur.blur_target_tiers(g, r, 1)
         np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"r={r} fb={fb}")
+
+
+@pytest.mark.gpu
+def test_smoothness_autograd_matches_loss_and_gradients():
+    """SURVEY 8(f) #3: the loss as a torch.autograd.Function for a trainer."""
+    import torch
+    from paper_2312_13299_b200 import smoothness as sm
+    g = np.random.default_rng(4)
+    planes_np = {"opacity": g.normal(size=(40, 40, 1)), "rotation": g.normal(size=(40, 40, 4)),
+                 "scale": g.normal(size=(40, 40, 3))}
+    params = sm.SmoothnessParams(weights={"opacity": 0.3, "rotation": 0.7, "scale": 0.0})
+    stack = plas.GridStack(plas.GridLayout(40), planes_np)
+    ref_loss, ref_grads = plas.smoothness_loss(stack, params)
+    planes = {k: torch.tensor(v, device="cuda", requires_grad=True) for k, v in planes_np.items()}
+    loss = sm.smoothness_loss_autograd(planes, params)
+    assert abs(loss.item() - ref_loss) <= 1e-12 * abs(ref_loss)
+    (2.0 * loss).backward()
+    for k, t in planes.items():
+        want = 2.0 * ref_grads[k] if params.weights[k] else np.zeros_like(planes_np[k])
+        got = t.grad.cpu().numpy() if t.grad is not None else np.zeros_like(planes_np[k])
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-15, err_msg=k)
+    small = {"opacity": torch.tensor(g.normal(size=(6, 6, 1)), device="cuda", requires_grad=True)}
+    p1 = sm.SmoothnessParams(weights={"opacity": 1.0}, kernel_size=3, sigma=1.0)
+    assert torch.autograd.gradcheck(lambda x: sm.smoothness_loss_autograd({"opacity": x}, p1),
+                                    (small["opacity"],), eps=1e-6, atol=1e-8)
