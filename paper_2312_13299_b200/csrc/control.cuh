@@ -175,6 +175,9 @@ __device__ __forceinline__ void set_cond(unsigned long long handle, unsigned v) 
 // Prepare the pass about to run (DEVICE mode draws its own offsets).  Called
 // by all threads of one CTA: thread 0 draws and lays out the pass, threads
 // 0..8 derive the nine block-class Feistel keys in parallel.
+// (the class keys are not kept in Ctrl: the grouping tables are built from the
+// level's pass records, gen_class_tables, so the controller tail only sets
+// the next pass's geometry)
 __device__ __forceinline__ void prepare_device_pass_cta(Ctrl* c, unsigned long long* s_gkey) {
   if (threadIdx.x == 0) {
     int dy, dx;
@@ -183,8 +186,6 @@ __device__ __forceinline__ void prepare_device_pass_cta(Ctrl* c, unsigned long l
     set_pass_geometry_base(c, dy, dx);
     *s_gkey = gk;
   }
-  __syncthreads();
-  if (threadIdx.x < 9) set_class_keys(c, threadIdx.x, *s_gkey);
   __syncthreads();
 }
 
