@@ -44,19 +44,23 @@ __device__ __forceinline__ void fb_append(bool need, int entry, int* __restrict_
 
 struct PadGeom {
   int H, W, C, S;
-  int pad;        // zero elements before/after every line (>= hmax + BLUR_R)
+  int pad;        // zero elements before/after every line (>= hmax + BPAD_R)
 };
 
 // AXIS 0: in = feat interior (row stride W*S, PAD zero rows above/below),
 //         out = tmp interior (row stride (W + 2 pad) * S).
 // AXIS 1: in = tmp interior, out = target (row stride W*S), EPI 1 divides by den32.
+#ifndef BPAD_R
+#define BPAD_R 8  // outputs per thread of the direct fold (register rings of BPAD_R)
+#endif
+
 template <int AXIS, int EPI>
 __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                        PadGeom pg, BlurLevelRef lvl,
                                                        const float* __restrict__ den32,
                                                        int* __restrict__ fb, int fb_cap,
                                                        int* __restrict__ fb_other) {
-  constexpr int R = BLUR_R;
+  constexpr int R = BPAD_R;
   // the other axis' fallback list has been consumed by now: clear its counter
   if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) fb_other[0] = 0;
   int h;

@@ -112,7 +112,10 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 // resident CTAs per SM the register budget must allow (~85 registers at 256 threads)
 // 4 CTAs per SM at 256 threads (64 registers): the passes are latency-bound, so
 // occupancy beats the second buffer (measured: C2 144.5 -> 138.5 ms)
-template <int L> __host__ __device__ constexpr int fft_min_blocks() { return L > 4096 ? 1 : 1024 / fft_threads_for<L>(); }
+#ifndef FFT_MINB
+#define FFT_MINB 4
+#endif
+template <int L> __host__ __device__ constexpr int fft_min_blocks() { return L > 4096 ? 1 : (FFT_MINB * 256) / fft_threads_for<L>(); }
 
 // Pass schedule of an L = 2^LOG2L point FFT: radix-8 passes, then one radix-4
 // or radix-2 pass for the remaining bits.  Pass p has sub-transform size
@@ -243,6 +246,61 @@ struct FftPass {
       }
     }
   }
+
+  // this thread's twiddles of the pass, loaded BEFORE the barrier that precedes
+  // the pass (their latency overlaps the barrier wait instead of the pass)
+  struct Tw {
+    double2 w[NB][R];
+  };
+  __device__ __forceinline__ static void load_tw(Tw& t, const double2* tw) {
+    if (Ns > 1) {
+      unsigned tid;
+      asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+#pragma unroll
+      for (int b = 0; b < NB; b++) {
+        const int j = (int)tid + b * T;
+        if (j < L / R) {
+          const double2* pt = tw + L + fft_pass_twiddle_offset(LOG2L, P) + (j & (Ns - 1));
+#pragma unroll
+          for (int r = 1; r < R; r++) t.w[b][r] = ld_ordered(pt + r * Ns);  // not movable across barriers
+        }
+      }
+    }
+  }
+  // in place with preloaded twiddles: every thread reads, the CTA syncs, every thread writes
+  template <bool SPEC>
+  __device__ __forceinline__ static void run_tw(double2* buf, const Tw& twv, const double* spec) {
+    unsigned tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    double2 v[NB][R];
+#pragma unroll
+    for (int t = 0; t < NB; t++) {
+      const int j = (int)tid + t * T;
+      if (j < L / R) {
+#pragma unroll
+        for (int r = 0; r < R; r++) v[t][r] = buf[fft_pad(j + r * (L / R))];
+        twiddle(v[t], twv.w[t]);
+        dft_small<R>(v[t]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NB; t++) {
+      const int j = (int)tid + t * T;
+      if (j < L / R) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          const int d = dest(j, r);
+          double2 o = v[t][r];
+          if (SPEC) {
+            const double sp = ld_ordered(spec + d);
+            o = make_double2(o.x * sp, -(o.y * sp));
+          }
+          buf[fft_pad(d)] = o;
+        }
+      }
+    }
+  }
 };
 
 template <int LOG2L, int P, int LAST>
@@ -257,6 +315,28 @@ struct FftChain {
     }
   }
 };
+
+// Passes P .. LAST-1 in place with twiddle prefetch: pass p + 1's twiddles are
+// loaded after pass p's writes and before the barrier between them; after the
+// last pass the twiddles of pass LAST (if it exists) go to `next`.
+template <int LOG2L, int P, int LAST>
+struct FftChainTw {
+  template <bool SPEC_LAST, typename NextTw>
+  __device__ __forceinline__ static void run(double2* buf, const double2* tw, const double* spec,
+                                             const typename FftPass<LOG2L, P>::Tw& cur, NextTw& next) {
+    FftPass<LOG2L, P>::template run_tw<SPEC_LAST && P == fft_npasses(LOG2L) - 1>(buf, cur, spec);
+    if constexpr (P + 1 < LAST) {
+      typename FftPass<LOG2L, P + 1>::Tw nt;
+      FftPass<LOG2L, P + 1>::load_tw(nt, tw);
+      __syncthreads();
+      FftChainTw<LOG2L, P + 1, LAST>::template run<SPEC_LAST>(buf, tw, spec, nt, next);
+    } else {
+      if constexpr (LAST < fft_npasses(LOG2L)) FftPass<LOG2L, LAST>::load_tw(next, tw);
+      __syncthreads();
+    }
+  }
+};
+struct NoTw {};
 
 __device__ __forceinline__ double warp_max_sum(double v, double m, double* out_max) {
 #pragma unroll
@@ -352,15 +432,21 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
       red[2 * (tid >> 5)] = ss;
       red[2 * (tid >> 5) + 1] = m;
     }
-    __syncthreads();
   }
+  typename FftPass<LOG2L, 1>::Tw tw1;
+  FftPass<LOG2L, 1>::load_tw(tw1, plan.tw);
+  __syncthreads();
   // ---- rest of the forward FFT (spectrum x conj in its last pass), then the
   //      second FFT up to its last pass
-  FftChain<LOG2L, 1, NP>::template run<true>(bufA, bufB, tid, plan.tw, plan.spec);
-  double2* src2 = (NP - 1) % 2 == 0 ? bufA : bufB;  // where the forward FFT ended
-  double2* oth2 = (NP - 1) % 2 == 0 ? bufB : bufA;
-  FftChain<LOG2L, 0, NP - 1>::template run<false>(src2, oth2, tid, plan.tw, plan.spec);
-  const double2* last_src = (NP - 1) % 2 == 0 ? src2 : oth2;
+  static_assert(fft_inplace<LOG2L>(), "twiddle prefetch assumes the in-place passes");
+  (void)bufB;
+  typename FftPass<LOG2L, NP - 1>::Tw twl;  // the last pass's twiddles, prefetched by the chain
+  {
+    typename FftPass<LOG2L, 0>::Tw tw0;  // pass 0 has no twiddles (Ns = 1)
+    FftChainTw<LOG2L, 1, NP>::template run<true>(bufA, plan.tw, plan.spec, tw1, tw0);
+    FftChainTw<LOG2L, 0, NP - 1>::template run<false>(bufA, plan.tw, plan.spec, tw0, twl);
+  }
+  const double2* last_src = bufA;
   // ---- bound B for this pair
   int h;
   const double* w;
@@ -382,8 +468,8 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
     for (int t = 0; t < PL::NB; t++) {
       const int j = tid + t * T;
       const bool jv = j < L / PL::R;
-      double2 v[PL::R], wv[PL::R];
-      PL::load_twiddles(wv, j, plan.tw);
+      double2 v[PL::R];
+      const double2(&wv)[PL::R] = twl.w[t];
 #pragma unroll
       for (int r = 0; r < PL::R; r++) v[r] = jv ? last_src[fft_pad(j + r * (L / PL::R))] : make_double2(0.0, 0.0);
       PL::twiddle(v, wv);

@@ -272,7 +272,7 @@ void fft_twiddles(int L, std::vector<double2>* tw) {
 }
 
 // zero halo of the padded blur buffers: the largest half-width plus one chunk
-int blur_pad(int side) { return (int)ceil(std::max(side / 2.0 - 1.0, 2.0)) + BLUR_R + 1; }
+int blur_pad(int side) { return (int)ceil(std::max(side / 2.0 - 1.0, 2.0)) + std::max(BLUR_R, BPAD_R) + 1; }
 
 size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long long tcap,
                   int rng_mode, int side, long long list_cap, SortWs* w, int world = 1) {
@@ -616,7 +616,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.D = D;
   lc.side = side;
   lc.n = n;
-  lc.blur_grid = grid_for((long long)side * S * ((side + BLUR_R - 1) / BLUR_R), 256, 8);
+  lc.blur_grid = grid_for((long long)side * S * ((side + BPAD_R - 1) / BPAD_R), 256, 8);
   lc.den_grid = std::min(side, num_sms() * 8);  // border_weight32_kernel: rows per CTA
   lc.fb_grid = num_sms() * 2;
   lc.pg = PadGeom{side, side, D, S, w.pad};
@@ -1182,7 +1182,7 @@ struct TierWs {
 static size_t carve_tiers(char* base, int H, int W, int C, int h, TierWs* t) {
   Carver c{base};
   const int S = row_stride(C);
-  t->pad = h + BLUR_R + 1;
+  t->pad = h + std::max(BLUR_R, BPAD_R) + 1;
   t->feat_floats = (size_t)(H + 2 * t->pad) * W * S;
   t->feat_alloc = c.take<float>(t->feat_floats);
   t->feat = t->feat_alloc ? t->feat_alloc + (size_t)t->pad * W * S : nullptr;
@@ -1262,7 +1262,7 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
     blur_tile_kernel<<<dim3((W + TB_T - 1) / TB_T, (H + TB_T - 1) / TB_T), TB_THREADS, smem, st>>>(t.feat, t.target, pg,
                                                                                                   lv, t.den32);
   } else if (tier == 0) {
-    const int g0 = grid_for((long long)W * S * ((H + BLUR_R - 1) / BLUR_R), 256, 8);
+    const int g0 = grid_for((long long)W * S * ((H + BPAD_R - 1) / BPAD_R), 256, 8);
     blur_pad_kernel<0, 0><<<g0, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap, t.fb1);
     CK(cudaMemcpyAsync(&hc[0], t.fb0, sizeof(int), cudaMemcpyDeviceToHost, st));
     blur_pad_fallback_kernel<0, 0><<<fbg, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap);
