@@ -637,16 +637,28 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
       int* sI = reinterpret_cast<int*>(sT + mmax * S);
       const int row4 = g.ww * nch;
       const float rr4 = __frcp_rn((float)row4), rw = __frcp_rn((float)g.ww);
+      const bool pow2 = (row4 & (row4 - 1)) == 0 && (g.ww & (g.ww - 1)) == 0;  // full blocks at beta = 2^k
+      const int sh4 = 31 - __clz(row4), shw = 31 - __clz(g.ww);
       for (int e = threadIdx.x; e < g.hh * row4; e += blockDim.x) {
         int r, c;
-        split_local((unsigned)e, row4, rr4, &r, &c);
+        if (pow2) {
+          r = e >> sh4;
+          c = e & (row4 - 1);
+        } else {
+          split_local((unsigned)e, row4, rr4, &r, &c);
+        }
         const long long go = ((long long)(g.y0 + r) * side + g.x0) * S + 4 * c;
         cp_async16(sF + 4 * e, feat + go);
         cp_async16(sT + 4 * e, target + go);
       }
       for (int e = threadIdx.x; e < g.hh * g.ww; e += blockDim.x) {
         int r, c;
-        split_local((unsigned)e, g.ww, rw, &r, &c);
+        if (pow2) {
+          r = e >> shw;
+          c = e & (g.ww - 1);
+        } else {
+          split_local((unsigned)e, g.ww, rw, &r, &c);
+        }
         cp_async4(sI + e, idx + (long long)(g.y0 + r) * side + g.x0 + c);
       }
     }
@@ -696,30 +708,31 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
         dst[i] = (int)((code >> (2 * i)) & 3u);
         mv[i] = dst[i] != i;
       }
-      long long gcell[4];
+      // this lane's slot's grid cell; the destinations by shuffle from the quad
+      int ly, lx;
+      split_local((unsigned)l, g.ww, rw, &ly, &lx);
+      const int mycell = (g.y0 + ly) * side + g.x0 + lx;
+      int dcl[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        int ly, lx;
-        split_local((unsigned)rowj[j], g.ww, rw, &ly, &lx);
-        gcell[j] = (long long)(g.y0 + ly) * side + g.x0 + lx;
-      }
+      for (int i = 0; i < 4; i++) dcl[i] = __shfl_sync(PLAS_FULL_MASK, mycell, (lane & ~3) + dst[i]);
       if (!WIDE) {
         if (s < nch) {
 #pragma unroll
           for (int i = 0; i < 4; i++)
-            if (mv[i]) st4(feat + pick4(gcell, dst[i]) * S + 4 * s, Fc[i]);
+            if (mv[i]) st4(feat + (long long)dcl[i] * S + 4 * s, Fc[i]);
         }
       } else {
         for (int c = s; c < nch; c += 4) {
 #pragma unroll
           for (int i = 0; i < 4; i++)
-            if (mv[i]) st4(feat + pick4(gcell, dst[i]) * S + 4 * c, ld4v(sF + (long long)rowj[i] * S + 4 * c));
+            if (mv[i]) st4(feat + (long long)dcl[i] * S + 4 * c, ld4v(sF + (long long)rowj[i] * S + 4 * c));
         }
       }
-      const bool my_mv = pick4(mv, s);
-      const long long dcell = pick4(gcell, pick4(dst, s));
-      if (my_mv) idx[dcell] = sI[pick4(rowj, s)];
-      stage_move<TILE_WARP_LIST>(my_mv, (int)dcell, wlist, &wcnt, mo);
+      const int my_dst = (int)((code >> (2 * s)) & 3u);
+      const bool my_mv = my_dst != s;
+      const int dcell = __shfl_sync(PLAS_FULL_MASK, mycell, (lane & ~3) + my_dst);
+      if (my_mv) idx[dcell] = sI[l];
+      stage_move<TILE_WARP_LIST>(my_mv, dcell, wlist, &wcnt, mo);
     }
     __syncthreads();  // stage st is refilled by the prefetch two iterations on
   }
