@@ -187,18 +187,9 @@ __global__ void border_weight_kernel(const double* __restrict__ row_weight, floa
 // value equals fp32 of the reference fold; otherwise the cell is folded
 // exactly.  O(H W) instead of O(H W h) -- the border plane is data-independent
 // but per level.
-// row_weight[y] = A(y) (border_rows_kernel); col_weight[x] = B(x).
-__global__ void border_cols_kernel(double* __restrict__ col_weight, int W, BlurLevelRef lvl) {
-  int h;
-  const double* w;
-  lvl.get(&h, &w);
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
-    double b = __ldg(w);
-    for (int j = h; j >= 1; j--) b += ((x - j >= 0) ? __ldg(w + j) : 0.0) + ((x + j < W) ? __ldg(w + j) : 0.0);
-    col_weight[x] = b;
-  }
-}
-
+// row_weight[y] = A(y) (border_rows_kernel); col_weight[x] = B(x) -- on the
+// sort's square grid the same array (B(x) = A(x) up to the fold's rounding,
+// which the bound covers).
 __global__ void border_weight32_kernel(const double* __restrict__ row_weight, const double* __restrict__ col_weight,
                                        float* __restrict__ den32, int H, int W, BlurLevelRef lvl) {
   int h;

@@ -164,7 +164,6 @@ struct SortWs {
   double* dcache;  // per-cell fp64 distance to the target (level start + pass updates)
   int* idx;
   double* rowweight;
-  double* colweight;
   double* partials;
   int* flags;  // [0] nonfinite, [1] moved
   double* scalars;  // [0] vad mean, [1] vad0, [2] vad1
@@ -295,7 +294,6 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->dcache = c.take<double>((size_t)n);
   w->idx = c.take<int>((size_t)n);
   w->rowweight = c.take<double>((size_t)side);
-  w->colweight = c.take<double>((size_t)side);
   w->partials = c.take<double>(MAX_PARTS);
   w->flags = c.take<int>(8);
   w->scalars = c.take<double>(8);
@@ -686,13 +684,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     cudaGraphNode_t nd_draws;
     CK(add_kernel(&nd_draws, obody, &nd[0], 1, pass_draws_kernel, dim3(PDRAW_MAX * 16 / 256), dim3(256), w.ctrl,
                   w.pdraw, w.prec));
-    cudaGraphNode_t nd_cols;
-    CK(add_kernel(&nd_cols, obody, &nd_draws, 1, border_cols_kernel, dim3(lc.rows_grid), dim3(128), w.colweight,
-                  side, lc.lvl));
-    CK(add_kernel(&nd[1], obody, &nd_cols, 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
+    // the sort's grid is square, so the column weights B(x) are the row weights
+    // A(x): one fold serves both axes of the certified product (border_weight32)
+    CK(add_kernel(&nd[1], obody, &nd_draws, 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
                   w.rowweight, side, lc.lvl));
     CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight32_kernel, dim3(lc.den_grid), dim3(256),
-                  (const double*)w.rowweight, (const double*)w.colweight, w.den32, side, side, lc.lvl));
+                  (const double*)w.rowweight, (const double*)w.rowweight, w.den32, side, side, lc.lvl));
     // IF (FFT tier this level) { spectrum, fft axis 0, fallback 0, fft axis 1, fallback 1 }
     // ELSE { direct fold axis 0, fallback 0, axis 1, fallback 1 }
     cudaGraphNode_t blur_if;
@@ -895,9 +892,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       });
       const bool use_fft = level_uses_fft(sch.hs[lv], side, hc.fft_min_h, hc.fft_L);
       timed(K_BORDER, [&] {
-        border_cols_kernel<<<lc.rows_grid, 128, 0, st>>>(w.colweight, side, lc.lvl);
         border_rows_kernel<<<lc.rows_grid, 128, 0, st>>>(w.rowweight, side, lc.lvl);
-        border_weight32_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.colweight, w.den32, side, side, lc.lvl);
+        border_weight32_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.rowweight, w.den32, side, side, lc.lvl);
       });
       if (use_fft) {
         timed(K_BLUR0, [&] {
