@@ -249,7 +249,8 @@ __device__ __host__ __forceinline__ bool level_uses_tile_blur(int h, int side, i
   return !level_uses_fft(h, side, fft_min_h, fft_L) && h <= tile_hmax;
 }
 
-__global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_cond, unsigned long long tblur_cond) {
+__global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_cond, unsigned long long tblur_cond,
+                                   unsigned long long tile_cond) {
   if (threadIdx.x) return;
   const int lv = c->level;
   c->beta = s.betas[lv];
@@ -263,6 +264,7 @@ __global__ void level_begin_kernel(Ctrl* c, Sched s, unsigned long long blur_con
   make_fastdiv((unsigned)(c->lv_seg_base + 1), &c->lv_seg_m[1], &c->lv_seg_l[1]);
   set_cond(blur_cond, level_uses_fft(c->h, c->side, c->fft_min_h, c->fft_L) ? 1u : 0u);
   set_cond(tblur_cond, level_uses_tile_blur(c->h, c->side, c->fft_min_h, c->fft_L, c->tile_blur_hmax) ? 1u : 0u);
+  set_cond(tile_cond, use_tile(c->beta, c->S) ? 1u : 0u);  // K3 regime of the whole level (beta is fixed)
   c->pass = 0;
   c->strikes = 0;
   c->level_done = 0;

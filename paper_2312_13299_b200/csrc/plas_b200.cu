@@ -668,19 +668,18 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     //   pass statistics (+controller); level_end.
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle outer_h, inner_h, tile_h;
+    cudaGraphConditionalHandle outer_h, tile_h;
     CK(cudaGraphConditionalHandleCreate(&outer_h, g, L > 0 ? 1 : 0, cudaGraphCondAssignDefault));
     cudaGraphNode_t outer_node;
     cudaGraph_t obody;
     CK(add_while(&outer_node, g, nullptr, 0, outer_h, &obody));
-    CK(cudaGraphConditionalHandleCreate(&inner_h, obody, 0, 0));
     CK(cudaGraphConditionalHandleCreate(&tile_h, obody, 0, 0));
     cudaGraphConditionalHandle blur_h, tblur_h;
     CK(cudaGraphConditionalHandleCreate(&blur_h, obody, 0, 0));
     CK(cudaGraphConditionalHandleCreate(&tblur_h, obody, 0, 0));
     cudaGraphNode_t nd[8];
     CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
-                  (unsigned long long)blur_h, (unsigned long long)tblur_h));
+                  (unsigned long long)blur_h, (unsigned long long)tblur_h, (unsigned long long)tile_h));
     cudaGraphNode_t nd_draws;
     CK(add_kernel(&nd_draws, obody, &nd[0], 1, pass_draws_kernel, dim3(PDRAW_MAX * 16 / 256), dim3(256), w.ctrl,
                   w.pdraw, w.prec));
@@ -777,27 +776,31 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
     }
     nd[4] = blur_if;
-    CK(add_kernel(&nd[5], obody, &nd[4], 1, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
-                  w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
-                  w.spart, done, (unsigned long long)inner_h, (unsigned long long)tile_h, w.sel, w.sel_stride));
-    cudaGraphNode_t inner_node;
-    cudaGraph_t ibody;
-    CK(add_while(&inner_node, obody, &nd[5], 1, inner_h, &ibody));
-    CK(add_kernel(&nd[6], obody, &inner_node, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl,
-                  lc.sched, (unsigned long long)outer_h));
-    cudaGraphNode_t if_node, pn[3];  // [0] tile, [1] gather, [2] statistics
-    cudaGraph_t if_bodies[2];
+    // IF (tile regime this level) { level statistics, WHILE { tile K3, pass
+    // statistics } } ELSE { the same with the gather K3 }: the regime is fixed
+    // per level (beta), so the pass loop carries no conditional of its own
+    cudaGraphNode_t reg_if;
+    cudaGraph_t rbody[2];
     {
       cudaGraphNodeParams p{};
       p.type = cudaGraphNodeTypeConditional;
       p.conditional.handle = tile_h;
       p.conditional.type = cudaGraphCondTypeIf;
       p.conditional.size = 2;
-      CK(cudaGraphAddNode(&if_node, ibody, nullptr, 0, &p));
-      if_bodies[0] = p.conditional.phGraph_out[0];
-      if_bodies[1] = p.conditional.phGraph_out[1];
+      CK(cudaGraphAddNode(&reg_if, obody, &nd[4], 1, &p));
+      rbody[0] = p.conditional.phGraph_out[0];  // tile_h != 0: tile regime
+      rbody[1] = p.conditional.phGraph_out[1];
     }
-    {
+    for (int rg = 0; rg < 2; rg++) {
+      cudaGraph_t rb = rbody[rg];
+      cudaGraphConditionalHandle loop_h;
+      CK(cudaGraphConditionalHandleCreate(&loop_h, rb, 0, 0));
+      cudaGraphNode_t ls, wl, kn, sn;
+      CK(add_kernel(&ls, rb, nullptr, 0, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
+                    w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
+                    w.spart, done, (unsigned long long)loop_h, 0ull, w.sel, w.sel_stride));
+      cudaGraph_t lb;
+      CK(add_while(&wl, rb, &ls, 1, loop_h, &lb));
       float* feat = w.feat;
       int* idx = w.idx;
       const float* target = w.target;
@@ -807,23 +810,27 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       int Dv = D, Sv = S;
       void* args[] = {&feat, &idx, &target, &Dv, &Sv, &ctrl, &sel, &sstride, &ml, &counters};
       cudaKernelNodeParams kp{};
-      kp.func = tile_kernel_ptr<false>(S);
-      kp.gridDim = dim3(lc.tile_grid);
-      kp.blockDim = dim3(TILE_THREADS);
-      kp.sharedMemBytes = (unsigned)tile_smem_bytes(S);
+      if (rg == 0) {
+        kp.func = tile_kernel_ptr<false>(S);
+        kp.gridDim = dim3(lc.tile_grid);
+        kp.blockDim = dim3(TILE_THREADS);
+        kp.sharedMemBytes = (unsigned)tile_smem_bytes(S);
+      } else {
+        const PassCfg pc = pass_cfg<false>(S);
+        kp.func = pc.fn;
+        kp.gridDim = dim3(pc.grid);
+        kp.blockDim = dim3(pc.block);
+        kp.sharedMemBytes = pc.smem;
+      }
       kp.kernelParams = args;
-      CK(cudaGraphAddKernelNode(&pn[0], if_bodies[0], nullptr, 0, &kp));
-      const PassCfg pc = pass_cfg<false>(S);
-      kp.func = pc.fn;
-      kp.gridDim = dim3(pc.grid);
-      kp.blockDim = dim3(pc.block);
-      kp.sharedMemBytes = pc.smem;
-      CK(cudaGraphAddKernelNode(&pn[1], if_bodies[1], nullptr, 0, &kp));
+      CK(cudaGraphAddKernelNode(&kn, lb, nullptr, 0, &kp));
+      CK(add_kernel(&sn, lb, &kn, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl, lc.sched,
+                    (const float*)w.feat, (const float*)w.target, w.dcache, D, S, (const int*)w.list, counters,
+                    w.spart, done, n, (unsigned long long)loop_h, 0ull, (double*)nullptr, w.sel,
+                    w.sel_stride));  // + next pass's tables
     }
-    CK(add_kernel(&pn[2], ibody, &if_node, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl,
-                  lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, D, S,
-                  (const int*)w.list, counters, w.spart, done, n, (unsigned long long)inner_h,
-                  (unsigned long long)tile_h, (double*)nullptr, w.sel, w.sel_stride));  // + next pass's tables
+    CK(add_kernel(&nd[6], obody, &reg_if, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
+                  (unsigned long long)outer_h));
     cudaGraphExec_t ge;
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
@@ -887,7 +894,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       const int beta = sch.betas[lv];
       const long long bsq = (long long)beta * beta;
       timed(K_CTRL, [&] {
-        level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull, 0ull);
+        level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull, 0ull, 0ull);
         if (!parity) pass_draws_kernel<<<PDRAW_MAX * 16 / 256, 256, 0, st>>>(w.ctrl, w.pdraw, w.prec);
       });
       const bool use_fft = level_uses_fft(sch.hs[lv], side, hc.fft_min_h, hc.fft_L);
