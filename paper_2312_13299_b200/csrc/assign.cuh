@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : 4) pass_kernel(float* __restri
                                                        MoveOut mo, int* __restrict__ counters) {
   __shared__ PassShared ps;
   __shared__ int s_list[8 * WARP_LIST];
+  if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
   load_pass_shared(ps, ctrl);
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
@@ -609,6 +610,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
   extern __shared__ float4 smem4[];
   __shared__ PassShared ps;
   __shared__ int s_list[8 * TILE_WARP_LIST];  // small lists: 3 CTAs per SM fit in shared memory
+  if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
   load_pass_shared(ps, ctrl);
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;

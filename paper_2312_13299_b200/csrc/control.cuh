@@ -385,12 +385,21 @@ __device__ __forceinline__ bool last_cta_reduce(double v, double* partials, int*
   return true;
 }
 
+// level_end_kernel's bookkeeping, done in graph mode by the statistics kernel
+// that ends the level (outer != 0), which saves a node per level
+__device__ __forceinline__ void level_end_work(Ctrl* c, Sched s, unsigned long long outer) {
+  s.level_counts[c->level] = c->pass + 1;
+  c->levels_done = c->level + 1;
+  c->level++;
+  if (c->level >= c->num_levels || c->status) set_cond(outer, 0);
+}
+
 // Level start (plas.py:256-258): fp64 distance of every cell to the fresh
 // target into the cache, sum -> previous, trace, open the pass loop.
 __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, long long n, int D, int S, double* partials, int* done,
-    unsigned long long inner, unsigned long long tile_cond, int* tab, long long tab_stride) {
+    unsigned long long inner, unsigned long long outer, int* tab, long long tab_stride) {
   __shared__ double sh[32];
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
@@ -422,6 +431,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
       c->status = 1;
       c->level_done = 1;
       set_cond(inner, 0);
+      if (outer) level_end_work(c, s, outer);
     } else {
       s.trace[c->trace_pos++] = c->previous;
       go = true;
@@ -430,10 +440,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
   go = __syncthreads_or(go);
   if (go) {
     if (c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
-    if (threadIdx.x == 0) {
-      if (c->rng_mode == 1) set_cond(tile_cond, c->tile);
-      set_cond(inner, 1);
-    }
+    if (threadIdx.x == 0) set_cond(inner, 1);
   }
   ctrl_from_smem(cg, &sc);
   if (gen && gridDim.x == 1) gen_class_tables(&sc, 0, tab, tab_stride, 0, 1);
@@ -482,11 +489,12 @@ __device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, lo
 __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
-    double* partials, int* done, long long n, unsigned long long inner, unsigned long long tile_cond,
+    double* partials, int* done, long long n, unsigned long long inner, unsigned long long outer,
     double* xpart, int* tab, long long tab_stride) {
   __shared__ double sh[32];
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
+  if (c->level_done) return;  // an unrolled pass slot after the level ended (no CTA takes a ticket)
   const int count = counters[2];
   double sum = 0.0;
   const int stride = gridDim.x * blockDim.x;
@@ -568,10 +576,8 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     more = controller_step(c, s, s_tot, n, inner);
   }
   more = __syncthreads_or(more);
-  if (more && c->rng_mode == 1) {
-    prepare_device_pass_cta(c, &s_gkey);
-    if (threadIdx.x == 0) set_cond(tile_cond, c->tile);
-  }
+  if (more && c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
+  if (!more && outer && threadIdx.x == 0) level_end_work(c, s, outer);
   ctrl_from_smem(cg, &sc);
   if (gen && gridDim.x == 1) gen_class_tables(&sc, sc.pass, tab, tab_stride, 0, 1);
 }

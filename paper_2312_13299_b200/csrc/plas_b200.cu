@@ -382,6 +382,16 @@ int pass_grid_size(int S) {
   return cached[which];
 }
 
+// passes per iteration of the graph's pass loop (PLAS_PASS_UNROLL, default 3: measured 1 -> 122.1, 2 -> 120.2, 3 -> 119.6, 4 -> 120.0 ms at C2)
+int pass_unroll() {
+  static int v = 0;
+  if (!v) {
+    const char* e = getenv("PLAS_PASS_UNROLL");
+    v = e ? std::max(1, std::min(8, atoi(e))) : 3;
+  }
+  return v;
+}
+
 // K3 launch configuration (gather regime)
 struct PassCfg {
   void* fn;
@@ -798,7 +808,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaGraphNode_t ls, wl, kn, sn;
       CK(add_kernel(&ls, rb, nullptr, 0, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
                     w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
-                    w.spart, done, (unsigned long long)loop_h, 0ull, w.sel, w.sel_stride));
+                    w.spart, done, (unsigned long long)loop_h, (unsigned long long)outer_h, w.sel, w.sel_stride));
       cudaGraph_t lb;
       CK(add_while(&wl, rb, &ls, 1, loop_h, &lb));
       float* feat = w.feat;
@@ -823,14 +833,19 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         kp.sharedMemBytes = pc.smem;
       }
       kp.kernelParams = args;
-      CK(cudaGraphAddKernelNode(&kn, lb, nullptr, 0, &kp));
-      CK(add_kernel(&sn, lb, &kn, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl, lc.sched,
-                    (const float*)w.feat, (const float*)w.target, w.dcache, D, S, (const int*)w.list, counters,
-                    w.spart, done, n, (unsigned long long)loop_h, 0ull, (double*)nullptr, w.sel,
-                    w.sel_stride));  // + next pass's tables
+      // the loop body holds `unroll` passes; a pass slot after the level ended
+      // returns at once (both kernels test Ctrl.level_done), so one loop
+      // iteration's overhead is shared by `unroll` passes
+      cudaGraphNode_t prev = nullptr;
+      for (int u = 0; u < pass_unroll(); u++) {
+        CK(cudaGraphAddKernelNode(&kn, lb, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+        CK(add_kernel(&sn, lb, &kn, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl, lc.sched,
+                      (const float*)w.feat, (const float*)w.target, w.dcache, D, S, (const int*)w.list,
+                      counters, w.spart, done, n, (unsigned long long)loop_h, (unsigned long long)outer_h,
+                      (double*)nullptr, w.sel, w.sel_stride));  // + next pass's tables (+ level end)
+        prev = sn;
+      }
     }
-    CK(add_kernel(&nd[6], obody, &reg_if, 1, level_end_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
-                  (unsigned long long)outer_h));
     cudaGraphExec_t ge;
     CK(cudaGraphInstantiate(&ge, g, 0));
     CK(cudaGraphLaunch(ge, st));
