@@ -134,18 +134,21 @@ __global__ void __launch_bounds__(256) blur_axis_kernel(const Tin* __restrict__ 
 
 // border_weight (blur.py:13-15) of an (H, W) ones plane, exact fp64 fold.
 // row_weight[y] = axis-0 fold of the ones column (identical for every x).
+__device__ __forceinline__ double border_row_value(int y, int H, int h, const double* __restrict__ w) {
+  double a = __dmul_rn(1.0, __ldg(w));
+  for (int j = h; j >= 1; j--) {
+    double p = __dadd_rn((y - j >= 0) ? 1.0 : 0.0, (y + j < H) ? 1.0 : 0.0);
+    a = __dadd_rn(a, __dmul_rn(p, __ldg(w + j)));
+  }
+  return a;
+}
+
 __global__ void border_rows_kernel(double* __restrict__ row_weight, int H, BlurLevelRef lvl) {
   int h;
   const double* w;
   lvl.get(&h, &w);
-  for (int y = blockIdx.x * blockDim.x + threadIdx.x; y < H; y += gridDim.x * blockDim.x) {
-    double a = __dmul_rn(1.0, __ldg(w));
-    for (int j = h; j >= 1; j--) {
-      double p = __dadd_rn((y - j >= 0) ? 1.0 : 0.0, (y + j < H) ? 1.0 : 0.0);
-      a = __dadd_rn(a, __dmul_rn(p, __ldg(w + j)));
-    }
-    row_weight[y] = a;
-  }
+  for (int y = blockIdx.x * blockDim.x + threadIdx.x; y < H; y += gridDim.x * blockDim.x)
+    row_weight[y] = border_row_value(y, H, h, w);
 }
 
 // den[y, x] = axis-1 fold of the plane A[y, :] = row_weight[y]; den(y, x) ==

@@ -568,26 +568,29 @@ inline size_t fft_smem_bytes(int L) {
 // K[m] = w0 + 2 sum_{j=1..h} w_j cos(2 pi j m / L), cosines from the twiddle
 // table (exact index reduction), compensated (TwoProduct + TwoSum) so the
 // error stays ~3 ulp regardless of h.
+__device__ __forceinline__ double fft_spectrum_value(int m, int h, const double* __restrict__ w, const FftPlan& plan) {
+  const int L = plan.L;
+  double s = __ldg(w), comp = 0.0;
+  for (int j = 1; j <= h; j++) {
+    const double cj = __ldg(&plan.tw[(long long)j * m & (L - 1)].x);
+    const double wj2 = 2.0 * __ldg(w + j);
+    const double p = wj2 * cj;
+    const double pe = fma(wj2, cj, -p);  // exact product error
+    const double t = s + p;
+    const double bp = t - s;
+    const double te = (s - (t - bp)) + (p - bp);  // TwoSum error
+    s = t;
+    comp += te + pe;
+  }
+  return s + comp;
+}
+
 __global__ void fft_spectrum_kernel(BlurLevelRef lvl, FftPlan plan) {
   int h;
   const double* w;
   lvl.get(&h, &w);
-  const int L = plan.L;
-  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < L; m += gridDim.x * blockDim.x) {
-    double s = __ldg(w), comp = 0.0;
-    for (int j = 1; j <= h; j++) {
-      const double cj = __ldg(&plan.tw[(long long)j * m & (L - 1)].x);
-      const double wj2 = 2.0 * __ldg(w + j);
-      const double p = wj2 * cj;
-      const double pe = fma(wj2, cj, -p);  // exact product error
-      const double t = s + p;
-      const double bp = t - s;
-      const double te = (s - (t - bp)) + (p - bp);  // TwoSum error
-      s = t;
-      comp += te + pe;
-    }
-    plan.spec[m] = s + comp;
-  }
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < plan.L; m += gridDim.x * blockDim.x)
+    plan.spec[m] = fft_spectrum_value(m, h, w, plan);
 }
 
 }  // namespace plas

@@ -354,12 +354,12 @@ __host__ __device__ __forceinline__ void set_pass_geometry(Ctrl* c, int dy, int 
 // DEVICE-mode per-pass draws: dy, dx and the grouping key come from the
 // Philox4x64-10 stream keyed like NumPy's (SeedSequence state), at counter
 // (block, pass, level, purpose) -- stateless, identical on every GPU.
-__host__ __device__ __forceinline__ void device_pass_draws_at(const Ctrl* c, int level, int pass, int* dy,
+__host__ __device__ __forceinline__ void device_pass_draws_at(const Ctrl* c, int level, int pass, int beta, int* dy,
                                                               int* dx, unsigned long long* gkey) {
   DeviceDraw d;
   d.init(c->key0, c->key1, (unsigned long long)pass, (unsigned long long)level, 0x504153535ull /* "PASS" */);
-  *dy = (int)d.bounded((unsigned)c->beta);
-  *dx = (int)d.bounded((unsigned)c->beta);
+  *dy = (int)d.bounded((unsigned)beta);
+  *dx = (int)d.bounded((unsigned)beta);
   *gkey = d.next64();
 }
 

@@ -203,40 +203,46 @@ __device__ __host__ __forceinline__ bool level_uses_fft(int h, int side, int fft
 
 // DEVICE mode, level start: every pass's draws of this level (stateless in
 // (level, pass)), so no kernel on the per-pass critical path runs Philox.
+// item t = (pass p = t / 16, item t % 16) of the level's draw records: item 9
+// stores the pass's draws, items 0..8 the class shapes and Feistel keys
+__device__ __forceinline__ void pass_draw_item(const Ctrl* c, int level, int beta, int side, int t,
+                                               int4* __restrict__ pdraw, int* __restrict__ prec) {
+  const int p = t >> 4, item = t & 15;
+  if (item > 9) return;
+  int dy, dx;
+  unsigned long long gk;
+  device_pass_draws_at(c, level, p, beta, &dy, &dx, &gk);
+  if (item == 9) {
+    pdraw[p] = make_int4(dy, dx, (int)(unsigned)gk, (int)(unsigned)(gk >> 32));
+    return;
+  }
+  // class `item`: its shape (set_pass_geometry_base) and keys (set_class_keys)
+  const int cls = item, ty = cls / 3, tx = cls % 3;
+  const int fy = dy > 0 ? dy : beta, fx = dx > 0 ? dx : beta;
+  const int nby = num_segments(fy, beta, side), nbx = num_segments(fx, beta, side);
+  int lo, hi, hh, ww;
+  if (ty == 1) hh = beta;
+  else { segment(ty == 0 ? 0 : nby - 1, fy, beta, side, &lo, &hi); hh = hi - lo; }
+  if (tx == 1) ww = beta;
+  else { segment(tx == 0 ? 0 : nbx - 1, fx, beta, side, &lo, &hi); ww = hi - lo; }
+  auto exists = [](int tt, int nn) { return tt == 0 || (tt == 2 && nn >= 2) || (tt == 1 && nn >= 3); };
+  const unsigned m = (unsigned)(hh * ww);
+  Feistel fe;
+  fe.init(class_key(gk, hh, ww), m);
+  int* r = prec + (long long)p * PREC_INTS;
+  r[cls] = (exists(ty, nby) && exists(tx, nbx)) ? (int)m : 0;
+  r[9 + cls] = fe.lbits;
+  r[18 + cls] = fe.rbits;
+  for (int k = 0; k < 6; k++) r[27 + 6 * cls + k] = (int)fe.keys[k];
+}
+
 __global__ void pass_draws_kernel(Ctrl* c, int4* __restrict__ pdraw, int* __restrict__ prec) {
-  // one thread per (pass, class) item (item 9 stores the draws): every chain is
-  // one Philox block plus at most one Feistel key setup
+  // one thread per (pass, class) item: every chain is one Philox block plus at
+  // most one Feistel key setup
   const int level = c->level;
   const int beta = c->beta, side = c->side;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < PDRAW_MAX * 16; t += gridDim.x * blockDim.x) {
-    const int p = t >> 4, item = t & 15;
-    if (item > 9) continue;
-    int dy, dx;
-    unsigned long long gk;
-    device_pass_draws_at(c, level, p, &dy, &dx, &gk);
-    if (item == 9) {
-      pdraw[p] = make_int4(dy, dx, (int)(unsigned)gk, (int)(unsigned)(gk >> 32));
-      continue;
-    }
-    // class `item`: its shape (set_pass_geometry_base) and keys (set_class_keys)
-    const int cls = item, ty = cls / 3, tx = cls % 3;
-    const int fy = dy > 0 ? dy : beta, fx = dx > 0 ? dx : beta;
-    const int nby = num_segments(fy, beta, side), nbx = num_segments(fx, beta, side);
-    int lo, hi, hh, ww;
-    if (ty == 1) hh = beta;
-    else { segment(ty == 0 ? 0 : nby - 1, fy, beta, side, &lo, &hi); hh = hi - lo; }
-    if (tx == 1) ww = beta;
-    else { segment(tx == 0 ? 0 : nbx - 1, fx, beta, side, &lo, &hi); ww = hi - lo; }
-    auto exists = [](int tt, int nn) { return tt == 0 || (tt == 2 && nn >= 2) || (tt == 1 && nn >= 3); };
-    const unsigned m = (unsigned)(hh * ww);
-    Feistel fe;
-    fe.init(class_key(gk, hh, ww), m);
-    int* r = prec + (long long)p * PREC_INTS;
-    r[cls] = (exists(ty, nby) && exists(tx, nbx)) ? (int)m : 0;
-    r[9 + cls] = fe.lbits;
-    r[18 + cls] = fe.rbits;
-    for (int k = 0; k < 6; k++) r[27 + 6 * cls + k] = (int)fe.keys[k];
-  }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < PDRAW_MAX * 16; t += gridDim.x * blockDim.x)
+    pass_draw_item(c, level, beta, side, t, pdraw, prec);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     c->pdraw = pdraw;
     c->prec = prec;

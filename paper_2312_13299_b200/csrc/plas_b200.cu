@@ -321,6 +321,55 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   return align_up(c.off);
 }
 
+// ---------------------------------------------------------------- level set-up (graph mode)
+// The data-independent set-up of a level in one kernel (one graph node instead
+// of four): block ranges [0, nd) build the level's pass draw records
+// (pass_draw_item), [nd, nd + nr) the row weights A(y) (border_row_value),
+// [nd + nr, nd + nr + ns) the real FFT spectrum if the level uses the FFT
+// tier; block 0 thread 0 does level_begin_kernel's bookkeeping.  Every block
+// reads only what is stable across the level boundary (Ctrl.level, side, the
+// keys, the schedule), so no block waits for another.
+__global__ void level_prep_kernel(Ctrl* c, Sched s, unsigned long long blur_cond, unsigned long long tblur_cond,
+                                  unsigned long long tile_cond, int4* __restrict__ pdraw, int* __restrict__ prec,
+                                  double* __restrict__ rowweight, BlurLevelRef lvl, FftPlan plan, int nd, int nr) {
+  const int level = c->level, side = c->side;
+  const int beta = s.betas[level];
+  int h;
+  const double* w;
+  lvl.get(&h, &w);
+  const int b = blockIdx.x;
+  if (b < nd) {
+    for (int t = b * blockDim.x + threadIdx.x; t < PDRAW_MAX * 16; t += nd * blockDim.x)
+      pass_draw_item(c, level, beta, side, t, pdraw, prec);
+    if (b == 0 && threadIdx.x == 0) {
+      c->pdraw = pdraw;
+      c->prec = prec;
+      c->pdraw_level = level;
+      // level_begin_kernel
+      c->beta = beta;
+      c->h = h;
+      c->lv_cap = (beta * beta + 3) / 4;
+      make_fastdiv((unsigned)c->lv_cap, &c->lv_cap_m, &c->lv_cap_l);
+      c->lv_seg_base = num_segments(beta, beta, side);
+      make_fastdiv((unsigned)c->lv_seg_base, &c->lv_seg_m[0], &c->lv_seg_l[0]);
+      make_fastdiv((unsigned)(c->lv_seg_base + 1), &c->lv_seg_m[1], &c->lv_seg_l[1]);
+      set_cond(blur_cond, level_uses_fft(h, side, c->fft_min_h, c->fft_L) ? 1u : 0u);
+      set_cond(tblur_cond, level_uses_tile_blur(h, side, c->fft_min_h, c->fft_L, c->tile_blur_hmax) ? 1u : 0u);
+      set_cond(tile_cond, use_tile(beta, c->S) ? 1u : 0u);
+      c->pass = 0;
+      c->strikes = 0;
+      c->level_done = 0;
+    }
+  } else if (b < nd + nr) {
+    for (int y = (b - nd) * blockDim.x + threadIdx.x; y < side; y += nr * blockDim.x)
+      rowweight[y] = border_row_value(y, side, h, w);
+  } else if (plan.L > 0 && level_uses_fft(h, side, c->fft_min_h, c->fft_L)) {
+    const int ns = gridDim.x - nd - nr;
+    for (int m = (b - nd - nr) * blockDim.x + threadIdx.x; m < plan.L; m += ns * blockDim.x)
+      plan.spec[m] = fft_spectrum_value(m, h, w, plan);
+  }
+}
+
 // ---------------------------------------------------------------- graph helpers
 template <typename... KArgs, typename... Args>
 cudaError_t add_kernel(cudaGraphNode_t* out, cudaGraph_t g, const cudaGraphNode_t* deps, int ndeps,
@@ -688,15 +737,17 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(cudaGraphConditionalHandleCreate(&blur_h, obody, 0, 0));
     CK(cudaGraphConditionalHandleCreate(&tblur_h, obody, 0, 0));
     cudaGraphNode_t nd[8];
-    CK(add_kernel(&nd[0], obody, nullptr, 0, level_begin_kernel, dim3(1), dim3(32), w.ctrl, lc.sched,
-                  (unsigned long long)blur_h, (unsigned long long)tblur_h, (unsigned long long)tile_h));
-    cudaGraphNode_t nd_draws;
-    CK(add_kernel(&nd_draws, obody, &nd[0], 1, pass_draws_kernel, dim3(PDRAW_MAX * 16 / 256), dim3(256), w.ctrl,
-                  w.pdraw, w.prec));
-    // the sort's grid is square, so the column weights B(x) are the row weights
-    // A(x): one fold serves both axes of the certified product (border_weight32)
-    CK(add_kernel(&nd[1], obody, &nd_draws, 1, border_rows_kernel, dim3(lc.rows_grid), dim3(128),
-                  w.rowweight, side, lc.lvl));
+    // level set-up in one node: level_begin + pass draw records + row weights
+    // (+ FFT spectrum); the sort's grid is square, so the column weights B(x)
+    // are the row weights A(x): one fold serves both axes of the certified
+    // product (border_weight32)
+    {
+      const int ndraw = PDRAW_MAX * 16 / 256, nrow = std::max(1, (side + 255) / 256);
+      const int nspec = w.fft_L ? std::max(1, w.fft_L / 256) : 0;
+      CK(add_kernel(&nd[1], obody, nullptr, 0, level_prep_kernel, dim3(ndraw + nrow + nspec), dim3(256), w.ctrl,
+                    lc.sched, (unsigned long long)blur_h, (unsigned long long)tblur_h, (unsigned long long)tile_h,
+                    w.pdraw, w.prec, w.rowweight, lc.lvl, fplan, ndraw, nrow));
+    }
     CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight32_kernel, dim3(lc.den_grid), dim3(256),
                   (const double*)w.rowweight, (const double*)w.rowweight, w.den32, side, side, lc.lvl));
     // IF (FFT tier this level) { spectrum, fft axis 0, fallback 0, fft axis 1, fallback 1 }
@@ -714,8 +765,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       bbody[1] = p.conditional.phGraph_out[1];
     }
     {
-      cudaGraphNode_t fn[5];
-      CK(add_kernel(&fn[0], bbody[0], nullptr, 0, fft_spectrum_kernel, dim3(spec_grid), dim3(128), lc.lvl, fplan));
+      cudaGraphNode_t fn[5];  // [0] unused: the spectrum comes from level_prep_kernel
       {
         const float* in0 = w.feat;
         float* out0 = w.tmp;
@@ -733,7 +783,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         kp.blockDim = dim3(fft_nthreads);
         kp.sharedMemBytes = (unsigned)fft_smem;
         kp.kernelParams = a0;
-        CK(cudaGraphAddKernelNode(&fn[1], bbody[0], &fn[0], 1, &kp));
+        CK(cudaGraphAddKernelNode(&fn[1], bbody[0], nullptr, 0, &kp));
         CK(add_kernel(&fn[2], bbody[0], &fn[1], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
                       (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
         const float* in1 = w.tmp;
