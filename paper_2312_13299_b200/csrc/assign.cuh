@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : 4) pass_kernel(float* __restri
   __shared__ PassShared ps;
   __shared__ int s_list[8 * WARP_LIST];
   if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
+  gtrace_mark(ctrl, 0);
   load_pass_shared(ps, ctrl);
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
@@ -552,6 +553,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : 4) pass_kernel(float* __restri
   flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
+  gtrace_mark(ctrl, 1);
 }
 
 // Tile-regime pass kernel (small blocks).  A CTA walks blocks b = blockIdx.x,
@@ -611,6 +613,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
   __shared__ PassShared ps;
   __shared__ int s_list[8 * TILE_WARP_LIST];  // small lists: 3 CTAs per SM fit in shared memory
   if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
+  gtrace_mark(ctrl, 0);
   load_pass_shared(ps, ctrl);
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
@@ -742,6 +745,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
   flush_moves<TILE_WARP_LIST>(mo, s_list, wcnt, ps.wcnt, &ps.base);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
+  gtrace_mark(ctrl, 1);
 }
 
 // Parity mode: per class (ty, tx) the stable filter master_perm[master_perm < m]

@@ -73,7 +73,21 @@ struct Ctrl {
   unsigned lv_cap_m, lv_seg_m[2];
   int lv_cap_l, lv_seg_l[2], lv_seg_base, lv_cap;
   int gen_pass;                    // pass whose grouping tables gen_tables_kernel builds
+  unsigned long long* gtrace;      // diagnostics (PLAS_GTRACE): per pass ~K3 start, K3 end, ~stats start, stats end
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// record the first start (slot 0/2, stored complemented) or the last time (other slots)
+__device__ __forceinline__ void gtrace_mark(const Ctrl* c, int slot) {
+  if (c->gtrace && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    atomicMax(&c->gtrace[6 * c->reorders + slot], (slot == 0 || slot == 2) ? ~t : t);
+  }
+}
 
 constexpr int PDRAW_MAX = 1024;  // passes per level with precomputed draws (beyond: computed on the fly)
 // per-pass grouping record: m[9], lbits[9], rbits[9], keys[9][6]

@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
   if (c->level_done) return;  // an unrolled pass slot after the level ended (no CTA takes a ticket)
+  gtrace_mark(c, 2);
   const int count = counters[2];
   double sum = 0.0;
   const int stride = gridDim.x * blockDim.x;
@@ -562,8 +563,13 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   int ticket = 0;
   if (!last_cta_reduce(sum, partials, done, &s_tot, sh, &ticket)) {
     if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
+    if (c->gtrace) {
+      __syncthreads();
+      gtrace_mark(c, 5);  // this CTA's table slice is done
+    }
     return;
   }
+  gtrace_mark(c, 4);  // the last CTA has its ticket
   if (c->world > 1) {
     if (threadIdx.x == 0) {
       xpart[0] = s_tot;
@@ -584,6 +590,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   more = __syncthreads_or(more);
   if (more && c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
   if (!more && outer && threadIdx.x == 0) level_end_work(c, s, outer);
+  if (cg->gtrace && threadIdx.x == 0) atomicMax(&cg->gtrace[6 * (sc.reorders - 1) + 3], gtimer());
   ctrl_from_smem(cg, &sc);
   if (gen && gridDim.x == 1) gen_class_tables(&sc, sc.pass, tab, tab_stride, 0, 1);
 }

@@ -598,6 +598,17 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   host::seed_key(a->seed, key);
   hc.key0 = key[0];
   hc.key1 = key[1];
+  // PLAS_GTRACE=1: per-pass globaltimer marks of K3 and the statistics (diagnostics)
+  unsigned long long* gtr = nullptr;
+  if (getenv("PLAS_GTRACE") && atoi(getenv("PLAS_GTRACE"))) {
+    if (cudaMalloc(&gtr, sizeof(unsigned long long) * 6 * (size_t)(tcap + 8)) == cudaSuccess) {
+      cudaMemsetAsync(gtr, 0, sizeof(unsigned long long) * 6 * (size_t)(tcap + 8), st);
+      hc.gtrace = gtr;
+    } else {
+      gtr = nullptr;
+      cudaGetLastError();
+    }
+  }
   hc.fft_min_h = fft_min_h();
   hc.fft_L = w.fft_L;
   hc.tile_blur_hmax = tile_blur_hmax();
@@ -1149,6 +1160,39 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   res->trace_len = out.trace_pos;
   res->cells_moved = fl[2];
   res->exact_warps = fl[3];
+  if (gtr) {
+    std::vector<unsigned long long> g(6 * (size_t)out.reorders);
+    cudaMemcpy(g.data(), gtr, sizeof(unsigned long long) * g.size(), cudaMemcpyDeviceToHost);
+    cudaFree(gtr);
+    double k3 = 0, st_ = 0, gap1 = 0, gap2 = 0, dist = 0, tail = 0, tabs = 0;
+    long long n1 = 0, n2 = 0;
+    for (long long p = 0; p < out.reorders; p++) {
+      const unsigned long long* e = &g[6 * p];
+      if (!e[0] || !e[1] || !e[2] || !e[3] || !e[4]) continue;
+      const double a0 = (double)~e[0], a1 = (double)e[1], b0 = (double)~e[2], b1 = (double)e[3];
+      const double tk = (double)e[4], tb = e[5] ? (double)e[5] : tk;
+      k3 += a1 - a0;
+      st_ += std::max(b1, tb) - b0;
+      gap1 += b0 - a1;
+      dist += tk - b0;
+      tail += b1 - tk;
+      tabs += tb - tk;
+      n1++;
+      if (p + 1 < out.reorders && g[6 * (p + 1)]) {
+        const double c0 = (double)~g[6 * (p + 1)];
+        const double end = std::max(b1, tb);
+        if (c0 > end && c0 - end < 2e4) {  // within a level (a level boundary carries a blur)
+          gap2 += c0 - end;
+          n2++;
+        }
+      }
+    }
+    if (n1)
+      fprintf(stderr, "gtrace: %lld passes  K3 %.2f us  stats %.2f us (to last ticket %.2f, controller tail %.2f, "
+              "tables after ticket %.2f)  gap K3->stats %.2f us  gap stats->K3 %.2f us (%lld)\n",
+              n1, k3 / n1 / 1e3, st_ / n1 / 1e3, dist / n1 / 1e3, tail / n1 / 1e3, tabs / n1 / 1e3,
+              gap1 / n1 / 1e3, n2 ? gap2 / n2 / 1e3 : 0.0, n2);
+  }
   if (out.status) return fail(PLAS_ERR_CAPACITY, "trace capacity exceeded");
   if (res->level_counts && L > 0)
     CK(cudaMemcpy(res->level_counts, w.level_counts, sizeof(long long) * L, cudaMemcpyDeviceToHost));
