@@ -574,13 +574,26 @@ def run_ours(args):
         cpu = cpu_reference_sample(feats, WORKLOADS[args.config]["cfg"], args.cpu_budget,
                                    [len(t) - 1 for _, t in rep["radius_trace"]], "this GPU run's")
 
-    # kernels launched per sort by our library (graph mode, plas_b200.cu): 6 init
-    # + 5 final; per level: begin, 2 border, 4 blur (direct fold + fallback per
-    # axis) or 5 (spectrum + FFT + fallback per axis, h >= 64), stats, end; per
-    # pass: K3 + statistics/controller (parity mode adds 3 per pass)
-    per_pass = 2 if args.mode == "device" else 5
-    fft_levels = sum(1 for r, _ in rep["radius_trace"] if math.ceil(r) >= 64)
-    launches = sum(11 + 8 * L + fft_levels + per_pass * P for L, P in zip(levels, passes))
+    # kernels launched per sort by our library (plas_b200.cu): 6 init + 5 final;
+    # DEVICE (one graph) per level: set-up, border weight, blur (FFT: 2 + 2
+    # fallback kernels for h >= 64; tile: 1 for h <= 4; direct: 2 + 2), level
+    # statistics, and the pass loop in iterations of 3 passes (K3 + statistics
+    # each; the slots after the level's last pass launch and return at once).
+    # PARITY (host-stepped) per level: begin, 2 border, blur (FFT adds the
+    # spectrum kernel), level statistics, level end; per pass: set-pass, class
+    # select, K3, statistics.
+    def blur_launches(h, device):
+        if h >= 64:
+            return 4 if device else 5
+        return 1 if h <= 4 else 4
+    per_level = []
+    for r, tr in rep["radius_trace"]:
+        h, p = math.ceil(r), len(tr) - 1
+        if args.mode == "device":
+            per_level.append(2 + blur_launches(h, True) + 1 + 6 * (-(-p // 3)))
+        else:
+            per_level.append(3 + blur_launches(h, False) + 2 + 4 * p)
+    launches = args.steps * (11 + sum(per_level))  # every timed step runs the same (deterministic) sort
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
