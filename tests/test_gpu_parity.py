@@ -464,3 +464,29 @@ def test_smoothness_autograd_matches_loss_and_gradients():
     p1 = sm.SmoothnessParams(weights={"opacity": 1.0}, kernel_size=3, sigma=1.0)
     assert torch.autograd.gradcheck(lambda x: sm.smoothness_loss_autograd({"opacity": x}, p1),
                                     (small["opacity"],), eps=1e-6, atol=1e-8)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("side,dim", [(256, 6), (128, 14), (96, 21)])
+def test_device_graph_matches_stepped(side, dim):
+    """DEVICE mode runs as one CUDA graph (per-level regime IF, pass loop unrolled
+    x3 with early-exit slots, level set-up node); the profiled run launches the
+    same kernels host-stepped.  Both must give the same permutation, pass counts
+    and trace."""
+    import torch
+    from paper_2312_13299_b200 import _lib
+    from paper_2312_13299_b200.plas import SortPlan
+    g = np.random.default_rng(side + dim)
+    f = torch.from_numpy(g.normal(size=(side * side, dim)).astype(np.float32)).cuda()
+    cfg = plas.SortConfig(rng_seed=3, rng_mode="device")
+    out = []
+    for prof in (None, _lib.SortProfile()):
+        perm = torch.empty(side * side, dtype=torch.int64, device="cuda")
+        rep = SortPlan(side * side, dim, cfg).run(f, perm, None, prof)
+        out.append((perm.cpu().numpy(), rep))
+    (p0, r0), (p1, r1) = out
+    assert np.array_equal(p0, p1)
+    assert r0["reorders"] == r1["reorders"] and r0["cells_moved"] == r1["cells_moved"]
+    assert [len(t) for _, t in r0["radius_trace"]] == [len(t) for _, t in r1["radius_trace"]]
+    np.testing.assert_array_equal(np.concatenate([t for _, t in r0["radius_trace"]]),
+                                  np.concatenate([t for _, t in r1["radius_trace"]]))
