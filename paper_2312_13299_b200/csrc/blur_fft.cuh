@@ -34,7 +34,7 @@
 namespace plas {
 
 struct FftPlan {
-  int log2L;
+  int log2L;          // length code lc (fft_len)
   int L;
   const double2* tw;   // [L] e^{-2 pi i t / L}, then the per-pass tables (fft_pass_twiddle_offset)
   double* spec;        // [L] real spectrum K of the current level (fft_spectrum_kernel)
@@ -63,7 +63,17 @@ __device__ __forceinline__ double ld_ordered(const double* p) {
 
 template <int R>
 __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
-  if (R == 2) {
+  if (R == 3) {
+    // W3 = e^{-2 pi i / 3} = -1/2 - i sqrt3/2
+    const double s3 = 0.86602540378443864676;
+    const double2 t = cadd(v[1], v[2]);
+    const double2 d = mul_mi(csub(v[1], v[2]));  // -i (x1 - x2)
+    const double2 m = make_double2(v[0].x - 0.5 * t.x, v[0].y - 0.5 * t.y);
+    const double2 sd = make_double2(s3 * d.x, s3 * d.y);
+    v[0] = cadd(v[0], t);
+    v[1] = cadd(m, sd);
+    v[2] = csub(m, sd);
+  } else if (R == 2) {
     const double2 a = v[0], b = v[1];
     v[0] = cadd(a, b);
     v[1] = csub(a, b);
@@ -117,22 +127,36 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 #endif
 template <int L> __host__ __device__ constexpr int fft_min_blocks() { return L > 4096 ? 1 : (FFT_MINB * 256) / fft_threads_for<L>(); }
 
-// Pass schedule of an L = 2^LOG2L point FFT: radix-8 passes, then one radix-4
-// or radix-2 pass for the remaining bits.  Pass p has sub-transform size
-// Ns = 8^p before it.
-__host__ __device__ constexpr int fft_npasses(int lg) { return lg / 3 + (lg % 3 ? 1 : 0); }
-__host__ __device__ constexpr int fft_radix(int lg, int p) { return p < lg / 3 ? 8 : (lg % 3 == 2 ? 4 : 2); }
+// FFT length code lc: L = 2^lc for lc < 32, L = 3 * 2^(lc - 32) otherwise
+// (L = 3 * 2^k cuts the padded length of a side-2^(k+1) grid by a quarter:
+// 1536 instead of 2048 at side 1024).  Pass schedule: radix-8 passes over the
+// power-of-two part, one radix-4 or radix-2 pass for its remaining bits, then
+// (3 * 2^k) one radix-3 pass.  Pass p has sub-transform size Ns = product of
+// the earlier radices (always a power of two).
+__host__ __device__ constexpr int fft_len(int lc) { return lc < 32 ? (1 << lc) : (3 << (lc - 32)); }
+__host__ __device__ constexpr int fft_p2(int lc) { return lc < 32 ? lc : lc - 32; }
+__host__ __device__ constexpr bool fft_has3(int lc) { return lc >= 32; }
+__host__ __device__ constexpr int fft_np2(int lc) { return fft_p2(lc) / 3 + (fft_p2(lc) % 3 ? 1 : 0); }
+__host__ __device__ constexpr int fft_npasses(int lc) { return fft_np2(lc) + (fft_has3(lc) ? 1 : 0); }
+__host__ __device__ constexpr int fft_radix(int lc, int p) {
+  return p < fft_np2(lc) ? (p < fft_p2(lc) / 3 ? 8 : (fft_p2(lc) % 3 == 2 ? 4 : 2)) : 3;
+}
+__host__ __device__ constexpr int fft_ns(int lc, int p) { return p < fft_np2(lc) ? (1 << (3 * p)) : (1 << fft_p2(lc)); }
+// lines of up to fft_out_max(lc) samples fit (n + h <= L checked by the caller);
+// the two raw input lines need 2 fft_out_max floats of shared memory
+__host__ __device__ constexpr int fft_out_max(int lc) { return fft_has3(lc) ? (2 << fft_p2(lc)) : fft_len(lc) / 2; }
+__host__ __device__ constexpr int fft_raw_floats(int lc) { return 2 * fft_out_max(lc); }
 
-// Per-pass twiddle tables follow the L-entry table: pass p (Ns = 8^p, radix R)
+// Per-pass twiddle tables follow the L-entry table: pass p (sub-size Ns, radix R)
 // holds W_{Ns R}^{r k} at [L + off_p + r Ns + k], k < Ns, r < R, so the lanes
 // of a warp (consecutive k) read consecutive entries.
-__host__ __device__ constexpr int fft_pass_twiddle_offset(int lg, int p) {
+__host__ __device__ constexpr int fft_pass_twiddle_offset(int lc, int p) {
   int off = 0;
-  for (int q = 0; q < p; q++) off += fft_radix(lg, q) * (1 << (3 * q));
+  for (int q = 0; q < p; q++) off += fft_radix(lc, q) * fft_ns(lc, q);
   return off;
 }
-__host__ __device__ constexpr int fft_twiddle_len(int lg) {
-  return (1 << lg) + fft_pass_twiddle_offset(lg, fft_npasses(lg));
+__host__ __device__ constexpr int fft_twiddle_len(int lc) {
+  return fft_len(lc) + fft_pass_twiddle_offset(lc, fft_npasses(lc));
 }
 
 // Shared-memory layout: one padding slot per 8 complex values, so the radix-8
@@ -150,9 +174,9 @@ template <int LOG2L> __host__ __device__ constexpr bool fft_inplace() { return t
 // dst[(j - k) R + k + r Ns] (natural order after the last pass).
 template <int LOG2L, int P>
 struct FftPass {
-  static constexpr int L = 1 << LOG2L;
+  static constexpr int L = fft_len(LOG2L);
   static constexpr int R = fft_radix(LOG2L, P);
-  static constexpr int Ns = 1 << (3 * P);
+  static constexpr int Ns = fft_ns(LOG2L, P);
   static constexpr int T = fft_threads_for<L>();
   static constexpr int NB = (L / R + T - 1) / T;  // butterflies per thread
 
@@ -360,15 +384,15 @@ __device__ __forceinline__ double warp_max_sum(double v, double m, double* out_m
 // registers and certifies / stores them.  The CTA also settles its own
 // uncertain outputs with the exact SciPy fold from a shared-memory copy of
 // the two input lines (FB_LOCAL of them; any excess goes to the global list).
-// Callers guarantee n + h <= L and n <= L / 2.
+// Callers guarantee n + h <= L and n <= fft_out_max(lc).
 constexpr int FB_LOCAL = 512;
 
 template <int AXIS, int EPI, int LOG2L>
-__global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_blocks<(1 << LOG2L)>())
+__global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blocks<fft_len(LOG2L)>())
     blur_fft_kernel(const float* __restrict__ in, float* __restrict__ out, PadGeom pg, BlurLevelRef lvl,
                     FftPlan plan, const float* __restrict__ den32, int* __restrict__ fb, int fb_cap,
                     int* __restrict__ fb_other) {
-  constexpr int L = 1 << LOG2L;
+  constexpr int L = fft_len(LOG2L);
   constexpr int T = fft_threads_for<L>();
   constexpr int NP = fft_npasses(LOG2L);
   extern __shared__ double2 fbuf[];
@@ -477,7 +501,7 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
 #pragma unroll
       for (int r = 0; r < PL::R; r++) {
         const int i = PL::dest(j, r);
-        if (PL::Ns * r >= L / 2) continue;  // dest(j, r) = j + r Ns >= L/2 >= n: zero padding, unused
+        if (PL::Ns * r >= fft_out_max(LOG2L)) continue;  // dest(j, r) = j + r Ns >= n: zero padding, unused
         const bool in_range = jv && i < n;
         const float dn = (EPI == 1 && in_range) ? den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)] : 1.f;
         float res[2];
@@ -559,9 +583,9 @@ __global__ void __launch_bounds__(fft_threads_for<(1 << LOG2L)>(), fft_min_block
 }
 
 // shared memory of blur_fft_kernel for an L-point FFT
-inline size_t fft_smem_bytes(int L) {
+inline size_t fft_smem_bytes(int lc) {
   const size_t nbuf = 1;  // fft_inplace
-  return sizeof(double2) * nbuf * (size_t)fft_buf_len(L) + sizeof(float) * (size_t)L;
+  return sizeof(double2) * nbuf * (size_t)fft_buf_len(fft_len(lc)) + sizeof(float) * (size_t)fft_raw_floats(lc);
 }
 
 // Real spectrum of the current level's symmetric kernel on L points:
@@ -571,8 +595,11 @@ inline size_t fft_smem_bytes(int L) {
 __device__ __forceinline__ double fft_spectrum_value(int m, int h, const double* __restrict__ w, const FftPlan& plan) {
   const int L = plan.L;
   double s = __ldg(w), comp = 0.0;
+  int jm = 0;  // j m mod L
   for (int j = 1; j <= h; j++) {
-    const double cj = __ldg(&plan.tw[(long long)j * m & (L - 1)].x);
+    jm += m;
+    if (jm >= L) jm -= L;
+    const double cj = __ldg(&plan.tw[jm].x);
     const double wj2 = 2.0 * __ldg(w + j);
     const double p = wj2 * cj;
     const double pe = fma(wj2, cj, -p);  // exact product error

@@ -184,14 +184,15 @@ struct SortWs {
   double2* fft_tw;   // [fft_L] twiddles (large-radius FFT blur)
   double* fft_spec;  // [fft_L] spectrum of the current level
   int fft_L;
+  int fft_lc;        // length code (fft_len(fft_lc) == fft_L), -1 without the FFT tier
 };
 
 // ---------------------------------------------------------------- FFT blur tier
 constexpr int FFT_MIN_LOG2 = 5, FFT_MAX_LOG2 = 13;  // 32 <= L <= 8192 (16 L bytes of shared memory per CTA)
 
 template <int AXIS, int EPI>
-void* fft_kernel_ptr(int log2L) {
-  switch (log2L) {
+void* fft_kernel_ptr(int lc) {
+  switch (lc) {
     case 5: return (void*)blur_fft_kernel<AXIS, EPI, 5>;
     case 6: return (void*)blur_fft_kernel<AXIS, EPI, 6>;
     case 7: return (void*)blur_fft_kernel<AXIS, EPI, 7>;
@@ -201,6 +202,9 @@ void* fft_kernel_ptr(int log2L) {
     case 11: return (void*)blur_fft_kernel<AXIS, EPI, 11>;
     case 12: return (void*)blur_fft_kernel<AXIS, EPI, 12>;
     case 13: return (void*)blur_fft_kernel<AXIS, EPI, 13>;
+    case 32 + 9: return (void*)blur_fft_kernel<AXIS, EPI, 32 + 9>;    // 1536
+    case 32 + 10: return (void*)blur_fft_kernel<AXIS, EPI, 32 + 10>;  // 3072
+    case 32 + 11: return (void*)blur_fft_kernel<AXIS, EPI, 32 + 11>;  // 6144
   }
   return nullptr;
 }
@@ -213,10 +217,36 @@ int next_log2(long long v) {
   return k;
 }
 
-// allocation: L = 2^k >= 2 side covers every h <= side; 0 when too long
-int fft_alloc_length(int side) {
-  const int k = std::max(next_log2(2LL * side), FFT_MIN_LOG2);
-  return k <= FFT_MAX_LOG2 ? (1 << k) : 0;
+// FFT length for lines of n samples and half-widths up to hmax: the shortest
+// instantiated L (2^k, 5 <= k <= 13, or 3 * 2^k, 9 <= k <= 11) with
+// n + hmax <= L and n <= fft_out_max; returns the length code, -1 if none.
+// PLAS_FFT3=0 keeps to powers of two.
+int fft_choose_code(long long n, long long hmax) {
+  static int use3 = -1;
+  if (use3 < 0) {
+    const char* e = getenv("PLAS_FFT3");
+    use3 = e ? atoi(e) != 0 : 1;
+  }
+  int best = -1;
+  for (int lc = FFT_MIN_LOG2; lc <= FFT_MAX_LOG2; lc++)
+    if (n + hmax <= fft_len(lc) && n <= fft_out_max(lc)) {
+      best = lc;
+      break;
+    }
+  if (use3)
+    for (int p = 9; p <= 11; p++) {
+      const int lc = 32 + p;
+      if (n + hmax <= fft_len(lc) && n <= fft_out_max(lc) && (best < 0 || fft_len(lc) < fft_len(best))) {
+        best = lc;
+        break;
+      }
+    }
+  return best;
+}
+// the sort's FFT length code: covers the top level's half-width ceil(side / 2 - 1)
+int fft_alloc_code(int side) {
+  const long long h0 = (long long)ceil(std::max(side / 2.0 - 1.0, 2.0));
+  return fft_choose_code(side, h0);
 }
 
 // smallest half-width that takes the FFT tier (0 = never); PLAS_FFT_MIN_H overrides
@@ -241,12 +271,14 @@ int tile_blur_hmax() {
 }
 
 // relative error constant of the FFT convolution (blur_fft.cuh), x2 safety
-double fft_error_constant(int log2L) {
+// Higham Thm 24.2 per radix-2 stage (eta); the radix-3 stage (two adds per
+// output, a product with the rounded sqrt3 / 2, |A| = sqrt3) is charged 2 eta
+double fft_error_constant(int lc) {
   const double u = ldexp(1.0, -53);
   const double mu = 2.0 * u, g4 = 4.0 * u / (1.0 - 4.0 * u);
   const double eta = mu + g4 * (sqrt(2.0) + mu);
-  const double k = (double)log2L;
-  const double c = k * eta / (1.0 - k * eta);
+  const double ke = (double)fft_p2(lc) * eta + (fft_has3(lc) ? 2.0 * eta : 0.0);
+  const double c = ke / (1.0 - ke);
   const double eK = 4.0 * u;
   const double e2 = (c + u * (1.0 + c)) * (1.0 + eK) + eK;
   return 2.0 * (c * (1.0 + e2) + e2);
@@ -254,19 +286,19 @@ double fft_error_constant(int log2L) {
 
 // e^{-2 pi i t / L} for t < L (correctly rounded from long double), then the
 // per-pass tables W_{Ns R}^{r k} = e^{-2 pi i r k step / L} (blur_fft.cuh)
-void fft_twiddles(int L, std::vector<double2>* tw) {
-  const int lg = next_log2(L);
-  tw->resize(fft_twiddle_len(lg));
+void fft_twiddles(int lc, std::vector<double2>* tw) {
+  const int L = fft_len(lc);
+  tw->resize(fft_twiddle_len(lc));
   const long double pi = 3.141592653589793238462643383279502884L;
   for (int t = 0; t < L; t++) {
     const long double a = -2.0L * pi * (long double)t / (long double)L;
     (*tw)[t] = make_double2((double)cosl(a), (double)sinl(a));
   }
-  for (int p = 0; p < fft_npasses(lg); p++) {
-    const int R = fft_radix(lg, p), Ns = 1 << (3 * p), step = L / (Ns * R);
+  for (int p = 0; p < fft_npasses(lc); p++) {
+    const int R = fft_radix(lc, p), Ns = fft_ns(lc, p), step = L / (Ns * R);
     for (int r = 0; r < R; r++)
       for (int k = 0; k < Ns; k++)
-        (*tw)[L + fft_pass_twiddle_offset(lg, p) + r * Ns + k] = (*tw)[((long long)r * k * step) & (L - 1)];
+        (*tw)[L + fft_pass_twiddle_offset(lc, p) + r * Ns + k] = (*tw)[((long long)r * k * step) % L];
   }
 }
 
@@ -315,8 +347,9 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS);
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
-  w->fft_L = fft_alloc_length(side);
-  w->fft_tw = c.take<double2>(w->fft_L ? (size_t)fft_twiddle_len(next_log2(w->fft_L)) : 1);
+  w->fft_lc = fft_alloc_code(side);
+  w->fft_L = w->fft_lc >= 0 ? fft_len(w->fft_lc) : 0;
+  w->fft_tw = c.take<double2>(w->fft_L ? (size_t)fft_twiddle_len(w->fft_lc) : 1);
   w->fft_spec = c.take<double>((size_t)std::max(w->fft_L, 1));
   return align_up(c.off);
 }
@@ -627,7 +660,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   CK(cudaMemsetAsync(w.fb1, 0, sizeof(int) * FB_HEADER, st));
   std::vector<double2> htw;
   if (w.fft_L) {
-    fft_twiddles(w.fft_L, &htw);
+    fft_twiddles(w.fft_lc, &htw);
     CK(cudaMemcpyAsync(w.fft_tw, htw.data(), sizeof(double2) * htw.size(), cudaMemcpyHostToDevice, st));
   }
 
@@ -694,12 +727,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.pass_grid = pass_grid_size(S);
   lc.tile_grid = tile_grid_size(S);
   lc.lvl = BlurLevelRef{w.ctrl, w.hs, w.weights, w.woff, 0, nullptr};
-  const int fft_log2 = w.fft_L ? next_log2(w.fft_L) : 0;
+  const int fft_log2 = w.fft_L ? w.fft_lc : 0;  // length code
   const FftPlan fplan{fft_log2, w.fft_L, w.fft_tw, w.fft_spec, w.fft_L ? fft_error_constant(fft_log2) : 0.0};
   const int fft_nthreads = w.fft_L ? fft_threads(w.fft_L) : 32;
   void* fft0 = w.fft_L ? fft_kernel_ptr<0, 0>(fft_log2) : nullptr;
   void* fft1 = w.fft_L ? fft_kernel_ptr<1, 1>(fft_log2) : nullptr;
-  const size_t fft_smem = w.fft_L ? fft_smem_bytes(w.fft_L) : 0;
+  const size_t fft_smem = w.fft_L ? fft_smem_bytes(w.fft_lc) : 0;
   int fft_grid = 1;
   if (w.fft_L) {
     CK(cudaFuncSetAttribute(fft0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
@@ -1287,7 +1320,7 @@ struct TierWs {
   double *rows, *w, *spec;
   double2* tw;
   int *fb0, *fb1;
-  int pad, fb_cap, L;
+  int pad, fb_cap, L, lc;
   size_t feat_floats, tmp_floats;
 };
 
@@ -1305,11 +1338,10 @@ static size_t carve_tiers(char* base, int H, int W, int C, int h, TierWs* t) {
   t->den32 = c.take<float>((size_t)H * W);
   t->rows = c.take<double>((size_t)H);
   t->w = c.take<double>((size_t)h + 1);
-  // FFT length: L >= n + h (linear convolution) and n <= L / 2 (the kernel's raw-line buffer)
-  const int k = std::max(std::max(next_log2((long long)std::max(H, W) + h), next_log2(2LL * std::max(H, W))),
-                         FFT_MIN_LOG2);
-  t->L = k <= FFT_MAX_LOG2 ? 1 << k : 0;
-  t->tw = c.take<double2>(t->L ? (size_t)fft_twiddle_len(next_log2(t->L)) : 1);
+  // FFT length: L >= n + h (linear convolution) and n <= fft_out_max (the raw-line buffer)
+  t->lc = fft_choose_code(std::max(H, W), h);
+  t->L = t->lc >= 0 ? fft_len(t->lc) : 0;
+  t->tw = c.take<double2>(t->L ? (size_t)fft_twiddle_len(t->lc) : 1);
   t->spec = c.take<double>((size_t)std::max(t->L, 1));
   t->fb_cap = (int)std::min<long long>((long long)H * W * S / 8 + 1024, 1LL << 26);
   t->fb0 = c.take<int>((size_t)FB_HEADER + t->fb_cap);
@@ -1383,13 +1415,13 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
     blur_pad_fallback_kernel<1, 1><<<fbg, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap);
   } else {
     std::vector<double2> htw;
-    fft_twiddles(t.L, &htw);
+    fft_twiddles(t.lc, &htw);
     CK(cudaMemcpyAsync(t.tw, htw.data(), sizeof(double2) * htw.size(), cudaMemcpyHostToDevice, st));
-    const int lg = next_log2(t.L);
+    const int lg = t.lc;
     const FftPlan plan{lg, t.L, t.tw, t.spec, fft_error_constant(lg)};
     void* f0 = fft_kernel_ptr<0, 0>(lg);
     void* f1 = fft_kernel_ptr<1, 1>(lg);
-    const size_t smem = fft_smem_bytes(t.L);
+    const size_t smem = fft_smem_bytes(t.lc);
     CK(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nt = fft_threads(t.L);
