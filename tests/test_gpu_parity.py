@@ -432,13 +432,15 @@ def test_sort_wide_rows_parity_vs_oracle(side, dim):
                                [v for _, t in wrep["radius_trace"] for v in t], rtol=1e-12)
 
 
-def test_blur_fft_tier_in_place_8192():
-    """L = 8192 (4096-wide lines, configs[4]): the single-buffer in-place FFT variant."""
-    rng = np.random.default_rng(29)
-    g = rng.normal(0, 1, (8, 4096, 3)).astype(np.float32)
-    for r in (300.0, 2047.0):
+@pytest.mark.parametrize("width,radii", [(4096, (300.0, 2047.0)), (2048, (600.0, 1023.0)), (1024, (64.0, 200.0))])
+def test_blur_fft_tier_long_lines(width, radii):
+    """Long lines through the FFT tier: 4096 (configs[4]) and 2048 (configs[3]) wide
+    lines take L = 6144 / 3072 (3 * 2^k, radix-3 last pass), 1024 takes 1536."""
+    rng = np.random.default_rng(29 + width)
+    g = rng.normal(0, 1, (8 if width > 2048 else 4, width, 3)).astype(np.float32)
+    for r in radii:
         got, fb = gblur.blur_target_tiers(g, r, 1)
-        np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"r={r} fb={fb}")
+        np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"width={width} r={r} fb={fb}")
 
 
 @pytest.mark.gpu
