@@ -582,8 +582,10 @@ def run_ours(args):
     # PARITY (host-stepped) per level: begin, 2 border, blur (FFT adds the
     # spectrum kernel), level statistics, level end; per pass: set-pass, class
     # select, K3, statistics.
+    fft_min_h = 48 if side <= 1024 else 64  # plas_b200.cu fft_min_h: L <= 2048 (side 1024 -> L 1536) or longer
+
     def blur_launches(h, device):
-        if h >= 64:
+        if h >= fft_min_h:
             return 4 if device else 5
         return 1 if h <= 4 else 4
     per_level = []

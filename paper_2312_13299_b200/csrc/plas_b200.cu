@@ -249,15 +249,17 @@ int fft_alloc_code(int side) {
   return fft_choose_code(side, h0);
 }
 
-// smallest half-width that takes the FFT tier (0 = never); PLAS_FFT_MIN_H overrides
-int fft_min_h() {
-  static int v = -1;
-  if (v < 0) {
+// smallest half-width that takes the FFT tier for length L (0 = never);
+// PLAS_FFT_MIN_H overrides.  Measured crossovers: 48 at C2 (L = 1536: 114.7 vs
+// 115.5 ms at 64), 64 at C4 (L = 6144: 2.625 vs 2.641 s at 48).
+int fft_min_h(int L) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("PLAS_FFT_MIN_H");
-    v = e ? atoi(e) : 64;  // measured crossover at C2: direct ~85 + 3.4 h us per axis, FFT ~290 us
-    if (v < 0) v = 0;
+    v = e ? std::max(atoi(e), 0) : -1;
   }
-  return v;
+  if (v >= 0) return v;
+  return L <= 2048 ? 48 : 64;
 }
 
 // largest half-width of the one-kernel tile blur (0 = off); PLAS_TILE_BLUR_HMAX overrides
@@ -642,7 +644,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaGetLastError();
     }
   }
-  hc.fft_min_h = fft_min_h();
+  hc.fft_min_h = fft_min_h(w.fft_L);
   hc.fft_L = w.fft_L;
   hc.tile_blur_hmax = tile_blur_hmax();
   hc.rank = world > 1 ? a->rank : 0;
