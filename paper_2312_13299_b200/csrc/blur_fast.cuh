@@ -298,12 +298,15 @@ __global__ void __launch_bounds__(TB_THREADS) blur_tile_kernel(const float* __re
   const int y0 = blockIdx.y * TB_T, x0 = blockIdx.x * TB_T;
   const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned ni_m;  // multiply-shift division by the staged side (no integer division per element)
+  int ni_l;
+  make_fastdiv((unsigned)NI, &ni_m, &ni_l);
   for (int cp = 0; cp < (C + 1) / 2; cp++) {
     const bool has_b = 2 * cp + 1 < C;
     // ---- stage the input tile (rows outside [0, H) are feat's zero halo rows)
     float mx = 0.f;
     for (int e = threadIdx.x; e < NI * NI; e += TB_THREADS) {
-      const int r = e / NI, cc = e - r * NI;
+      const int r = (int)fastdiv((unsigned)e, ni_m, ni_l), cc = e - r * NI;
       const int y = y0 - h + r, x = x0 - h + cc;
       float2 v = make_float2(0.f, 0.f);
       if (x >= 0 && x < W && y < H + pg.pad)
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(TB_THREADS) blur_tile_kernel(const float* __re
     // ---- axis 0: rows [h, h + T) of the stage, every staged column
     float mx1 = 0.f;
     for (int e = threadIdx.x; e < TB_T * NI; e += TB_THREADS) {
-      const int r = e / NI, cc = e - r * NI;
+      const int r = (int)fastdiv((unsigned)e, ni_m, ni_l), cc = e - r * NI;
       const int x = x0 - h + cc;
       double2 o = make_double2(0.0, 0.0);
       if (x >= 0 && x < W && y0 + r < H) {
