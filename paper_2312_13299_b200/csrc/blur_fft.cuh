@@ -63,7 +63,25 @@ __device__ __forceinline__ double ld_ordered(const double* p) {
 
 template <int R>
 __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
-  if (R == 3) {
+  if (R == 5) {
+    // W5^k = e^{-2 pi i k / 5}: y_k = x0 + sum_{m=1..4} W5^{k m} x_m, paired as
+    // (x1 + x4, x1 - x4), (x2 + x3, x2 - x3)
+    const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;  // cos 2pi/5, cos 4pi/5
+    const double s1 = 0.95105651629515357212, s2 = 0.58778525229247312917;   // sin 2pi/5, sin 4pi/5
+    const double2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+    const double2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+    const double2 x0 = v[0];
+    const double2 r1 = make_double2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
+    const double2 r2 = make_double2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
+    // -i (s1 b1 + s2 b2) and -i (s2 b1 - s1 b2)
+    const double2 i1 = mul_mi(make_double2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y));
+    const double2 i2 = mul_mi(make_double2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y));
+    v[0] = cadd(x0, cadd(a1, a2));
+    v[1] = cadd(r1, i1);
+    v[4] = csub(r1, i1);
+    v[2] = cadd(r2, i2);
+    v[3] = csub(r2, i2);
+  } else if (R == 3) {
     // W3 = e^{-2 pi i / 3} = -1/2 - i sqrt3/2
     const double s3 = 0.86602540378443864676;
     const double2 t = cadd(v[1], v[2]);
@@ -127,25 +145,34 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 #endif
 template <int L> __host__ __device__ constexpr int fft_min_blocks() { return L > 4096 ? 1 : (FFT_MINB * 256) / fft_threads_for<L>(); }
 
-// FFT length code lc: L = 2^lc for lc < 32, L = 3 * 2^(lc - 32) otherwise
-// (L = 3 * 2^k cuts the padded length of a side-2^(k+1) grid by a quarter:
-// 1536 instead of 2048 at side 1024).  Pass schedule: radix-8 passes over the
-// power-of-two part, one radix-4 or radix-2 pass for its remaining bits, then
-// (3 * 2^k) one radix-3 pass.  Pass p has sub-transform size Ns = product of
-// the earlier radices (always a power of two).
-__host__ __device__ constexpr int fft_len(int lc) { return lc < 32 ? (1 << lc) : (3 << (lc - 32)); }
-__host__ __device__ constexpr int fft_p2(int lc) { return lc < 32 ? lc : lc - 32; }
-__host__ __device__ constexpr bool fft_has3(int lc) { return lc >= 32; }
+// FFT length code lc = p2 + 32 m: L = M 2^p2 with M = 1, 3, 5, 9 for m = 0..3
+// (the odd factors cut the padded length: at side 1024 a level with h <= 128
+// uses 1152, h <= 256 1280, h <= 511 1536, instead of 2048).  Pass schedule:
+// radix-8 passes over the power-of-two part, one radix-4 or radix-2 pass for
+// its remaining bits, then the odd part: one radix-3 (M = 3), one radix-5
+// (M = 5) or two radix-3 passes (M = 9).  Pass p has sub-transform size Ns =
+// product of the earlier radices.
+__host__ __device__ constexpr int fft_mult(int lc) { return (lc >> 5) == 0 ? 1 : ((lc >> 5) == 1 ? 3 : ((lc >> 5) == 2 ? 5 : 9)); }
+__host__ __device__ constexpr int fft_p2(int lc) { return lc & 31; }
+__host__ __device__ constexpr int fft_len(int lc) { return fft_mult(lc) << fft_p2(lc); }
 __host__ __device__ constexpr int fft_np2(int lc) { return fft_p2(lc) / 3 + (fft_p2(lc) % 3 ? 1 : 0); }
-__host__ __device__ constexpr int fft_npasses(int lc) { return fft_np2(lc) + (fft_has3(lc) ? 1 : 0); }
+__host__ __device__ constexpr int fft_nodd(int lc) { return fft_mult(lc) == 1 ? 0 : (fft_mult(lc) == 9 ? 2 : 1); }
+__host__ __device__ constexpr int fft_npasses(int lc) { return fft_np2(lc) + fft_nodd(lc); }
 __host__ __device__ constexpr int fft_radix(int lc, int p) {
-  return p < fft_np2(lc) ? (p < fft_p2(lc) / 3 ? 8 : (fft_p2(lc) % 3 == 2 ? 4 : 2)) : 3;
+  return p < fft_np2(lc) ? (p < fft_p2(lc) / 3 ? 8 : (fft_p2(lc) % 3 == 2 ? 4 : 2)) : (fft_mult(lc) == 5 ? 5 : 3);
 }
-__host__ __device__ constexpr int fft_ns(int lc, int p) { return p < fft_np2(lc) ? (1 << (3 * p)) : (1 << fft_p2(lc)); }
-// lines of up to fft_out_max(lc) samples fit (n + h <= L checked by the caller);
-// the two raw input lines need 2 fft_out_max floats of shared memory
-__host__ __device__ constexpr int fft_out_max(int lc) { return fft_has3(lc) ? (2 << fft_p2(lc)) : fft_len(lc) / 2; }
+__host__ __device__ constexpr int fft_ns(int lc, int p) {
+  return p < fft_np2(lc) ? (1 << (3 * p)) : (p == fft_np2(lc) ? (1 << fft_p2(lc)) : (3 << fft_p2(lc)));
+}
+// lines of up to fft_out_max(lc) samples fit (n + h <= L checked by the caller):
+// L / 2 for powers of two, else the largest power of two below L; the two raw
+// input lines need 2 fft_out_max floats of shared memory
+__host__ __device__ constexpr int fft_out_max(int lc) {
+  return fft_mult(lc) == 1 ? fft_len(lc) / 2 : (fft_mult(lc) == 3 ? 2 : (fft_mult(lc) == 5 ? 4 : 8)) << fft_p2(lc);
+}
 __host__ __device__ constexpr int fft_raw_floats(int lc) { return 2 * fft_out_max(lc); }
+// radix-2-stage equivalents charged to the error bound for the odd passes
+__host__ __device__ constexpr int fft_odd_stages(int lc) { return fft_mult(lc) == 1 ? 0 : (fft_mult(lc) == 3 ? 2 : (fft_mult(lc) == 5 ? 3 : 4)); }
 
 // Per-pass twiddle tables follow the L-entry table: pass p (sub-size Ns, radix R)
 // holds W_{Ns R}^{r k} at [L + off_p + r Ns + k], k < Ns, r < R, so the lanes
@@ -183,7 +210,7 @@ struct FftPass {
   // twiddles W_{Ns R}^{r k}, r = 1..R-1 (all R-1 loads issued together)
   __device__ __forceinline__ static void load_twiddles(double2 (&wv)[R], int j, const double2* __restrict__ tw) {
     if (Ns > 1) {
-      const int k = j & (Ns - 1);
+      const int k = jmod(j);
       const double2* pt = tw + L + fft_pass_twiddle_offset(LOG2L, P) + k;
 #pragma unroll
       for (int r = 1; r < R; r++) wv[r] = __ldg(pt + r * Ns);
@@ -195,8 +222,9 @@ struct FftPass {
       for (int r = 1; r < R; r++) v[r] = cmul(v[r], wv[r]);
     }
   }
+  __device__ __forceinline__ static int jmod(int j) { return (Ns & (Ns - 1)) == 0 ? (j & (Ns - 1)) : (j % Ns); }
   __device__ __forceinline__ static int dest(int j, int r) {
-    const int k = j & (Ns - 1);
+    const int k = jmod(j);
     return (j - k) * R + k + r * Ns;
   }
   // smem -> smem (SPEC: multiply by the real spectrum and conjugate)
@@ -284,7 +312,7 @@ struct FftPass {
       for (int b = 0; b < NB; b++) {
         const int j = (int)tid + b * T;
         if (j < L / R) {
-          const double2* pt = tw + L + fft_pass_twiddle_offset(LOG2L, P) + (j & (Ns - 1));
+          const double2* pt = tw + L + fft_pass_twiddle_offset(LOG2L, P) + jmod(j);
 #pragma unroll
           for (int r = 1; r < R; r++) t.w[b][r] = ld_ordered(pt + r * Ns);  // not movable across barriers
         }

@@ -181,14 +181,18 @@ struct SortWs {
   int* list;      // moved-cell list of the current pass
   double* spart;  // statistic-kernel partials
   float* orig32;      // sharding: f32 features in element order
-  double2* fft_tw;   // [fft_L] twiddles (large-radius FFT blur)
-  double* fft_spec;  // [fft_L] spectrum of the current level
-  int fft_L;
-  int fft_lc;        // length code (fft_len(fft_lc) == fft_L), -1 without the FFT tier
+  // FFT tier: up to FFT_PLANS lengths (the shortest that fits each level's h)
+  int fft_count;                   // number of lengths
+  int fft_codes[4];                // length codes, increasing length
+  double2* fft_tws[4];             // twiddles of each length
+  double* fft_spec;                // spectrum of the current level (longest length)
+  FftPlan* fft_plans;              // device copies of the plans (level_prep_kernel)
+  int* lvl_mode;                   // per level: plan index, FFT_PLANS = tile tier, FFT_PLANS + 1 = direct
+  int fft_L;                       // longest length (0: no FFT tier)
 };
 
 // ---------------------------------------------------------------- FFT blur tier
-constexpr int FFT_MIN_LOG2 = 5, FFT_MAX_LOG2 = 13;  // 32 <= L <= 8192 (16 L bytes of shared memory per CTA)
+constexpr int FFT_PLANS = 4;  // 32 <= L <= 8192 (16 L bytes of shared memory per CTA)
 
 template <int AXIS, int EPI>
 void* fft_kernel_ptr(int lc) {
@@ -205,48 +209,59 @@ void* fft_kernel_ptr(int lc) {
     case 32 + 9: return (void*)blur_fft_kernel<AXIS, EPI, 32 + 9>;    // 1536
     case 32 + 10: return (void*)blur_fft_kernel<AXIS, EPI, 32 + 10>;  // 3072
     case 32 + 11: return (void*)blur_fft_kernel<AXIS, EPI, 32 + 11>;  // 6144
+    case 64 + 9: return (void*)blur_fft_kernel<AXIS, EPI, 64 + 9>;    // 2560
+    case 64 + 10: return (void*)blur_fft_kernel<AXIS, EPI, 64 + 10>;  // 5120
   }
   return nullptr;
 }
 
 int fft_threads(int L) { return L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8); }
 
-int next_log2(long long v) {
-  int k = 0;
-  while ((1LL << k) < v) k++;
-  return k;
-}
-
 // FFT length for lines of n samples and half-widths up to hmax: the shortest
-// instantiated L (2^k, 5 <= k <= 13, or 3 * 2^k, 9 <= k <= 11) with
-// n + hmax <= L and n <= fft_out_max; returns the length code, -1 if none.
-// PLAS_FFT3=0 keeps to powers of two.
+// instantiated L (2^k, 5 <= k <= 13; 3 * 2^k, 9 <= k <= 11; 5 * 2^k, 9 <= k
+// <= 10) with n + hmax <= L and n <= fft_out_max; returns the length code, -1
+// if none.  PLAS_FFT3 = bit mask of the odd factors allowed (1: 3, 2: 5; 0
+// keeps to powers of two).  Measured: 2560 beats 3072 at C3
+// (1.895 vs 2.033 s), 1280 loses to 1536 at C2 (114.9 vs 114.3 ms), so 5 * 2^8
+// is not offered; the 9 * 2^k lengths (radix-3 twice) lost at every config.
 int fft_choose_code(long long n, long long hmax) {
-  static int use3 = -1;
-  if (use3 < 0) {
+  static int odd_mask = -1;
+  if (odd_mask < 0) {
     const char* e = getenv("PLAS_FFT3");
-    use3 = e ? atoi(e) != 0 : 1;
+    odd_mask = e ? (atoi(e) & 3) : 3;
   }
+  static const int codes[] = {5, 6, 7, 8, 9, 10, 11, 12, 13,           // 2^k
+                              32 + 9, 32 + 10, 32 + 11,               // 3 2^k
+                              64 + 9, 64 + 10};                       // 5 2^k
   int best = -1;
-  for (int lc = FFT_MIN_LOG2; lc <= FFT_MAX_LOG2; lc++)
-    if (n + hmax <= fft_len(lc) && n <= fft_out_max(lc)) {
-      best = lc;
-      break;
-    }
-  if (use3)
-    for (int p = 9; p <= 11; p++) {
-      const int lc = 32 + p;
-      if (n + hmax <= fft_len(lc) && n <= fft_out_max(lc) && (best < 0 || fft_len(lc) < fft_len(best))) {
-        best = lc;
-        break;
-      }
-    }
+  for (int lc : codes) {
+    if (lc >= 32 && !(odd_mask >> (lc / 32 - 1) & 1)) continue;
+    if (n + hmax <= fft_len(lc) && n <= fft_out_max(lc) && (best < 0 || fft_len(lc) < fft_len(best))) best = lc;
+  }
   return best;
 }
 // the sort's FFT length code: covers the top level's half-width ceil(side / 2 - 1)
 int fft_alloc_code(int side) {
   const long long h0 = (long long)ceil(std::max(side / 2.0 - 1.0, 2.0));
   return fft_choose_code(side, h0);
+}
+int fft_min_h(int L);
+// the lengths a sort at this side can use: the shortest fitting length of every
+// half-width from the crossover up to the top level's (sorted by length)
+void fft_plan_codes(int side, int* count, int* codes) {
+  *count = 0;
+  const int top = fft_alloc_code(side);
+  if (top < 0) return;
+  const long long h0 = (long long)ceil(std::max(side / 2.0 - 1.0, 2.0));
+  const int hmin = std::max(fft_min_h(fft_len(top)), 1);
+  for (long long h = hmin; h <= h0; h++) {
+    const int lc = fft_choose_code(side, h);
+    if (lc < 0) continue;
+    bool seen = false;
+    for (int i = 0; i < *count; i++) seen |= codes[i] == lc;
+    if (!seen && *count < 4) codes[(*count)++] = lc;
+  }
+  std::sort(codes, codes + *count, [](int a, int b) { return fft_len(a) < fft_len(b); });
 }
 
 // smallest half-width that takes the FFT tier for length L (0 = never);
@@ -279,7 +294,7 @@ double fft_error_constant(int lc) {
   const double u = ldexp(1.0, -53);
   const double mu = 2.0 * u, g4 = 4.0 * u / (1.0 - 4.0 * u);
   const double eta = mu + g4 * (sqrt(2.0) + mu);
-  const double ke = (double)fft_p2(lc) * eta + (fft_has3(lc) ? 2.0 * eta : 0.0);
+  const double ke = (double)(fft_p2(lc) + fft_odd_stages(lc)) * eta;
   const double c = ke / (1.0 - ke);
   const double eK = 4.0 * u;
   const double e2 = (c + u * (1.0 + c)) * (1.0 + eK) + eK;
@@ -349,10 +364,13 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS);
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
-  w->fft_lc = fft_alloc_code(side);
-  w->fft_L = w->fft_lc >= 0 ? fft_len(w->fft_lc) : 0;
-  w->fft_tw = c.take<double2>(w->fft_L ? (size_t)fft_twiddle_len(w->fft_lc) : 1);
+  fft_plan_codes(side, &w->fft_count, w->fft_codes);
+  w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
+  for (int i = 0; i < 4; i++)
+    w->fft_tws[i] = i < w->fft_count ? c.take<double2>((size_t)fft_twiddle_len(w->fft_codes[i])) : nullptr;
   w->fft_spec = c.take<double>((size_t)std::max(w->fft_L, 1));
+  w->fft_plans = c.take<FftPlan>(4);
+  w->lvl_mode = c.take<int>((size_t)std::max(L, 1));
   return align_up(c.off);
 }
 
@@ -364,10 +382,12 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
 // tier; block 0 thread 0 does level_begin_kernel's bookkeeping.  Every block
 // reads only what is stable across the level boundary (Ctrl.level, side, the
 // keys, the schedule), so no block waits for another.
-__global__ void level_prep_kernel(Ctrl* c, Sched s, unsigned long long blur_cond, unsigned long long tblur_cond,
-                                  unsigned long long tile_cond, int4* __restrict__ pdraw, int* __restrict__ prec,
-                                  double* __restrict__ rowweight, BlurLevelRef lvl, FftPlan plan, int nd, int nr) {
+__global__ void level_prep_kernel(Ctrl* c, Sched s, unsigned long long blur_switch, unsigned long long tile_cond,
+                                  int4* __restrict__ pdraw, int* __restrict__ prec, double* __restrict__ rowweight,
+                                  BlurLevelRef lvl, const int* __restrict__ lvl_mode,
+                                  const FftPlan* __restrict__ plans, int nplans, int nd, int nr) {
   const int level = c->level, side = c->side;
+  const int mode = lvl_mode[level];
   const int beta = s.betas[level];
   int h;
   const double* w;
@@ -388,8 +408,7 @@ __global__ void level_prep_kernel(Ctrl* c, Sched s, unsigned long long blur_cond
       c->lv_seg_base = num_segments(beta, beta, side);
       make_fastdiv((unsigned)c->lv_seg_base, &c->lv_seg_m[0], &c->lv_seg_l[0]);
       make_fastdiv((unsigned)(c->lv_seg_base + 1), &c->lv_seg_m[1], &c->lv_seg_l[1]);
-      set_cond(blur_cond, level_uses_fft(h, side, c->fft_min_h, c->fft_L) ? 1u : 0u);
-      set_cond(tblur_cond, level_uses_tile_blur(h, side, c->fft_min_h, c->fft_L, c->tile_blur_hmax) ? 1u : 0u);
+      set_cond(blur_switch, (unsigned)mode);
       set_cond(tile_cond, use_tile(beta, c->S) ? 1u : 0u);
       c->pass = 0;
       c->strikes = 0;
@@ -398,7 +417,8 @@ __global__ void level_prep_kernel(Ctrl* c, Sched s, unsigned long long blur_cond
   } else if (b < nd + nr) {
     for (int y = (b - nd) * blockDim.x + threadIdx.x; y < side; y += nr * blockDim.x)
       rowweight[y] = border_row_value(y, side, h, w);
-  } else if (plan.L > 0 && level_uses_fft(h, side, c->fft_min_h, c->fft_L)) {
+  } else if (mode < nplans) {
+    const FftPlan plan = plans[mode];
     const int ns = gridDim.x - nd - nr;
     for (int m = (b - nd - nr) * blockDim.x + threadIdx.x; m < plan.L; m += ns * blockDim.x)
       plan.spec[m] = fft_spectrum_value(m, h, w, plan);
@@ -660,10 +680,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   CK(cudaMemsetAsync(w.target, 0, sizeof(float) * n * S, st));
   CK(cudaMemsetAsync(w.fb0, 0, sizeof(int) * FB_HEADER, st));
   CK(cudaMemsetAsync(w.fb1, 0, sizeof(int) * FB_HEADER, st));
-  std::vector<double2> htw;
-  if (w.fft_L) {
-    fft_twiddles(w.fft_lc, &htw);
-    CK(cudaMemcpyAsync(w.fft_tw, htw.data(), sizeof(double2) * htw.size(), cudaMemcpyHostToDevice, st));
+  std::vector<std::vector<double2>> htw(w.fft_count);
+  for (int i = 0; i < w.fft_count; i++) {
+    fft_twiddles(w.fft_codes[i], &htw[i]);
+    CK(cudaMemcpyAsync(w.fft_tws[i], htw[i].data(), sizeof(double2) * htw[i].size(), cudaMemcpyHostToDevice, st));
   }
 
   // ---- initial permutation (plas.py:241)
@@ -729,21 +749,39 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.pass_grid = pass_grid_size(S);
   lc.tile_grid = tile_grid_size(S);
   lc.lvl = BlurLevelRef{w.ctrl, w.hs, w.weights, w.woff, 0, nullptr};
-  const int fft_log2 = w.fft_L ? w.fft_lc : 0;  // length code
-  const FftPlan fplan{fft_log2, w.fft_L, w.fft_tw, w.fft_spec, w.fft_L ? fft_error_constant(fft_log2) : 0.0};
-  const int fft_nthreads = w.fft_L ? fft_threads(w.fft_L) : 32;
-  void* fft0 = w.fft_L ? fft_kernel_ptr<0, 0>(fft_log2) : nullptr;
-  void* fft1 = w.fft_L ? fft_kernel_ptr<1, 1>(fft_log2) : nullptr;
-  const size_t fft_smem = w.fft_L ? fft_smem_bytes(w.fft_lc) : 0;
-  int fft_grid = 1;
-  if (w.fft_L) {
-    CK(cudaFuncSetAttribute(fft0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
-    CK(cudaFuncSetAttribute(fft1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fft0, fft_nthreads, fft_smem));
-    fft_grid = side * ((D + 1) / 2);  // one CTA per line pair
+  // FFT plans (one per length) and the per-level blur mode: plan index for
+  // the FFT tier, FFT_PLANS for the tile tier, FFT_PLANS + 1 for the direct fold
+  const int NPL = w.fft_count;
+  FftPlan fplans[4];
+  void* fft0s[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* fft1s[4] = {nullptr, nullptr, nullptr, nullptr};
+  int fft_nthreads[4] = {32, 32, 32, 32};
+  size_t fft_smems[4] = {0, 0, 0, 0};
+  for (int i = 0; i < NPL; i++) {
+    const int lcode = w.fft_codes[i];
+    fplans[i] = FftPlan{lcode, fft_len(lcode), w.fft_tws[i], w.fft_spec, fft_error_constant(lcode)};
+    fft0s[i] = fft_kernel_ptr<0, 0>(lcode);
+    fft1s[i] = fft_kernel_ptr<1, 1>(lcode);
+    fft_nthreads[i] = fft_threads(fft_len(lcode));
+    fft_smems[i] = fft_smem_bytes(lcode);
+    CK(cudaFuncSetAttribute(fft0s[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smems[i]));
+    CK(cudaFuncSetAttribute(fft1s[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smems[i]));
   }
-  const int spec_grid = std::max(1, w.fft_L / 128);
+  const int fft_grid = side * ((D + 1) / 2);  // one CTA per line pair
+  std::vector<int> hmode(std::max(L, 1));
+  for (int lv = 0; lv < L; lv++) {
+    const int h = sch.hs[lv];
+    int m = level_uses_tile_blur(h, side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax) ? NPL : NPL + 1;
+    if (NPL && level_uses_fft(h, side, hc.fft_min_h, hc.fft_L)) {
+      const int lcode = fft_choose_code(side, h);
+      m = NPL - 1;  // the longest length covers every FFT level
+      for (int i = NPL - 1; i >= 0; i--)
+        if (w.fft_codes[i] == lcode) m = i;
+    }
+    hmode[lv] = m;
+  }
+  CK(cudaMemcpyAsync(w.lvl_mode, hmode.data(), sizeof(int) * L, cudaMemcpyHostToDevice, st));
+  if (NPL) CK(cudaMemcpyAsync(w.fft_plans, fplans, sizeof(FftPlan) * NPL, cudaMemcpyHostToDevice, st));
   lc.tb_grid = dim3((side + TB_T - 1) / TB_T, (side + TB_T - 1) / TB_T);
   if (hc.tile_blur_hmax > 0)
     CK(cudaFuncSetAttribute(blur_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -779,9 +817,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     cudaGraph_t obody;
     CK(add_while(&outer_node, g, nullptr, 0, outer_h, &obody));
     CK(cudaGraphConditionalHandleCreate(&tile_h, obody, 0, 0));
-    cudaGraphConditionalHandle blur_h, tblur_h;
+    cudaGraphConditionalHandle blur_h;
     CK(cudaGraphConditionalHandleCreate(&blur_h, obody, 0, 0));
-    CK(cudaGraphConditionalHandleCreate(&tblur_h, obody, 0, 0));
     cudaGraphNode_t nd[8];
     // level set-up in one node: level_begin + pass draw records + row weights
     // (+ FFT spectrum); the sort's grid is square, so the column weights B(x)
@@ -791,94 +828,81 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       const int ndraw = PDRAW_MAX * 16 / 256, nrow = std::max(1, (side + 255) / 256);
       const int nspec = w.fft_L ? std::max(1, w.fft_L / 256) : 0;
       CK(add_kernel(&nd[1], obody, nullptr, 0, level_prep_kernel, dim3(ndraw + nrow + nspec), dim3(256), w.ctrl,
-                    lc.sched, (unsigned long long)blur_h, (unsigned long long)tblur_h, (unsigned long long)tile_h,
-                    w.pdraw, w.prec, w.rowweight, lc.lvl, fplan, ndraw, nrow));
+                    lc.sched, (unsigned long long)blur_h, (unsigned long long)tile_h, w.pdraw, w.prec, w.rowweight,
+                    lc.lvl, (const int*)w.lvl_mode, (const FftPlan*)w.fft_plans, NPL, ndraw, nrow));
     }
     CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight32_kernel, dim3(lc.den_grid), dim3(256),
                   (const double*)w.rowweight, (const double*)w.rowweight, w.den32, side, side, lc.lvl));
-    // IF (FFT tier this level) { spectrum, fft axis 0, fallback 0, fft axis 1, fallback 1 }
-    // ELSE { direct fold axis 0, fallback 0, axis 1, fallback 1 }
+    // SWITCH (blur mode of the level) { FFT at length 0 | ... | FFT at length
+    // NPL - 1 | one tile kernel | direct fold + fallbacks }
     cudaGraphNode_t blur_if;
-    cudaGraph_t bbody[2];
+    cudaGraph_t bbody[FFT_PLANS + 2];
     {
       cudaGraphNodeParams p{};
       p.type = cudaGraphNodeTypeConditional;
       p.conditional.handle = blur_h;
-      p.conditional.type = cudaGraphCondTypeIf;
-      p.conditional.size = 2;
+      p.conditional.type = cudaGraphCondTypeSwitch;
+      p.conditional.size = NPL + 2;
       CK(cudaGraphAddNode(&blur_if, obody, &nd[2], 1, &p));
-      bbody[0] = p.conditional.phGraph_out[0];
-      bbody[1] = p.conditional.phGraph_out[1];
+      for (int i = 0; i < NPL + 2; i++) bbody[i] = p.conditional.phGraph_out[i];
+    }
+    for (int i = 0; i < NPL; i++) {
+      cudaGraphNode_t fn[5];
+      const float* in0 = w.feat;
+      float* out0 = w.tmp;
+      const float* dnull = nullptr;
+      int* fb0 = w.fb0;
+      int* fb1 = w.fb1;
+      int cap = w.fb_cap;
+      PadGeom pg = lc.pg;
+      BlurLevelRef lv = lc.lvl;
+      FftPlan pl = fplans[i];
+      void* a0[] = {&in0, &out0, &pg, &lv, &pl, &dnull, &fb0, &cap, &fb1};
+      cudaKernelNodeParams kp{};
+      kp.func = fft0s[i];
+      kp.gridDim = dim3(fft_grid);
+      kp.blockDim = dim3(fft_nthreads[i]);
+      kp.sharedMemBytes = (unsigned)fft_smems[i];
+      kp.kernelParams = a0;
+      CK(cudaGraphAddKernelNode(&fn[1], bbody[i], nullptr, 0, &kp));
+      CK(add_kernel(&fn[2], bbody[i], &fn[1], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
+                    (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
+      const float* in1 = w.tmp;
+      float* out1 = w.target;
+      const float* den = w.den32;
+      void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &fb1, &cap, &fb0};
+      kp.func = fft1s[i];
+      kp.kernelParams = a1;
+      CK(cudaGraphAddKernelNode(&fn[3], bbody[i], &fn[2], 1, &kp));
+      CK(add_kernel(&fn[4], bbody[i], &fn[3], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
+                    (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
     }
     {
-      cudaGraphNode_t fn[5];  // [0] unused: the spectrum comes from level_prep_kernel
-      {
-        const float* in0 = w.feat;
-        float* out0 = w.tmp;
-        const float* dnull = nullptr;
-        int* fb0 = w.fb0;
-        int* fb1 = w.fb1;
-        int cap = w.fb_cap;
-        PadGeom pg = lc.pg;
-        BlurLevelRef lv = lc.lvl;
-        FftPlan pl = fplan;
-        void* a0[] = {&in0, &out0, &pg, &lv, &pl, &dnull, &fb0, &cap, &fb1};
-        cudaKernelNodeParams kp{};
-        kp.func = fft0;
-        kp.gridDim = dim3(fft_grid);
-        kp.blockDim = dim3(fft_nthreads);
-        kp.sharedMemBytes = (unsigned)fft_smem;
-        kp.kernelParams = a0;
-        CK(cudaGraphAddKernelNode(&fn[1], bbody[0], nullptr, 0, &kp));
-        CK(add_kernel(&fn[2], bbody[0], &fn[1], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
-                      (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
-        const float* in1 = w.tmp;
-        float* out1 = w.target;
-        const float* den = w.den32;
-        void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &fb1, &cap, &fb0};
-        kp.func = fft1;
-        kp.kernelParams = a1;
-        CK(cudaGraphAddKernelNode(&fn[3], bbody[0], &fn[2], 1, &kp));
-        CK(add_kernel(&fn[4], bbody[0], &fn[3], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
-                      (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
-      }
-      // ELSE: IF (h <= tile_blur_hmax) { one tile kernel } ELSE { direct fold + fallbacks }
-      cudaGraphNode_t tb_if;
-      cudaGraph_t tbody[2];
-      {
-        cudaGraphNodeParams p{};
-        p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = tblur_h;
-        p.conditional.type = cudaGraphCondTypeIf;
-        p.conditional.size = 2;
-        CK(cudaGraphAddNode(&tb_if, bbody[1], nullptr, 0, &p));
-        tbody[0] = p.conditional.phGraph_out[0];
-        tbody[1] = p.conditional.phGraph_out[1];
-      }
-      {
-        const float* fin = w.feat;
-        float* tout = w.target;
-        PadGeom pg = lc.pg;
-        BlurLevelRef lv = lc.lvl;
-        const float* den = w.den32;
-        void* ta[] = {&fin, &tout, &pg, &lv, &den};
-        cudaKernelNodeParams kp{};
-        kp.func = (void*)blur_tile_kernel;
-        kp.gridDim = lc.tb_grid;
-        kp.blockDim = dim3(TB_THREADS);
-        kp.sharedMemBytes = (unsigned)tile_blur_smem_bytes(hc.tile_blur_hmax);
-        kp.kernelParams = ta;
-        cudaGraphNode_t tn;
-        CK(cudaGraphAddKernelNode(&tn, tbody[0], nullptr, 0, &kp));
-      }
+      const float* fin = w.feat;
+      float* tout = w.target;
+      PadGeom pg = lc.pg;
+      BlurLevelRef lv = lc.lvl;
+      const float* den = w.den32;
+      void* ta[] = {&fin, &tout, &pg, &lv, &den};
+      cudaKernelNodeParams kp{};
+      kp.func = (void*)blur_tile_kernel;
+      kp.gridDim = lc.tb_grid;
+      kp.blockDim = dim3(TB_THREADS);
+      kp.sharedMemBytes = (unsigned)tile_blur_smem_bytes(std::max(hc.tile_blur_hmax, 1));
+      kp.kernelParams = ta;
+      cudaGraphNode_t tn;
+      CK(cudaGraphAddKernelNode(&tn, bbody[NPL], nullptr, 0, &kp));
+    }
+    {
+      cudaGraph_t db = bbody[NPL + 1];
       cudaGraphNode_t bn[4];
-      CK(add_kernel(&bn[0], tbody[1], nullptr, 0, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
+      CK(add_kernel(&bn[0], db, nullptr, 0, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
-      CK(add_kernel(&bn[1], tbody[1], &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
+      CK(add_kernel(&bn[1], db, &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
-      CK(add_kernel(&bn[2], tbody[1], &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
+      CK(add_kernel(&bn[2], db, &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
-      CK(add_kernel(&bn[3], tbody[1], &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
+      CK(add_kernel(&bn[3], db, &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
     }
     nd[4] = blur_if;
@@ -1008,24 +1032,25 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         level_begin_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, 0ull, 0ull, 0ull);
         if (!parity) pass_draws_kernel<<<PDRAW_MAX * 16 / 256, 256, 0, st>>>(w.ctrl, w.pdraw, w.prec);
       });
-      const bool use_fft = level_uses_fft(sch.hs[lv], side, hc.fft_min_h, hc.fft_L);
+      const int mode = hmode[lv];
+      const bool use_fft = mode < NPL;
       timed(K_BORDER, [&] {
         border_rows_kernel<<<lc.rows_grid, 128, 0, st>>>(w.rowweight, side, lc.lvl);
         border_weight32_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.rowweight, w.den32, side, side, lc.lvl);
       });
       if (use_fft) {
         timed(K_BLUR0, [&] {
-          fft_spectrum_kernel<<<spec_grid, 128, 0, st>>>(lc.lvl, fplan);
+          fft_spectrum_kernel<<<std::max(1, fplans[mode].L / 128), 128, 0, st>>>(lc.lvl, fplans[mode]);
           {
             const float* in0 = w.feat;
             float* out0 = w.tmp;
             const float* dnull = nullptr;
             PadGeom pg = lc.pg;
             BlurLevelRef lv = lc.lvl;
-            FftPlan pl = fplan;
+            FftPlan pl = fplans[mode];
             int cap = w.fb_cap;
             void* a0[] = {&in0, &out0, &pg, &lv, &pl, &dnull, &w.fb0, &cap, &w.fb1};
-            cudaLaunchKernel(fft0, dim3(fft_grid), dim3(fft_nthreads), a0, fft_smem, st);
+            cudaLaunchKernel(fft0s[mode], dim3(fft_grid), dim3(fft_nthreads[mode]), a0, fft_smems[mode], st);
           }
           blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
                                                                      w.fb_cap);
@@ -1037,15 +1062,15 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
             const float* den = w.den32;
             PadGeom pg = lc.pg;
             BlurLevelRef lv = lc.lvl;
-            FftPlan pl = fplan;
+            FftPlan pl = fplans[mode];
             int cap = w.fb_cap;
             void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &w.fb1, &cap, &w.fb0};
-            cudaLaunchKernel(fft1, dim3(fft_grid), dim3(fft_nthreads), a1, fft_smem, st);
+            cudaLaunchKernel(fft1s[mode], dim3(fft_grid), dim3(fft_nthreads[mode]), a1, fft_smems[mode], st);
           }
           blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
                                                                      w.fb_cap);
         });
-      } else if (level_uses_tile_blur(sch.hs[lv], side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax)) {
+      } else if (mode == NPL) {
         timed(K_BLUR0, [&] {
           blur_tile_kernel<<<lc.tb_grid, TB_THREADS, tile_blur_smem_bytes(hc.tile_blur_hmax), st>>>(
               w.feat, w.target, lc.pg, lc.lvl, w.den32);
@@ -1158,8 +1183,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         flush_profile();
         fprintf(stderr, "level %3d h %4d beta %4d %s passes %3d pass %7.1f us blur0 %7.1f blur1 %7.1f border %6.1f "
                 "dist %6.1f ctrl %7.1f us (%d)\n", lv, sch.hs[lv], beta,
-                use_fft ? "fft " : (level_uses_tile_blur(sch.hs[lv], side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax)
-                                        ? "tile" : "dir "),
+                use_fft ? (fplans[mode].L == 1536 ? "f1536" : fplans[mode].L == 1280 ? "f1280" : fplans[mode].L == 1152 ? "f1152" : "fft  ")
+                        : mode == NPL ? "tile " : "dir  ",
                 lvl_n[K_PASS], 1e3 * lvl_ms[K_PASS] / (lvl_n[K_PASS] ? lvl_n[K_PASS] : 1), 1e3 * lvl_ms[K_BLUR0],
                 1e3 * lvl_ms[K_BLUR1], 1e3 * lvl_ms[K_BORDER], 1e3 * lvl_ms[K_DIST], 1e3 * lvl_ms[K_CTRL],
                 lvl_n[K_CTRL]);
