@@ -576,7 +576,8 @@ def run_ours(args):
 
     # kernels launched per sort by our library (plas_b200.cu): 6 init + 5 final;
     # DEVICE (one graph) per level: set-up, border weight, blur (FFT: 2 + 2
-    # fallback kernels for h >= 64; tile: 1 for h <= 4; direct: 2 + 2), level
+    # fallback kernels for h >= 48 (side <= 1024) or 64; tile: 1 for h <= 4 and D <= 16;
+    # direct: 2 + 2), level
     # statistics, and the pass loop in iterations of 3 passes (K3 + statistics
     # each; the slots after the level's last pass launch and return at once).
     # PARITY (host-stepped) per level: begin, 2 border, blur (FFT adds the
@@ -587,7 +588,7 @@ def run_ours(args):
     def blur_launches(h, device):
         if h >= fft_min_h:
             return 4 if device else 5
-        return 1 if h <= 4 else 4
+        return 1 if h <= 4 and D <= 16 else 4  # tile blur only for rows of <= 16 floats
     per_level = []
     for r, tr in rep["radius_trace"]:
         h, p = math.ceil(r), len(tr) - 1

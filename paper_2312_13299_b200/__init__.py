@@ -7,7 +7,7 @@ Importing the package does not touch the GPU; the first GPU call loads
 libplas_b200.so and fails loudly if it is missing.
 """
 
-from .metrics import SortReport, vad
+from .metrics import BENCH_CSV_FIELDS, SortReport, attribute_psnr, bench_rows_to_csv, bench_sort, vad
 from .plas import (PERMUTATIONS, SortConfig, block_size, blur_target, grid_distance,
                    initial_radius, partition_blocks, reassign_block, sort_grid,
                    sort_grid_report, sort_on_device)
@@ -24,4 +24,5 @@ __all__ = [
     "block_size", "blur_target", "build_grid_layout", "normalize_for_sorting", "prune_to_grid",
     "grid_distance", "huber", "huber_grad", "initial_radius", "partition_blocks", "reassign_block",
     "smoothness_loss", "smoothness_loss_autograd", "sort_grid", "sort_grid_report", "sort_on_device", "vad",
+    "BENCH_CSV_FIELDS", "attribute_psnr", "bench_rows_to_csv", "bench_sort",
 ]

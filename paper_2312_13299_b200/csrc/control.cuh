@@ -391,6 +391,71 @@ __device__ __forceinline__ bool last_cta_reduce(double v, double* partials, int*
   return true;
 }
 
+// Deterministic pass statistic: the moved-cell list comes in atomic
+// reservation order, so an fp64 sum over it would depend on the schedule.
+// Each cell's change (new - cached distance, computed the same way in every
+// schedule) is rounded to a multiple of 2^-64 (fx64) and the changes are
+// summed as 128-bit integers -- exact, so any order gives the same total.
+__device__ __forceinline__ __int128 fx64(double v) {
+  const double t = rint(v * 18446744073709551616.0);  // v 2^64 (exact scaling), rounded to an integer
+  const double hi = trunc(t * 9.094947017729282379150390625e-13);  // t 2^-40: |hi| < 2^63 for |v| < 2^87
+  const double lo = fma(hi, -1099511627776.0, t);                  // t - hi 2^40, exact: |lo| < 2^40
+  return ((__int128)(long long)hi << 40) + (__int128)(long long)lo;
+}
+__device__ __forceinline__ double fx64_to_double(__int128 q) {
+  const long long hi = (long long)(q >> 64);
+  const unsigned long long lo = (unsigned long long)q;
+  return (double)hi + (double)lo * 5.42101086242752217003726400434970855712890625e-20;  // lo 2^-64
+}
+__device__ __forceinline__ __int128 shfl_xor_i128(__int128 v, int m) {
+  const long long h = __shfl_xor_sync(0xffffffffu, (long long)(v >> 64), m);
+  const unsigned long long l = __shfl_xor_sync(0xffffffffu, (unsigned long long)v, m);
+  return ((__int128)h << 64) | (__int128)l;
+}
+
+// last_cta_reduce for 128-bit fixed-point values (two 8-byte partial slots per CTA)
+__device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, double* partials, int* done, double* total,
+                                                   int* ticket) {
+  __shared__ __int128 sq[32];
+  __shared__ int s_last, s_ticket;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) sq[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __int128 b = 0;
+    for (int w = 0; w < nw; w++) b += sq[w];
+    long long* pp = reinterpret_cast<long long*>(partials);
+    pp[2 * blockIdx.x] = (long long)(b >> 64);
+    pp[2 * blockIdx.x + 1] = (long long)(unsigned long long)b;
+    __threadfence();
+    s_ticket = atomicAdd(done, 1);
+    s_last = s_ticket == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  *ticket = s_ticket;
+  if (!s_last) return false;
+  __threadfence();
+  __int128 t = 0;
+  const volatile long long* pp = reinterpret_cast<const volatile long long*>(partials);
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    t += ((__int128)pp[2 * i] << 64) | (__int128)(unsigned long long)pp[2 * i + 1];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += shfl_xor_i128(t, o);
+  __syncthreads();
+  if (lane == 0) sq[wid] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __int128 b = 0;
+    for (int w = 0; w < nw; w++) b += sq[w];
+    *total = fx64_to_double(b);
+    *done = 0;
+  }
+  __syncthreads();
+  return true;
+}
+
 // level_end_kernel's bookkeeping, done in graph mode by the statistics kernel
 // that ends the level (outer != 0), which saves a node per level
 __device__ __forceinline__ void level_end_work(Ctrl* c, Sched s, unsigned long long outer) {
@@ -497,16 +562,58 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
     double* partials, int* done, long long n, unsigned long long inner, unsigned long long outer,
     double* xpart, int* tab, long long tab_stride) {
-  __shared__ double sh[32];
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
   if (c->level_done) return;  // an unrolled pass slot after the level ended (no CTA takes a ticket)
   gtrace_mark(c, 2);
   const int count = counters[2];
-  double sum = 0.0;
+  __int128 sum = 0;  // fixed point (fx64): order-free
   const int stride = gridDim.x * blockDim.x;
+  if (S > 16) {
+    // wide rows: a quad of lanes per cell, lane s extends cell_dist2's chain
+    // p[s] over chunks s, s + 4, ... (coalesced 64-byte row pieces); the
+    // xor-1-then-xor-2 reduction forms (p0 + p1) + (p2 + p3): the same value
+    // (warp-uniform trip count: 8 cells per warp per step, all lanes shuffle)
+    const int s4 = threadIdx.x & 3, nch = S >> 2, qw = (threadIdx.x & 31) >> 2;
+    for (int eb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 8; eb < count; eb += (stride >> 5) * 8) {
+      const int e = eb + qw;
+      const bool ok = e < count;
+      const long long cell = ok ? list[e] : 0;
+      const double old = ok && s4 == 0 ? dcache[cell] : 0.0;
+      const float4* xa = reinterpret_cast<const float4*>(feat + cell * S);
+      const float4* ya = reinterpret_cast<const float4*>(target + cell * S);
+      double acc = 0.0;
+      for (int c0 = s4; c0 < nch; c0 += 16) {
+        float4 x[4], y[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int c = c0 + 4 * r;
+          x[r] = ok && c < nch ? __ldg(xa + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          y[r] = ok && c < nch ? __ldg(ya + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int c = c0 + 4 * r;
+          const float xs[4] = {x[r].x, x[r].y, x[r].z, x[r].w}, ys[4] = {y[r].x, y[r].y, y[r].z, y[r].w};
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (4 * c + q < D) {
+              const double df = (double)xs[q] - (double)ys[q];
+              acc = fma(df, df, acc);
+            }
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (ok && s4 == 0) {
+        const double d = sqrt(acc);
+        sum += fx64(d - old);
+        dcache[cell] = d;
+      }
+    }
+  }
   // two independent cells per thread in flight, every row load issued first
-  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < count; e0 += 2 * stride) {
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; S <= 16 && e0 < count; e0 += 2 * stride) {
     long long cell[2];
     double old[2];
 #pragma unroll
@@ -541,7 +648,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
           p[c] = acc;
         }
         const double d = sqrt((p[0] + p[1]) + (p[2] + p[3]));
-        sum += d - old[u];
+        sum += fx64(d - old[u]);
         dcache[cell[u]] = d;
       }
     } else {
@@ -549,7 +656,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
       for (int u = 0; u < 2; u++) {
         if (cell[u] >= 0) {
           const double d = sqrt(cell_dist2_any(feat + cell[u] * S, target + cell[u] * S, D, S));
-          sum += d - old[u];
+          sum += fx64(d - old[u]);
           dcache[cell[u]] = d;
         }
       }
@@ -561,7 +668,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   // the controller's writes to Ctrl leave the fields read here unchanged)
   const bool gen = tab && c->rng_mode == 1;
   int ticket = 0;
-  if (!last_cta_reduce(sum, partials, done, &s_tot, sh, &ticket)) {
+  if (!last_cta_reduce_fx(sum, partials, done, &s_tot, &ticket)) {
     if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
     if (c->gtrace) {
       __syncthreads();

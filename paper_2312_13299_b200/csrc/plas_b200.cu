@@ -277,14 +277,19 @@ int fft_min_h(int L) {
   return L <= 2048 ? 48 : 64;
 }
 
-// largest half-width of the one-kernel tile blur (0 = off); PLAS_TILE_BLUR_HMAX overrides
-int tile_blur_hmax() {
-  static int v = -1;
-  if (v < 0) {
+// largest half-width of the one-kernel tile blur (0 = off); PLAS_TILE_BLUR_HMAX
+// overrides.  Measured: 4 is best at C2 (the tile kernel is latency-bound
+// above); for rows wider than 16 floats the direct fold wins at every h (C3:
+// 1.69 s without the tile tier, 1.75 s with h <= 2, 1.80 s with h <= 4 -- the
+// tile kernel reads each row once per channel pair, ~10x its algorithmic bytes)
+int tile_blur_hmax(int S) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("PLAS_TILE_BLUR_HMAX");
-    v = e ? std::min(std::max(atoi(e), 0), TB_HMAX) : 4;  // measured best at C2 (tile kernel is latency-bound above)
+    v = e ? std::min(std::max(atoi(e), 0), TB_HMAX) : -1;
   }
-  return v;
+  if (v >= 0) return v;
+  return S <= 16 ? 4 : 0;
 }
 
 // relative error constant of the FFT convolution (blur_fft.cuh), x2 safety
@@ -362,7 +367,7 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->pdraw = c.take<int4>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX);
   w->prec = c.take<int>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX * PREC_INTS);
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
-  w->spart = c.take<double>(MAX_PARTS);
+  w->spart = c.take<double>(2 * MAX_PARTS);  // pass statistics: one 128-bit fixed-point partial per CTA
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
   fft_plan_codes(side, &w->fft_count, w->fft_codes);
   w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
@@ -666,7 +671,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   }
   hc.fft_min_h = fft_min_h(w.fft_L);
   hc.fft_L = w.fft_L;
-  hc.tile_blur_hmax = tile_blur_hmax();
+  hc.tile_blur_hmax = tile_blur_hmax(S);
   hc.rank = world > 1 ? a->rank : 0;
   hc.world = world;
   hc.pdraw = nullptr;

@@ -8,7 +8,7 @@ small fixtures under tests/golden/ that the CPU oracle tests and the GPU parity
 tests compare against.
 
 Usage:  python tests/golden/make_golden.py PART [PART ...]
-PART in: versions rng blur assign metrics smooth sort_small c0 c1 c2 paired_null_c0 paired_null_c1
+PART in: versions rng blur assign metrics bench smooth sort_small c0 c1 c2 paired_null_c0 paired_null_c1
 """
 
 import hashlib
@@ -183,6 +183,24 @@ def part_metrics():
         arrays[f"gd_out{i}"] = np.array(ref_plas.grid_distance(a, b))
         arrays[f"gd_outw{i}"] = np.array(ref_plas.grid_distance(a, b, weights=w))
     np.savez_compressed(out("metrics.npz"), **arrays)
+
+
+def part_bench():
+    """metrics.bench_sort rows (minus the wall time), its CSV, and attribute_psnr cases."""
+    rows = ref_metrics.bench_sort([2, 8, 16], channels=3, seeds=(0, 1))
+    rows += ref_metrics.bench_sort([12], channels=5, seeds=(7,))
+    keep = [{k: v for k, v in r.items() if k != "time_s"} for r in rows]
+    fixed = [dict(r, time_s=0.125) for r in rows]
+    rng = np.random.default_rng(5)
+    psnr = []
+    for shape, peak in [((16, 16), 255.0), ((7, 9, 3), 1.0), ((33,), 2.5)]:
+        a = rng.uniform(0, peak, shape)
+        b = np.clip(a + rng.normal(0, 0.01 * peak, shape), 0, peak)
+        psnr.append({"a": a.ravel().tolist(), "b": b.ravel().tolist(), "shape": list(shape), "peak": peak,
+                     "psnr": ref_metrics.attribute_psnr(a, b, peak)})
+    with open(out("bench.json"), "w") as f:
+        json.dump({"rows": keep, "csv_rows": fixed, "csv": ref_metrics.bench_rows_to_csv(fixed),
+                   "fields": list(ref_metrics.BENCH_CSV_FIELDS), "psnr": psnr}, f)
 
 
 def part_smooth():
