@@ -583,7 +583,9 @@ def run_ours(args):
     # PARITY (host-stepped) per level: begin, 2 border, blur (FFT adds the
     # spectrum kernel), level statistics, level end; per pass: set-pass, class
     # select, K3, statistics.
-    fft_min_h = 48 if side <= 1024 else 64  # plas_b200.cu fft_min_h: L <= 2048 (side 1024 -> L 1536) or longer
+    # plas_b200.cu fft_min_h: 40 for rows wider than 16 floats, else 48 when the
+    # longest FFT length is <= 2048 (side 1024 -> 1536), 64 above
+    fft_min_h = 40 if D > 16 else (48 if side <= 1024 else 64)
 
     def blur_launches(h, device):
         if h >= fft_min_h:

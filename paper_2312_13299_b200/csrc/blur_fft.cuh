@@ -143,7 +143,12 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 #ifndef FFT_MINB
 #define FFT_MINB 4
 #endif
-template <int L> __host__ __device__ constexpr int fft_min_blocks() { return L > 4096 ? 1 : (FFT_MINB * 256) / fft_threads_for<L>(); }
+#ifndef FFT_MINB_3072
+#define FFT_MINB_3072 3
+#endif
+template <int L> __host__ __device__ constexpr int fft_min_blocks() {
+  return L > 4096 ? 1 : (L == 3072 ? FFT_MINB_3072 : (FFT_MINB * 256) / fft_threads_for<L>());
+}
 
 // FFT length code lc = p2 + 32 m: L = M 2^p2 with M = 1, 3, 5, 9 for m = 0..3
 // (the odd factors cut the padded length: at side 1024 a level with h <= 128

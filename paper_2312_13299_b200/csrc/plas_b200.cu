@@ -245,15 +245,15 @@ int fft_alloc_code(int side) {
   const long long h0 = (long long)ceil(std::max(side / 2.0 - 1.0, 2.0));
   return fft_choose_code(side, h0);
 }
-int fft_min_h(int L);
+int fft_min_h(int L, int S);
 // the lengths a sort at this side can use: the shortest fitting length of every
 // half-width from the crossover up to the top level's (sorted by length)
-void fft_plan_codes(int side, int* count, int* codes) {
+void fft_plan_codes(int side, int S, int* count, int* codes) {
   *count = 0;
   const int top = fft_alloc_code(side);
   if (top < 0) return;
   const long long h0 = (long long)ceil(std::max(side / 2.0 - 1.0, 2.0));
-  const int hmin = std::max(fft_min_h(fft_len(top)), 1);
+  const int hmin = std::max(fft_min_h(fft_len(top), S), 1);
   for (long long h = hmin; h <= h0; h++) {
     const int lc = fft_choose_code(side, h);
     if (lc < 0) continue;
@@ -267,13 +267,14 @@ void fft_plan_codes(int side, int* count, int* codes) {
 // smallest half-width that takes the FFT tier for length L (0 = never);
 // PLAS_FFT_MIN_H overrides.  Measured crossovers: 48 at C2 (L = 1536: 114.7 vs
 // 115.5 ms at 64), 64 at C4 (L = 6144: 2.625 vs 2.641 s at 48).
-int fft_min_h(int L) {
+int fft_min_h(int L, int S) {
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("PLAS_FFT_MIN_H");
     v = e ? std::max(atoi(e), 0) : -1;
   }
   if (v >= 0) return v;
+  if (S > 16) return 40;  // C3 (59 channels): 1.661 s at 40 vs 1.672 s at 64
   return L <= 2048 ? 48 : 64;
 }
 
@@ -369,7 +370,7 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(2 * MAX_PARTS);  // pass statistics: one 128-bit fixed-point partial per CTA
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
-  fft_plan_codes(side, &w->fft_count, w->fft_codes);
+  fft_plan_codes(side, row_stride(dim), &w->fft_count, w->fft_codes);
   w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
   for (int i = 0; i < 4; i++)
     w->fft_tws[i] = i < w->fft_count ? c.take<double2>((size_t)fft_twiddle_len(w->fft_codes[i])) : nullptr;
@@ -669,7 +670,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaGetLastError();
     }
   }
-  hc.fft_min_h = fft_min_h(w.fft_L);
+  hc.fft_min_h = fft_min_h(w.fft_L, S);
   hc.fft_L = w.fft_L;
   hc.tile_blur_hmax = tile_blur_hmax(S);
   hc.rank = world > 1 ? a->rank : 0;
@@ -1186,10 +1187,14 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       if (level_trace) {
         CK(cudaStreamSynchronize(st));
         flush_profile();
-        fprintf(stderr, "level %3d h %4d beta %4d %s passes %3d pass %7.1f us blur0 %7.1f blur1 %7.1f border %6.1f "
+        char lab[16];
+        if (use_fft)
+          snprintf(lab, sizeof(lab), "f%d", fplans[mode].L);
+        else
+          snprintf(lab, sizeof(lab), "%s", mode == NPL ? "tile" : "dir");
+        fprintf(stderr, "level %3d h %4d beta %4d %-5s passes %3d pass %7.1f us blur0 %7.1f blur1 %7.1f border %6.1f "
                 "dist %6.1f ctrl %7.1f us (%d)\n", lv, sch.hs[lv], beta,
-                use_fft ? (fplans[mode].L == 1536 ? "f1536" : fplans[mode].L == 1280 ? "f1280" : fplans[mode].L == 1152 ? "f1152" : "fft  ")
-                        : mode == NPL ? "tile " : "dir  ",
+                lab,
                 lvl_n[K_PASS], 1e3 * lvl_ms[K_PASS] / (lvl_n[K_PASS] ? lvl_n[K_PASS] : 1), 1e3 * lvl_ms[K_BLUR0],
                 1e3 * lvl_ms[K_BLUR1], 1e3 * lvl_ms[K_BORDER], 1e3 * lvl_ms[K_DIST], 1e3 * lvl_ms[K_CTRL],
                 lvl_n[K_CTRL]);
