@@ -146,6 +146,9 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 #ifndef FFT_MINB_3072
 #define FFT_MINB_3072 3
 #endif
+// (L > 4096: one CTA per SM; two with 64 registers spill 150-200 bytes and
+// C4 went from 2.61 to 2.75 s.  L = 3072: three CTAs at 56 registers beat two
+// at 72 -- C3 1.692 -> 1.672 s.)
 template <int L> __host__ __device__ constexpr int fft_min_blocks() {
   return L > 4096 ? 1 : (L == 3072 ? FFT_MINB_3072 : (FFT_MINB * 256) / fft_threads_for<L>());
 }
