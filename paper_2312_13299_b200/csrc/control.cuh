@@ -413,8 +413,11 @@ __device__ __forceinline__ __int128 shfl_xor_i128(__int128 v, int m) {
   return ((__int128)h << 64) | (__int128)l;
 }
 
-// last_cta_reduce for 128-bit fixed-point values (two 8-byte partial slots per CTA)
-__device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, double* partials, int* done, double* total,
+// last_cta_reduce for 128-bit fixed-point values: each CTA adds its block sum
+// into a 128-bit accumulator acc[0..1] (low word, then high word plus the
+// carry its own low-word add produced -- exact modulo 2^128 in any order); the
+// last CTA reads it and clears it for the next pass (zeroed at sort start).
+__device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, unsigned long long* acc, int* done, double* total,
                                                    int* ticket) {
   __shared__ __int128 sq[32];
   __shared__ int s_last, s_ticket;
@@ -426,9 +429,10 @@ __device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, double* partials,
   if (threadIdx.x == 0) {
     __int128 b = 0;
     for (int w = 0; w < nw; w++) b += sq[w];
-    long long* pp = reinterpret_cast<long long*>(partials);
-    pp[2 * blockIdx.x] = (long long)(b >> 64);
-    pp[2 * blockIdx.x + 1] = (long long)(unsigned long long)b;
+    const unsigned long long lo = (unsigned long long)b;
+    const unsigned long long old = atomicAdd(acc, lo);
+    const unsigned long long carry = old + lo < old ? 1ull : 0ull;
+    atomicAdd(acc + 1, (unsigned long long)(b >> 64) + carry);
     __threadfence();
     s_ticket = atomicAdd(done, 1);
     s_last = s_ticket == (int)gridDim.x - 1;
@@ -436,20 +440,13 @@ __device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, double* partials,
   __syncthreads();
   *ticket = s_ticket;
   if (!s_last) return false;
-  __threadfence();
-  __int128 t = 0;
-  const volatile long long* pp = reinterpret_cast<const volatile long long*>(partials);
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
-    t += ((__int128)pp[2 * i] << 64) | (__int128)(unsigned long long)pp[2 * i + 1];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += shfl_xor_i128(t, o);
-  __syncthreads();
-  if (lane == 0) sq[wid] = t;
-  __syncthreads();
   if (threadIdx.x == 0) {
-    __int128 b = 0;
-    for (int w = 0; w < nw; w++) b += sq[w];
-    *total = fx64_to_double(b);
+    __threadfence();
+    volatile unsigned long long* va = acc;
+    const unsigned long long lo = va[0], hi = va[1];
+    va[0] = 0ull;
+    va[1] = 0ull;
+    *total = fx64_to_double((__int128)(((unsigned __int128)hi << 64) | (unsigned __int128)lo));
     *done = 0;
   }
   __syncthreads();
@@ -557,6 +554,7 @@ __device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, lo
 // Sharded (world > 1): the last CTA only publishes this rank's partial
 // (change, moved count) to xpart; shard_control_kernel runs the controller
 // once every rank's partial has been exchanged.
+template <bool WROWS>  // rows wider than 16 floats (a quad of lanes per cell)
 __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
     double* __restrict__ dcache, int D, int S, const int* __restrict__ list, int* counters,
@@ -569,7 +567,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   const int count = counters[2];
   __int128 sum = 0;  // fixed point (fx64): order-free
   const int stride = gridDim.x * blockDim.x;
-  if (S > 16) {
+  if (WROWS) {
     // wide rows: a quad of lanes per cell, lane s extends cell_dist2's chain
     // p[s] over chunks s, s + 4, ... (coalesced 64-byte row pieces); the
     // xor-1-then-xor-2 reduction forms (p0 + p1) + (p2 + p3): the same value
@@ -613,7 +611,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     }
   }
   // two independent cells per thread in flight, every row load issued first
-  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; S <= 16 && e0 < count; e0 += 2 * stride) {
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; !WROWS && e0 < count; e0 += 2 * stride) {
     long long cell[2];
     double old[2];
 #pragma unroll
@@ -668,7 +666,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   // the controller's writes to Ctrl leave the fields read here unchanged)
   const bool gen = tab && c->rng_mode == 1;
   int ticket = 0;
-  if (!last_cta_reduce_fx(sum, partials, done, &s_tot, &ticket)) {
+  if (!last_cta_reduce_fx(sum, reinterpret_cast<unsigned long long*>(partials), done, &s_tot, &ticket)) {
     if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
     if (c->gtrace) {
       __syncthreads();

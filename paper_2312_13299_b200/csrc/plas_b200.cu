@@ -368,7 +368,7 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->pdraw = c.take<int4>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX);
   w->prec = c.take<int>(rng_mode == PLAS_RNG_PARITY ? 1 : (size_t)PDRAW_MAX * PREC_INTS);
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
-  w->spart = c.take<double>(2 * MAX_PARTS);  // pass statistics: one 128-bit fixed-point partial per CTA
+  w->spart = c.take<double>(MAX_PARTS + 2);  // [MAX_PARTS, +2): the pass statistic's 128-bit accumulator
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
   fft_plan_codes(side, row_stride(dim), &w->fft_count, w->fft_codes);
   w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
@@ -680,6 +680,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.pdraw_level = -1;
   CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
+  CK(cudaMemsetAsync(w.spart + MAX_PARTS, 0, 2 * sizeof(double), st));  // pass statistic's 128-bit accumulator
   // zero halos of the padded blur buffers, pad channels, fallback counters
   CK(cudaMemsetAsync(w.feat_alloc, 0, sizeof(float) * w.feat_alloc_floats, st));
   CK(cudaMemsetAsync(w.tmp_alloc, 0, sizeof(float) * w.tmp_alloc_floats, st));
@@ -965,9 +966,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaGraphNode_t prev = nullptr;
       for (int u = 0; u < pass_unroll(); u++) {
         CK(cudaGraphAddKernelNode(&kn, lb, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
-        CK(add_kernel(&sn, lb, &kn, 1, pass_stats_kernel, dim3(sgrid), dim3(RED_THREADS), w.ctrl, lc.sched,
+        CK(add_kernel(&sn, lb, &kn, 1, S > 16 ? pass_stats_kernel<true> : pass_stats_kernel<false>, dim3(sgrid), dim3(RED_THREADS), w.ctrl, lc.sched,
                       (const float*)w.feat, (const float*)w.target, w.dcache, D, S, (const int*)w.list,
-                      counters, w.spart, done, n, (unsigned long long)loop_h, (unsigned long long)outer_h,
+                      counters, w.spart + MAX_PARTS, done, n, (unsigned long long)loop_h, (unsigned long long)outer_h,
                       (double*)nullptr, w.sel, w.sel_stride));  // + next pass's tables (+ level end)
         prev = sn;
       }
@@ -1138,8 +1139,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           }
         }
         timed(K_CTRL, [&] {
-          pass_stats_kernel<<<sgrid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, D, S,
-                                                           w.list, counters, w.spart, done, n, 0, 0, a->xchg_part,
+          (S > 16 ? pass_stats_kernel<true> : pass_stats_kernel<false>)<<<sgrid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, D, S,
+                                                           w.list, counters, w.spart + MAX_PARTS, done, n, 0, 0, a->xchg_part,
                                                            parity || world > 1 ? nullptr : w.sel, w.sel_stride);
           if (!parity && world > 1) gen_tables_kernel<<<num_sms(), 256, 0, st>>>(w.ctrl, w.sel, w.sel_stride);
         });
