@@ -550,7 +550,10 @@ int stats_grid_size() {
   static int g = 0;
   if (!g) {
     const char* e = getenv("PLAS_STATS_CTAS_PER_SM");
-    const int per = e ? std::max(1, atoi(e)) : 4;
+    // measured (C2 / C3 / C4): 1 -> 116.1 ms; 2 -> 115.1 ms / 1.655 s / 2.608 s;
+    // 4 -> 115.8 ms / 1.661 s / 2.612 s; 8 -> 120.3 ms (fewer tickets and
+    // table workers shorten the kernel's tail)
+    const int per = e ? std::max(1, atoi(e)) : 2;
     g = std::min(num_sms() * per, MAX_PARTS);
   }
   return g;
