@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libplas_b200.so")
+LIB_PATH = os.environ.get("PLAS_LIB_PATH") or os.path.join(HERE, "libplas_b200.so")  # PLAS_LIB_PATH: A/B builds
 
 PLAS_OK = 0
 PLAS_ERR_INVALID = -1
