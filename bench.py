@@ -291,11 +291,16 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(prefixes=("pass_kernel", "tile_pass_kernel")):
-    """DRAM bytes (read + write) per K3 launch from the committed ncu launch list
-    (profiles/ncu_summary.json, tools/launch_summary.py), launch-weighted over the
-    gather and tile variants; None if absent."""
-    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+NCU_LISTS = {"C2": "ncu_summary.json", "C3": "r01_launches_c3.json"}  # committed launch lists per workload
+
+
+def ncu_traffic(config, prefixes=("pass_kernel", "tile_pass_kernel")):
+    """DRAM bytes (read + write) per K3 launch from the committed ncu launch list of
+    this workload (profiles/, tools/launch_summary.py), launch-weighted over the
+    gather and tile variants; None if that workload has no list."""
+    if config not in NCU_LISTS:
+        return None
+    path = os.path.join(REPO, "profiles", NCU_LISTS[config])
     try:
         with open(path) as f:
             ks = json.load(f)["kernels"]
@@ -551,7 +556,7 @@ def run_ours(args):
         achieved = alg_pass / avg_pass_s / 1e9
         roofline = {"bound": "hbm", "kernel": "pass_kernel (K3 fused assign+swap+distance)",
                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(),
+                    "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
                     "algorithmic_bytes_per_launch": alg_pass, "avg_launch_us": round(avg_pass_s * 1e6, 2),
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                     "dominant_by_time": dominant,
