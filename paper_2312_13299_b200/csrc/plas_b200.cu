@@ -19,6 +19,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <utility>
@@ -492,6 +494,41 @@ int pass_grid_size(int S) {
   return cached[which];
 }
 
+// Instantiated sort graphs by workspace layout (a few entries; the oldest is
+// destroyed when a new shape arrives).
+struct GraphKey {
+  const void* ws;
+  size_t ws_bytes;
+  long long n;
+  int D, L;
+  long long wlen, tcap;
+  int mode, device;
+  bool operator==(const GraphKey& o) const {
+    return ws == o.ws && ws_bytes == o.ws_bytes && n == o.n && D == o.D && L == o.L && wlen == o.wlen &&
+           tcap == o.tcap && mode == o.mode && device == o.device;
+  }
+};
+std::mutex g_graph_mu;
+std::vector<std::pair<GraphKey, cudaGraphExec_t>> g_graphs;
+int cudaGetDevice_or(int dflt) {
+  int d = dflt;
+  return cudaGetDevice(&d) == cudaSuccess ? d : dflt;
+}
+cudaGraphExec_t graph_cache_get(const GraphKey& k) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto& e : g_graphs)
+    if (e.first == k) return e.second;
+  return nullptr;
+}
+void graph_cache_put(const GraphKey& k, cudaGraphExec_t ge) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  if (g_graphs.size() >= 4) {
+    cudaGraphExecDestroy(g_graphs.front().second);
+    g_graphs.erase(g_graphs.begin());
+  }
+  g_graphs.push_back({k, ge});
+}
+
 // passes per iteration of the graph's pass loop (PLAS_PASS_UNROLL, default 3: measured 1 -> 122.1, 2 -> 120.2, 3 -> 119.6, 4 -> 120.0 ms at C2)
 int pass_unroll() {
   static int v = 0;
@@ -610,6 +647,9 @@ int plas_host_permutation(uint64_t seed, int64_t n, int64_t* out) {
 }
 
 int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t ws_bytes) {
+  const auto ht0 = std::chrono::steady_clock::now();
+  auto hms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ht0).count(); };
+  const bool htrace = getenv("PLAS_HOST_TRACE") && atoi(getenv("PLAS_HOST_TRACE"));
   if (!a || !res || !a->features || !res->perm) return fail(PLAS_ERR_INVALID, "null argument");
   const long long n = a->n;
   const int D = a->dim;
@@ -719,6 +759,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
   CK(cudaEventRecord(ev0, st));
+  if (htrace) fprintf(stderr, "host: ev0 at %.3f ms\n", hms());
   const int gi = grid_for(n * S, 256, 8);
   if (a->features_dtype == PLAS_F32)
     gather_init_kernel<float><<<gi, 256, 0, st>>>((const float*)a->features, w.idx, w.feat, n, D, S,
@@ -814,11 +855,18 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   int* counters = w.flags + 2;  // [0] moved cells, [1] exact decisions, [2] moved-list length
   MoveOut ml{w.list, counters + 2};
   int* done = w.flags + 6;      // last-CTA ticket of the statistic kernels
+  if (htrace) fprintf(stderr, "host: graph/loop start at %.3f ms\n", hms());
   if (mode == PLAS_RNG_DEVICE && !a->profile && world == 1) {
     // ------------------------------------------------------------ graph
     // outer WHILE (levels): level_begin, border weight, blur axis 0, blur axis 1,
     //   level statistics, inner WHILE (passes): IF(tile){tile}ELSE{gather},
     //   pass statistics (+controller); level_end.
+    // the graph is a function of the workspace layout (every node argument is
+    // a workspace pointer or a shape constant), so an instantiated graph is
+    // reused by later sorts of the same shape on the same workspace
+    const GraphKey gkey{wsp, ws_bytes, n, D, L, (long long)sch.weights.size(), tcap, mode, cudaGetDevice_or(-1)};
+    cudaGraphExec_t ge = graph_cache_get(gkey);
+    if (!ge) {
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle outer_h, tile_h;
@@ -976,12 +1024,15 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         prev = sn;
       }
     }
-    cudaGraphExec_t ge;
+    if (htrace) fprintf(stderr, "host: graph built at %.3f ms\n", hms());
     CK(cudaGraphInstantiate(&ge, g, 0));
-    CK(cudaGraphLaunch(ge, st));
-    CK(cudaStreamSynchronize(st));
-    cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
+    graph_cache_put(gkey, ge);
+    if (htrace) fprintf(stderr, "host: instantiated at %.3f ms\n", hms());
+    }
+    CK(cudaGraphLaunch(ge, st));
+    if (htrace) fprintf(stderr, "host: launched at %.3f ms\n", hms());
+    CK(cudaStreamSynchronize(st));
   } else {
     // ------------------------------------------------------------ host-stepped loop
     // PARITY (host draws) or DEVICE with profiling (device draws, events per launch)

@@ -21,6 +21,7 @@ Two RNG modes (``SortConfig.rng_mode``):
 
 import ctypes
 import itertools
+import functools
 import math
 import time
 from dataclasses import dataclass, field
@@ -190,6 +191,13 @@ def _validate(features):
     return t, n, side
 
 
+@functools.lru_cache(maxsize=64)
+def _schedule(side, radius_decay, min_block_size, start):
+    """Schedules are pure functions of these four values (read-only after
+    construction), so repeated sorts of one shape reuse the host tables."""
+    return Schedule(side, radius_decay, min_block_size, start)
+
+
 class SortPlan:
     """Host-side state of one sort shape: schedule, workspace and the C-ABI call."""
 
@@ -199,7 +207,7 @@ class SortPlan:
         self.side = math.isqrt(n)
         self.config = config
         self.mode = RNG_MODES[config.rng_mode]
-        self.schedule = Schedule(self.side, config.radius_decay, config.min_block_size,
+        self.schedule = _schedule(self.side, config.radius_decay, config.min_block_size,
                                  config.initial_radius)
         self.trace_capacity = max(64 * max(self.schedule.num_levels, 1), 4096)
 
