@@ -492,3 +492,29 @@ def test_device_graph_matches_stepped(side, dim):
     assert [len(t) for _, t in r0["radius_trace"]] == [len(t) for _, t in r1["radius_trace"]]
     np.testing.assert_array_equal(np.concatenate([t for _, t in r0["radius_trace"]]),
                                   np.concatenate([t for _, t in r1["radius_trace"]]))
+
+
+@pytest.mark.gpu
+def test_device_graph_cache_reuse_and_eviction():
+    """Instantiated DEVICE graphs are cached per workspace layout: a cached graph
+    run on new data of the same shape, and shapes evicted from the cache and
+    rebuilt, give the host-stepped (uncached) result."""
+    import torch
+    from paper_2312_13299_b200 import _lib
+    from paper_2312_13299_b200.plas import SortPlan
+    cfg = plas.SortConfig(rng_seed=5, rng_mode="device")
+
+    def run(f, stepped):
+        perm = torch.empty(f.shape[0], dtype=torch.int64, device="cuda")
+        rep = SortPlan(f.shape[0], f.shape[1], cfg).run(f, perm, None, _lib.SortProfile() if stepped else None)
+        return perm.cpu().numpy(), rep["reorders"]
+
+    g = np.random.default_rng(11)
+    shapes = [(64, 3), (48, 5), (80, 2), (96, 4), (32, 7), (64, 3)]  # 5 layouts: the first is evicted, then rebuilt
+    for side, dim in shapes:
+        for _ in range(2):  # second pass on the same layout: a cache hit on new data
+            f = torch.from_numpy(g.uniform(size=(side * side, dim)).astype(np.float32)).cuda()
+            p_graph, r_graph = run(f, False)
+            p_step, r_step = run(f, True)
+            np.testing.assert_array_equal(p_graph, p_step)
+            assert r_graph == r_step
