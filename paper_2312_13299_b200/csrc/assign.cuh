@@ -382,6 +382,9 @@ struct MoveOut {
 };
 
 constexpr int WARP_LIST = 512;  // shared staging entries per warp
+#ifndef K3_MINB
+#define K3_MINB 4
+#endif
 
 // Append this lane's moved cell (if mv) to its warp's staging segment; the
 // warp-uniform fill level lives in *wcnt (a register in every lane).  A full
@@ -443,7 +446,7 @@ __device__ __forceinline__ void load_pass_shared(PassShared& ps, const Ctrl* __r
 //   sel[cls][...] (plas.py:209, built by class_select_kernel).
 // DEVICE: the class grouping is a keyed bijection on [0, m) (Ctrl.fe_*).
 template <bool WIDE, bool PARITY>
-__global__ void __launch_bounds__(256, WIDE ? 2 : 4) pass_kernel(float* __restrict__ feat, int* __restrict__ idx,
+__global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __restrict__ feat, int* __restrict__ idx,
                                                        const float* __restrict__ target, int D, int S,
                                                        const Ctrl* __restrict__ ctrl,
                                                        const int* __restrict__ sel, long long sel_stride,
