@@ -148,9 +148,15 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 #endif
 // (L > 4096: one CTA per SM; two with 64 registers spill 150-200 bytes and
 // C4 went from 2.61 to 2.75 s.  L = 3072: three CTAs at 56 registers beat two
-// at 72 -- C3 1.692 -> 1.672 s.)
+// at 72 -- C3 1.692 -> 1.672 s; four CTAs at 2560 and 3072 (48 / 40
+// registers, 160-280 bytes of spills): C3 1.80 s vs 1.65 s.)
+#ifndef FFT_MINB_2560
+#define FFT_MINB_2560 3
+#endif
 template <int L> __host__ __device__ constexpr int fft_min_blocks() {
-  return L > 4096 ? 1 : (L == 3072 ? FFT_MINB_3072 : (FFT_MINB * 256) / fft_threads_for<L>());
+  return L > 4096 ? 1
+                  : (L == 3072 ? FFT_MINB_3072
+                               : (L == 2560 ? FFT_MINB_2560 : (FFT_MINB * 256) / fft_threads_for<L>()));
 }
 
 // FFT length code lc = p2 + 32 m: L = M 2^p2 with M = 1, 3, 5, 9 for m = 0..3
