@@ -291,7 +291,7 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-NCU_LISTS = {"C2": "ncu_summary.json", "C3": "r01_launches_c3.json"}  # committed launch lists per workload
+NCU_LISTS = {"C2": "ncu_summary.json", "C3": "r01_launches_c3.json", "C4": "r01_launches_c4.json"}  # per workload
 
 
 def ncu_traffic(config, prefixes=("pass_kernel", "tile_pass_kernel")):
