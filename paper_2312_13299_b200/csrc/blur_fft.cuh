@@ -136,7 +136,16 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
   }
 }
 
-template <int L> __host__ __device__ constexpr int fft_threads_for() { return L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8); }
+#ifndef FFT_LONG_T
+#define FFT_LONG_T 512  // threads per CTA for L > 4096
+#endif
+#ifndef FFT_LONG_MINB
+#define FFT_LONG_MINB 1
+#endif
+__host__ __device__ constexpr int fft_threads_len(int L) {
+  return L > 4096 ? FFT_LONG_T : (L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8));
+}
+template <int L> __host__ __device__ constexpr int fft_threads_for() { return fft_threads_len(L); }
 // resident CTAs per SM the register budget must allow (~85 registers at 256 threads)
 // 4 CTAs per SM at 256 threads (64 registers): the passes are latency-bound, so
 // occupancy beats the second buffer (measured: C2 144.5 -> 138.5 ms)
@@ -154,7 +163,7 @@ template <int L> __host__ __device__ constexpr int fft_threads_for() { return L 
 #define FFT_MINB_2560 3
 #endif
 template <int L> __host__ __device__ constexpr int fft_min_blocks() {
-  return L > 4096 ? 1
+  return L > 4096 ? FFT_LONG_MINB
                   : (L == 3072 ? FFT_MINB_3072
                                : (L == 2560 ? FFT_MINB_2560 : (FFT_MINB * 256) / fft_threads_for<L>()));
 }

@@ -217,7 +217,7 @@ void* fft_kernel_ptr(int lc) {
   return nullptr;
 }
 
-int fft_threads(int L) { return L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8); }
+int fft_threads(int L) { return fft_threads_len(L); }
 
 // FFT length for lines of n samples and half-widths up to hmax: the shortest
 // instantiated L (2^k, 5 <= k <= 13; 3 * 2^k, 9 <= k <= 11; 5 * 2^k, 9 <= k
