@@ -96,7 +96,12 @@ constexpr int PREC_INTS = 96;
 // Blocks whose feature + target rows fit in TILE_SMEM_MAX bytes of shared
 // memory are processed by the tile kernel (coalesced staging), larger blocks
 // by the gather kernel.
-constexpr int TILE_ROWS_MAX = 32 * 1024;  // F + T rows of one block
+// measured at C2: 24 KB 114.2 ms, 32 KB 113.1 ms, 40 KB 114.9 ms, 48 KB 115.3-117.0 ms (C4: 32 KB
+// 2.610 s, 48 KB 2.635 s)
+#ifndef TILE_ROWS_KB
+#define TILE_ROWS_KB 32
+#endif
+constexpr int TILE_ROWS_MAX = TILE_ROWS_KB * 1024;  // F + T rows of one block
 __host__ __device__ __forceinline__ bool use_tile(int beta, int S) {
   return 2ll * beta * beta * S * 4 <= TILE_ROWS_MAX;
 }
