@@ -152,6 +152,12 @@ int plas_sort(const plas_sort_args* args, plas_sort_result* result, void* ws, si
 int plas_assign_groups(float* feat, int64_t* point_idx, const float* target, int dim, int stride,
                        const int64_t* groups, int64_t num_groups, int group_size, void* stream);
 
+/* Same with a float64 target (rows of `stride` doubles, dim <= 64): the
+ * reference's numba kernel then differences in fp64 (plas.py:134-136 with a
+ * float64 `target`), which this entry reproduces. */
+int plas_assign_groups_f64t(float* feat, int64_t* point_idx, const double* target, int dim, int stride,
+                            const int64_t* groups, int64_t num_groups, int group_size, void* stream);
+
 /* Workspace for the auxiliary entry points below on an (H, W, C) grid. */
 size_t plas_aux_workspace_bytes(int H, int W, int C);
 

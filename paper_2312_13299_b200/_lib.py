@@ -78,6 +78,7 @@ SIGNATURES = {
     "plas_sort_workspace_bytes_sharded": (sz, [i64, i32, i32, i64, i64, i32, i32]),
     "plas_sort": (i32, [ctypes.POINTER(SortArgs), ctypes.POINTER(SortResult), P, sz]),
     "plas_assign_groups": (i32, [P, P, P, i32, i32, P, i64, i32, P]),
+    "plas_assign_groups_f64t": (i32, [P, P, P, i32, i32, P, i64, i32, P]),
     "plas_aux_workspace_bytes": (sz, [i32, i32, i32]),
     "plas_blur": (i32, [P, P, i32, i32, i32, i32, P, i32, i32, P, sz, P]),
     "plas_blur_tiers_workspace_bytes": (sz, [i32, i32, i32, i32]),
@@ -154,18 +155,26 @@ def ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-_ws = {}
+_ws = threading.local()
 
 
 def workspace(nbytes, tag="main"):
-    """A cached uint8 device buffer of at least nbytes (torch caching allocator)."""
+    """A cached uint8 device buffer of at least nbytes (torch caching allocator).
+
+    Buffers are private to (calling thread, device, current stream): the C ABI
+    releases the GIL (ctypes), so two threads sorting at once, or one thread
+    queueing asynchronous API calls on two streams, never share scratch memory.
+    A thread's buffers are freed with the thread."""
     import torch
     dev = torch.cuda.current_device()
-    key = (tag, dev)
-    buf = _ws.get(key)
+    cache = getattr(_ws, "bufs", None)
+    if cache is None:
+        cache = _ws.bufs = {}
+    key = (tag, dev, torch.cuda.current_stream(dev).cuda_stream)
+    buf = cache.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=f"cuda:{dev}")
-        _ws[key] = buf
+        cache[key] = buf
     return buf
 
 

@@ -211,14 +211,55 @@ __device__ __forceinline__ void lane_best_fast_cols(float c0, const float (&x)[4
 // groups of a warp).  rowj[j] = row index (cell or staged local index) of slot
 // j, Fb/Tb the row bases.  With WIDE == false (S <= 16) Fc[i] returns chunk s
 // of feature row i for the move.  Returns the arrangement index (0 = identity).
+//
+// Lane s keeps its partial sums in *rotated* target order: acc[i][jj] is the
+// pair (slot i, target jj ^ s) -- the target rows are fetched through
+// rowt[jj] = rowj[jj ^ s], which the caller gets for free from its shuffles.
+// Then the column reduce-scatter over the group's 4 lanes needs no selects:
+// lane s keeps jj in {0, 1} and receives jj ^ 2 from lane s ^ 2 (the same
+// target, jj ^ s), then keeps jj = 0 (target s) and receives jj = 1 from lane
+// s ^ 1 (target 1 ^ s ^ 1 = s).
+// acc[i][jj] += the packed squared differences of chunk pair (Fc[i], Tc[jj])
+__device__ __forceinline__ void accum_chunks(unsigned long long (&acc)[4][4], const float4 (&Fc)[4],
+                                             const float4 (&Tc)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      acc[i][j] = sqacc2(sub2(pk2(Fc[i].x, Fc[i].y), pk2(Tc[j].x, Tc[j].y)), acc[i][j]);
+      acc[i][j] = sqacc2(sub2(pk2(Fc[i].z, Fc[i].w), pk2(Tc[j].z, Tc[j].w)), acc[i][j]);
+    }
+}
+
+// chunk c of the 4 feature rows (slot order) and the 4 target rows (rotated
+// order) of a group.  No data selects: slots >= k read row rowj = 0 (their
+// pairs are never used); a lane past the row (c >= nch) reads chunk 0 of the
+// quad's first feature row as every operand, so all its differences are
+// exactly zero.
+template <bool TNC>
+__device__ __forceinline__ void load_chunks(const float* Fb, const float* Tb, const int (&rowj)[4],
+                                            const int (&rowt)[4], int S, int c, bool valid, float4 (&Fc)[4],
+                                            float4 (&Tc)[4]) {
+  const float* Tv = valid ? Tb : Fb;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const unsigned fo = valid ? (unsigned)rowj[i] * (unsigned)S + 4u * c : (unsigned)rowj[0] * (unsigned)S;
+    const unsigned to = valid ? (unsigned)rowt[i] * (unsigned)S + 4u * c : (unsigned)rowj[0] * (unsigned)S;
+    Fc[i] = ld4v(Fb + fo);
+    Tc[i] = (TNC && valid) ? ld4g(Tv + to) : ld4v(Tv + to);
+  }
+}
+
+__device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4][4], const float* Fb,
+                                               const float* Tb, const int (&rowj)[4], int D, int S, int k,
+                                               int* exact);
+
 template <bool WIDE, bool TNC>
-__device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const int (&rowj)[4], int D,
-                                       int S, int k, float4 (&Fc)[4], int* exact) {
-  const int lane = threadIdx.x & 31;
-  const int s = lane & 3;
-  const int gbase = lane & ~3;
+__device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const int (&rowj)[4],
+                                       const int (&rowt)[4], int D, int S, int k, float4 (&Fc)[4], int* exact) {
+  const int s = threadIdx.x & 3;
   const int nch = S >> 2;
-  // fast-tier partial squared distances: acc[i][j] holds the (even, odd)
+  // fast-tier partial squared distances: acc[i][jj] holds the (even, odd)
   // channel halves as one f32x2 register, fed straight from the 8-byte halves
   // of the loaded chunks; pad channels (>= D) are zero in both rows
   unsigned long long acc[4][4];
@@ -229,26 +270,20 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
   const int rounds = WIDE ? (nch + 3) >> 2 : 1;
   for (int r = 0; r < rounds; r++) {
     const int c = 4 * r + s;
-    const bool valid = c < nch;
-    // no data selects: slots >= k read row rowj = 0 (their pairs are never
-    // used); a lane past the row reads chunk 0 of the quad's first feature row
-    // as every operand, so all its differences are exactly zero
-    const float* Tv = valid ? Tb : Fb;
     float4 Tc[4];
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const long long off = valid ? (long long)rowj[i] * S + 4 * c : (long long)rowj[0] * S;
-      Fc[i] = ld4v(Fb + off);
-      Tc[i] = (TNC && valid) ? ld4g(Tv + off) : ld4v(Tv + off);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        acc[i][j] = sqacc2(sub2(pk2(Fc[i].x, Fc[i].y), pk2(Tc[j].x, Tc[j].y)), acc[i][j]);
-        acc[i][j] = sqacc2(sub2(pk2(Fc[i].z, Fc[i].w), pk2(Tc[j].z, Tc[j].w)), acc[i][j]);
-      }
+    load_chunks<TNC>(Fb, Tb, rowj, rowt, S, c, c < nch, Fc, Tc);
+    accum_chunks(acc, Fc, Tc);
   }
+  return decide_from_acc(acc, Fb, Tb, rowj, D, S, k, exact);
+}
+
+__device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4][4], const float* Fb,
+                                               const float* Tb, const int (&rowj)[4], int D, int S, int k,
+                                               int* exact) {
+  const int lane = threadIdx.x & 31;
+  const int s = lane & 3;
+  const int gbase = lane & ~3;
+  const int nch = S >> 2;
   float part[4][4];
 #pragma unroll
   for (int i = 0; i < 4; i++)
@@ -257,24 +292,14 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
       const float2 h = upk2(acc[i][j]);
       part[i][j] = h.x + h.y;
     }
-  // reduce-scatter over the 4 lanes by column: lane s ends with column j = s
-  // of the cost matrix, col[i] = C[i][s]
-  const bool hi2 = (s & 2) != 0, hi1 = (s & 1) != 0;
-  float half[2][4];
-#pragma unroll
-  for (int t = 0; t < 2; t++)
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const float send = hi2 ? part[i][t] : part[i][2 + t];
-      const float keep = hi2 ? part[i][2 + t] : part[i][t];
-      half[t][i] = keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 2);
-    }
+  // reduce-scatter over the 4 lanes by column (rotated order, no selects):
+  // lane s ends with column s of the cost matrix, col[i] = C[i][s]
   float col[4];
 #pragma unroll
   for (int i = 0; i < 4; i++) {
-    const float send = hi1 ? half[0][i] : half[1][i];
-    const float keep = hi1 ? half[1][i] : half[0][i];
-    col[i] = sqrt_approx(keep + __shfl_xor_sync(PLAS_FULL_MASK, send, 1));
+    const float h0 = part[i][0] + __shfl_xor_sync(PLAS_FULL_MASK, part[i][2], 2);
+    const float h1 = part[i][1] + __shfl_xor_sync(PLAS_FULL_MASK, part[i][3], 2);
+    col[i] = sqrt_approx(h0 + __shfl_xor_sync(PLAS_FULL_MASK, h1, 1));
   }
   // lane s takes the arrangements that put slot 0's element in target s: it
   // needs C[i][o_q] for the other targets o_0 < o_1 < o_2, i.e. column o_q's
@@ -307,7 +332,7 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
   if (__any_sync(PLAS_FULL_MASK, !certain)) {
     // ---- exact tier for the whole warp (same decision wherever the fast one was
     // certain): lane s recomputes row s with the reference arithmetic
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double dacc[4] = {0.0, 0.0, 0.0, 0.0};
     float cst[4];
     const long long fo = (long long)pick4(rowj, s) * S;
 #pragma unroll
@@ -321,11 +346,11 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
           for (int e = 0; e < 4; e++)
             if (4 * c + e < D) {
               const float df = __fsub_rn(f4get(f, e), f4get(t, e));
-              acc[j] = __dadd_rn(acc[j], (double)__fmul_rn(df, df));
+              dacc[j] = __dadd_rn(dacc[j], (double)__fmul_rn(df, df));
             }
         }
       }
-      cst[j] = __double2float_rn(__dsqrt_rn(acc[j]));
+      cst[j] = __double2float_rn(__dsqrt_rn(dacc[j]));
     }
     CostMat C;
 #pragma unroll
@@ -343,36 +368,24 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
         bp = op;
       }
     }
+    // every arrangement sum +inf (fp32 costs overflowed): the reference keeps
+    // best = 0, the identity (plas.py:138-146, strict < against best_cost = inf)
+    if (bp == 0x7fffffff) bp = 0;
     if (s == 0 && k >= 2 && !certain) *exact += 1;
   }
   return k < 2 ? 0 : bp;
 }
 
-// Local index l of the block's grouping for slot s of quad q (plas.py:209):
-// PARITY: the filtered master permutation; DEVICE: the keyed bijection.
-template <bool PARITY>
-__device__ __forceinline__ unsigned group_local(const int* __restrict__ sel, long long sel_stride, int cls,
+// Grouping-table entry (pack_local: (ly << 16) | lx) of slot s of quad q of a
+// block of class cls.  PARITY: the filtered master permutation
+// (plas.py:209, class_select_kernel); DEVICE: the keyed bijection tabulated by
+// gen_class_tables (the caller passes the buffer of this pass's parity).
+__device__ __forceinline__ unsigned group_entry(const int* __restrict__ sel, long long sel_stride, int cls,
                                                 unsigned q, int s) {
-  // PARITY: host-exact master permutation filtered per class (class_select_kernel);
-  // DEVICE: the keyed bijections tabulated by gen_class_tables (the caller passes
-  // the buffer of this pass's parity)
   return (unsigned)__ldg(sel + (long long)cls * sel_stride + 4 * q + s);
 }
-
-// l -> (ly, lx) = (l / ww, l % ww) with a float reciprocal (l < 2^24) and a +-1 fix
-__device__ __forceinline__ void split_local(unsigned l, int ww, float rw, int* ly, int* lx) {
-  int y = (int)__float2uint_rz(__fmul_rn((float)l, rw));
-  int x = (int)l - y * ww;
-  if (x < 0) {
-    y--;
-    x += ww;
-  } else if (x >= ww) {
-    y++;
-    x -= ww;
-  }
-  *ly = y;
-  *lx = x;
-}
+__device__ __forceinline__ int entry_cell_off(unsigned e, int side) { return (int)(e >> 16) * side + (int)(e & 0xffffu); }
+__device__ __forceinline__ int entry_row(unsigned e, int ww) { return (int)(e >> 16) * ww + (int)(e & 0xffffu); }
 
 // Moved-cell list: CTAs stage the destination cells of their moves in shared
 // memory and append them to list[] with one reservation on *count per flush.
@@ -475,10 +488,11 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
   // geometry of group g for lane slot s; the table entry load is issued here
   // and consumed one iteration later (prefetch)
   struct Geo {
-    int k, ww, y0, x0, l;
+    int k, base;  // slot count, block origin cell
+    unsigned e;   // this lane's table entry (pack_local)
   };
   auto geo = [&](unsigned g) {
-    Geo o{0, 1, 0, 0, 0};
+    Geo o{0, 0, 0u};
     if (g < total) {
       const unsigned b = fastdiv(g, cap_m, cap_l);
       const unsigned q = g - b * cap;
@@ -490,10 +504,10 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
       const int rem = hh * ww - 4 * (int)q;
       if (rem >= 2) {  // a single leftover cell never moves
         o.k = rem >= 4 ? 4 : rem;
-        o.ww = ww;
-        o.y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
-        o.x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
-        if (s < o.k) o.l = (int)group_local<PARITY>(selp, sel_stride, ty * 3 + tx, q, s);
+        const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
+        const int x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
+        o.base = y0 * side + x0;
+        if (s < o.k) o.e = group_entry(selp, sel_stride, ty * 3 + tx, q, s);
       }
     }
     return o;
@@ -503,19 +517,17 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
     const Geo gc = gnext;
     gnext = geo(base + gridDim.x * 64u + gl);
     const int k = gc.k;
-    int cell = 0;
-    if (s < k) {
-      int ly, lx;
-      split_local((unsigned)gc.l, gc.ww, __frcp_rn((float)gc.ww), &ly, &lx);
-      cell = (gc.y0 + ly) * side + gc.x0 + lx;
-    }
+    const int cell = s < k ? gc.base + entry_cell_off(gc.e, side) : 0;
     // this lane's element index, needed only if its cell moves (loaded with the rows)
     const int my_idx0 = s < k ? idx[cell] : 0;
-    int rowj[4];
+    int rowj[4], rowt[4];
 #pragma unroll
-    for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+    for (int j = 0; j < 4; j++) {
+      rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+      rowt[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + (j ^ s));
+    }
     float4 Fc[4];
-    const int bp = decide4<WIDE, true>(feat, target, rowj, D, S, k, Fc, &exact);
+    const int bp = decide4<WIDE, true>(feat, target, rowj, rowt, D, S, k, Fc, &exact);
     const unsigned code = perm_dest_code(k, bp);
     int dst[4], dcl[4];
     bool mv[4];
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
       if (s < nch) {
 #pragma unroll
         for (int i = 0; i < 4; i++)
-          if (mv[i]) st4(feat + (long long)dcl[i] * S + 4 * s, Fc[i]);
+          if (mv[i]) st4(feat + (unsigned)dcl[i] * (unsigned)S + 4 * s, Fc[i]);
       }
     } else {
       // chunk columns: every read of a column precedes its writes
@@ -559,34 +571,183 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
   gtrace_mark(ctrl, 1);
 }
 
+// Gather-regime pass kernel for rows of <= 16 floats, software-pipelined: the
+// rows (and element indices) of a team's next group are loaded into registers
+// before the current group is decided, so every warp keeps one group's
+// gathers in flight while it computes (the plain form waited for them with
+// all its warps in the same phase: long-scoreboard stalls dominated).  The
+// early loads touch other groups' cells only (a pass's groups are disjoint,
+// plas.py:118-121), so they never race with this group's moves.  Same
+// decisions and table layout as pass_kernel.
+#ifndef K3P_MINB
+#define K3P_MINB 2
+#endif
+template <bool PARITY>
+__global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restrict__ feat, int* __restrict__ idx,
+                                                                  const float* __restrict__ target, int D, int S,
+                                                                  const Ctrl* __restrict__ ctrl,
+                                                                  const int* __restrict__ sel, long long sel_stride,
+                                                                  MoveOut mo, int* __restrict__ counters) {
+  __shared__ PassShared ps;
+  __shared__ int s_list[8 * WARP_LIST];
+  if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
+  gtrace_mark(ctrl, 0);
+  load_pass_shared(ps, ctrl);
+  const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
+  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+  int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
+  int wcnt = 0;
+  const int side = ctrl->side;
+  const int beta = ctrl->beta;
+  const int fy = ctrl->first_y, fx = ctrl->first_x;
+  const int nby = ctrl->nby, nbx = ctrl->nbx;
+  const unsigned cap = (unsigned)ctrl->cap;
+  const unsigned g_lo = (unsigned)ctrl->g_lo, total = (unsigned)ctrl->g_hi;  // this rank's groups
+  const unsigned cap_m = ctrl->cap_m, nbx_m = ctrl->nbx_m;
+  const int cap_l = ctrl->cap_l, nbx_l = ctrl->nbx_l;
+  const int nch = S >> 2;
+  const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
+  const bool cvalid = s < nch;
+  int exact = 0;
+  // (slot count, this lane's cell) of group g; cell 0 for absent slots
+  auto group_cell = [&](unsigned g, int* k) {
+    *k = 0;
+    int cell = 0;
+    if (g < total) {
+      const unsigned b = fastdiv(g, cap_m, cap_l);
+      const unsigned q = g - b * cap;
+      const unsigned by = fastdiv(b, nbx_m, nbx_l);
+      const unsigned bx = b - by * (unsigned)nbx;
+      const int ty = by == 0 ? 0 : (by == (unsigned)nby - 1 ? 2 : 1);
+      const int tx = bx == 0 ? 0 : (bx == (unsigned)nbx - 1 ? 2 : 1);
+      const int hh = ps.seg[ty], ww = ps.seg[3 + tx];
+      const int rem = hh * ww - 4 * (int)q;
+      if (rem >= 2) {  // a single leftover cell never moves
+        *k = rem >= 4 ? 4 : rem;
+        const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
+        const int x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
+        if (s < *k) cell = y0 * side + x0 + entry_cell_off(group_entry(selp, sel_stride, ty * 3 + tx, q, s), side);
+      }
+    }
+    return cell;
+  };
+  const unsigned stride = gridDim.x * 64u;
+  unsigned g = g_lo + blockIdx.x * 64u + gl;
+  int k;
+  int cell = group_cell(g, &k);
+  int rowj[4], rowt[4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+    rowt[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + (j ^ s));
+  }
+  float4 Fc[4], Tc[4];
+  load_chunks<true>(feat, target, rowj, rowt, S, s, cvalid, Fc, Tc);
+  int my_idx = s < k ? idx[cell] : 0;
+  for (unsigned base = g_lo + blockIdx.x * 64u; base < total; base += stride) {
+    // ---- the next group's gathers go out first
+    g += stride;
+    int nk;
+    const int ncell = group_cell(g, &nk);
+    int nrowj[4], nrowt[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      nrowj[j] = __shfl_sync(PLAS_FULL_MASK, ncell, (lane & ~3) + j);
+      nrowt[j] = __shfl_sync(PLAS_FULL_MASK, ncell, (lane & ~3) + (j ^ s));
+    }
+    float4 nFc[4], nTc[4];
+    load_chunks<true>(feat, target, nrowj, nrowt, S, s, cvalid, nFc, nTc);
+    const int nidx = s < nk ? idx[ncell] : 0;
+    // ---- decide and apply the current group
+    unsigned long long acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
+    accum_chunks(acc, Fc, Tc);
+    const int bp = decide_from_acc(acc, feat, target, rowj, D, S, k, &exact);
+    const unsigned code = perm_dest_code(k, bp);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int dst = (int)((code >> (2 * i)) & 3u);
+      const int dcl = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + dst);  // destination cell of slot i
+      if (dst != i && cvalid) st4(feat + (unsigned)dcl * (unsigned)S + 4 * s, Fc[i]);
+    }
+    const int my_dst = (int)((code >> (2 * s)) & 3u);
+    const bool my_mv = my_dst != s;
+    const int dcell = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + my_dst);
+    if (my_mv) idx[dcell] = my_idx;
+    stage_move(my_mv, dcell, wlist, &wcnt, mo);
+    // ---- rotate
+    k = nk;
+    cell = ncell;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      rowj[j] = nrowj[j];
+      Fc[j] = nFc[j];
+      Tc[j] = nTc[j];
+    }
+    my_idx = nidx;
+  }
+  flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
+  if (lane == 0 && ex) atomicAdd(counters + 1, ex);
+  gtrace_mark(ctrl, 1);
+}
+
 // Tile-regime pass kernel (small blocks).  A CTA walks blocks b = blockIdx.x,
-// +gridDim.x, ... with a two-stage cp.async pipeline: while the groups of
-// block b are decided from shared memory, the feature rows, target rows and
-// indices of the next block are being copied in (every block row is
-// contiguous in HBM, so the copies are coalesced 16-byte transfers).  Only
-// moved rows are written back, from the staged copy, so in-place swaps need
-// no ordering.  Same decisions as pass_kernel.
+// +gridDim.x, ... through a TILE_NST-stage shared-memory ring: while the
+// groups of block b are decided from shared memory, the feature and target
+// rows of the next blocks arrive by bulk copies (cp.async.bulk, one per block
+// row and array, issued by the lanes of warp 0 and counted on the stage's
+// "full" mbarrier), so the staging costs a few instructions per block instead
+// of one per 16 bytes.  Each warp releases a stage on its "empty" mbarrier
+// when it has read it, and the producer refills a stage only after all warps
+// released it: no CTA-wide barrier per block, warps drift apart by up to
+// TILE_NST - 1 blocks.
+// Every block row is contiguous in HBM (ww * S floats), so the copies stream.
+// Element indices are read per group from global memory (only moved cells
+// write them back).  Only moved rows are written back, from registers (rows
+// <= 16 floats) or the staged copy, so in-place swaps need no ordering.  Same
+// decisions as pass_kernel.
 constexpr int TILE_THREADS = 256;
 constexpr int TILE_WARP_LIST = 128;  // moved-cell staging per warp in the tile kernel
+#ifndef TILE_NST
+#define TILE_NST 2
+#endif
+#ifndef TILE_MINB
+#define TILE_MINB (TILE_NST == 2 ? 3 : 2)
+#endif
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// bytes of one pipeline stage for blocks of up to bmax x bmax cells
+// bytes of one pipeline stage for blocks of up to bmax x bmax cells (F rows, T rows)
 __host__ __device__ __forceinline__ long long tile_stage_bytes(int bmax, int S) {
   const long long m = (long long)bmax * bmax;
-  return (2 * m * S * 4 + m * 4 + 15) / 16 * 16;  // F rows, T rows, idx
+  return (2 * m * S * 4 + 127) / 128 * 128;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 struct TileGeom {
@@ -608,16 +769,24 @@ __device__ __forceinline__ TileGeom tile_geom(int b, int nbx, unsigned nbx_m, in
 }
 
 template <bool WIDE, bool PARITY>
-__global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
+__global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : TILE_MINB) tile_pass_kernel(
     float* __restrict__ feat, int* __restrict__ idx, const float* __restrict__ target, int D, int S,
     const Ctrl* __restrict__ ctrl, const int* __restrict__ sel, long long sel_stride, MoveOut mo,
     int* __restrict__ counters) {
-  extern __shared__ float4 smem4[];
+  extern __shared__ __align__(128) float4 smem4[];
   __shared__ PassShared ps;
   __shared__ int s_list[8 * TILE_WARP_LIST];  // small lists: 3 CTAs per SM fit in shared memory
+  __shared__ unsigned long long s_full[TILE_NST], s_empty[TILE_NST];
   if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
   gtrace_mark(ctrl, 0);
-  load_pass_shared(ps, ctrl);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TILE_NST; i++) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], TILE_THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  load_pass_shared(ps, ctrl);  // (its __syncthreads also publishes the barriers)
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
   if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
@@ -631,83 +800,78 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
   const int nbx_l = ctrl->nbx_l;
   const int b_lo = ctrl->b_lo, nblocks = ctrl->b_hi;  // this rank's blocks
   const int nch = S >> 2;
-  const long long mmax = (long long)beta * beta;
-  const size_t stage_floats = (size_t)(tile_stage_bytes(beta, S) / 4);
+  const int mmax = beta * beta;
+  const int stage_floats = (int)(tile_stage_bytes(beta, S) / 4);
   float* stage_base = reinterpret_cast<float*>(smem4);
   const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
+  const int first = b_lo + blockIdx.x;
+  const int G = gridDim.x;
 
-  // issue the copies of block b into stage st
-  auto prefetch = [&](int b, int st) {
-    if (b < nblocks) {
+  // warp 0: the CTA's it-th block into stage it % TILE_NST once every warp
+  // released that stage's previous block (lane r copies row r of both arrays;
+  // lane 0 first announces the byte count)
+  auto produce = [&](int it) {
+    const int b = first + it * G;
+    if (threadIdx.x < 32 && b < nblocks) {
+      const int st = it % TILE_NST;
+      if (it >= TILE_NST) mbar_wait(&s_empty[st], (unsigned)((it / TILE_NST - 1) & 1));
       const TileGeom g = tile_geom(b, nbx, nbx_m, nbx_l, nby, fy, fx, beta, ps.seg);
+      const unsigned rowb = (unsigned)(g.ww * S * 4);
+      if (lane == 0) mbar_expect_tx(&s_full[st], 2u * rowb * (unsigned)g.hh);
+      __syncwarp();
       float* sF = stage_base + st * stage_floats;
       float* sT = sF + mmax * S;
-      int* sI = reinterpret_cast<int*>(sT + mmax * S);
-      const int row4 = g.ww * nch;
-      const float rr4 = __frcp_rn((float)row4), rw = __frcp_rn((float)g.ww);
-      const bool pow2 = (row4 & (row4 - 1)) == 0 && (g.ww & (g.ww - 1)) == 0;  // full blocks at beta = 2^k
-      const int sh4 = 31 - __clz(row4), shw = 31 - __clz(g.ww);
-      for (int e = threadIdx.x; e < g.hh * row4; e += blockDim.x) {
-        int r, c;
-        if (pow2) {
-          r = e >> sh4;
-          c = e & (row4 - 1);
-        } else {
-          split_local((unsigned)e, row4, rr4, &r, &c);
-        }
-        const long long go = ((long long)(g.y0 + r) * side + g.x0) * S + 4 * c;
-        cp_async16(sF + 4 * e, feat + go);
-        cp_async16(sT + 4 * e, target + go);
-      }
-      for (int e = threadIdx.x; e < g.hh * g.ww; e += blockDim.x) {
-        int r, c;
-        if (pow2) {
-          r = e >> shw;
-          c = e & (g.ww - 1);
-        } else {
-          split_local((unsigned)e, g.ww, rw, &r, &c);
-        }
-        cp_async4(sI + e, idx + (long long)(g.y0 + r) * side + g.x0 + c);
+      for (int r = lane; r < g.hh; r += 32) {
+        const unsigned go = ((unsigned)(g.y0 + r) * (unsigned)side + (unsigned)g.x0) * (unsigned)S;
+        const unsigned so = (unsigned)(r * g.ww * S);
+        bulk_g2s(sF + so, feat + go, rowb, &s_full[st]);
+        bulk_g2s(sT + so, target + go, rowb, &s_full[st]);
       }
     }
-    cp_async_commit();
   };
 
   int exact = 0;
-  int b = b_lo + blockIdx.x, st = 0;
-  prefetch(b, 0);
-  for (; b < nblocks; b += gridDim.x, st ^= 1) {
-    prefetch(b + gridDim.x, st ^ 1);
-    cp_async_wait<1>();  // block b's stage has landed
-    __syncthreads();
+  for (int it = 0; it < TILE_NST - 1; it++) produce(it);
+  for (int it = 0; first + it * G < nblocks; it++) {
+    produce(it + TILE_NST - 1);
+    const int b = first + it * G;
+    const int st = it % TILE_NST;
+    mbar_wait(&s_full[st], (unsigned)((it / TILE_NST) & 1));  // block b's rows have landed
     const TileGeom g = tile_geom(b, nbx, nbx_m, nbx_l, nby, fy, fx, beta, ps.seg);
     const float* sF = stage_base + st * stage_floats;
     const float* sT = sF + mmax * S;
-    const int* sI = reinterpret_cast<const int*>(sT + mmax * S);
     const int m = g.hh * g.ww;
     const int ngroups = (m + 3) >> 2;
-    const float rw = __frcp_rn((float)g.ww);
+    const int origin = g.y0 * side + g.x0;
     // slot count and table entry of group q (the entry of the next group is
     // loaded one iteration ahead)
-    auto group_at = [&](int q, int* k, int* l) {
+    auto group_at = [&](int q, int* k, unsigned* e) {
       *k = 0;
-      *l = 0;
+      *e = 0u;
       if (q < ngroups) {
         const int rem = m - 4 * q;
         if (rem >= 2) *k = rem >= 4 ? 4 : rem;
-        if (s < *k) *l = (int)group_local<PARITY>(selp, sel_stride, g.cls, (unsigned)q, s);
+        if (s < *k) *e = group_entry(selp, sel_stride, g.cls, (unsigned)q, s);
       }
     };
-    int knext, lnext;
-    group_at(gl, &knext, &lnext);
+    int knext;
+    unsigned enext;
+    group_at(gl, &knext, &enext);
     for (int q0 = 0; q0 < ngroups; q0 += TILE_THREADS / 4) {
-      const int k = knext, l = lnext;
-      group_at(q0 + TILE_THREADS / 4 + gl, &knext, &lnext);
-      int rowj[4];
+      const int k = knext;
+      const unsigned e = enext;
+      group_at(q0 + TILE_THREADS / 4 + gl, &knext, &enext);
+      const int mycell = origin + entry_cell_off(e, side);
+      const int my_idx = s < k ? __ldg(idx + mycell) : 0;  // consumed after the decision
+      const int myrow = entry_row(e, g.ww);
+      int rowj[4], rowt[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, l, (lane & ~3) + j);
+      for (int j = 0; j < 4; j++) {
+        rowj[j] = __shfl_sync(PLAS_FULL_MASK, myrow, (lane & ~3) + j);
+        rowt[j] = __shfl_sync(PLAS_FULL_MASK, myrow, (lane & ~3) + (j ^ s));
+      }
       float4 Fc[4];
-      const int bp = decide4<WIDE, false>(sF, sT, rowj, D, S, k, Fc, &exact);
+      const int bp = decide4<WIDE, false>(sF, sT, rowj, rowt, D, S, k, Fc, &exact);
       const unsigned code = perm_dest_code(k, bp);
       int dst[4];
       bool mv[4];
@@ -716,10 +880,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
         dst[i] = (int)((code >> (2 * i)) & 3u);
         mv[i] = dst[i] != i;
       }
-      // this lane's slot's grid cell; the destinations by shuffle from the quad
-      int ly, lx;
-      split_local((unsigned)l, g.ww, rw, &ly, &lx);
-      const int mycell = (g.y0 + ly) * side + g.x0 + lx;
       int dcl[4];
 #pragma unroll
       for (int i = 0; i < 4; i++) dcl[i] = __shfl_sync(PLAS_FULL_MASK, mycell, (lane & ~3) + dst[i]);
@@ -727,24 +887,24 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
         if (s < nch) {
 #pragma unroll
           for (int i = 0; i < 4; i++)
-            if (mv[i]) st4(feat + (long long)dcl[i] * S + 4 * s, Fc[i]);
+            if (mv[i]) st4(feat + (unsigned)dcl[i] * (unsigned)S + 4 * s, Fc[i]);
         }
       } else {
         for (int c = s; c < nch; c += 4) {
 #pragma unroll
           for (int i = 0; i < 4; i++)
-            if (mv[i]) st4(feat + (long long)dcl[i] * S + 4 * c, ld4v(sF + (long long)rowj[i] * S + 4 * c));
+            if (mv[i]) st4(feat + (unsigned)dcl[i] * (unsigned)S + 4 * c, ld4v(sF + (unsigned)rowj[i] * (unsigned)S + 4 * c));
         }
       }
       const int my_dst = (int)((code >> (2 * s)) & 3u);
       const bool my_mv = my_dst != s;
       const int dcell = __shfl_sync(PLAS_FULL_MASK, mycell, (lane & ~3) + my_dst);
-      if (my_mv) idx[dcell] = sI[l];
+      if (my_mv) idx[dcell] = my_idx;
       stage_move<TILE_WARP_LIST>(my_mv, dcell, wlist, &wcnt, mo);
     }
-    __syncthreads();  // stage st is refilled by the prefetch two iterations on
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[st]);  // this warp is done with stage st
   }
-  cp_async_wait<0>();
   flush_moves<TILE_WARP_LIST>(mo, s_list, wcnt, ps.wcnt, &ps.base);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
@@ -752,7 +912,8 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : 3) tile_pass_kernel(
 }
 
 // Parity mode: per class (ty, tx) the stable filter master_perm[master_perm < m]
-// (plas.py:209).  One CTA per class; master perm of beta^2 entries.
+// (plas.py:209), stored as pack_local entries.  One CTA per class; master perm
+// of beta^2 entries.
 __global__ void __launch_bounds__(1024) class_select_kernel(const int* __restrict__ mp,
                                                              const Ctrl* __restrict__ ctrl,
                                                              int* __restrict__ sel,
@@ -765,7 +926,8 @@ __global__ void __launch_bounds__(1024) class_select_kernel(const int* __restric
   // class exists?  type 0 = first segment, 2 = last (needs >= 2 segments), 1 = interior (>= 3)
   auto exists = [](int t, int n) { return t == 0 || (t == 2 && n >= 2) || (t == 1 && n >= 3); };
   if (!exists(ty, nby) || !exists(tx, nbx)) return;
-  const long long m = (long long)ctrl->seg_h[ty] * ctrl->seg_w[tx];
+  const unsigned ww = (unsigned)ctrl->seg_w[tx];
+  const long long m = (long long)ctrl->seg_h[ty] * ww;
   const long long n = (long long)beta * beta;
   const long long per = (n + blockDim.x - 1) / blockDim.x;
   const long long s0 = threadIdx.x * per, s1 = min(n, s0 + per);
@@ -784,10 +946,9 @@ __global__ void __launch_bounds__(1024) class_select_kernel(const int* __restric
   int* out = sel + (long long)cls * sel_stride;
   for (long long i = s0; i < s1; i++) {
     int v = mp[i];
-    if (v < m) out[pos++] = v;
+    if (v < m) out[pos++] = pack_local((unsigned)v, ww);
   }
 }
-
 
 // ABI kernel for _assign_groups on an explicit (G, k) group list (plas.py:113-156).
 template <bool WIDE>
@@ -804,11 +965,14 @@ __global__ void __launch_bounds__(256) groups_kernel(float* __restrict__ feat,
     const long long g = base + (threadIdx.x >> 2);
     const int k = g < G ? kk : 0;
     const int cell = s < k ? (int)groups[g * kk + s] : 0;
-    int rowj[4];
+    int rowj[4], rowt[4];
 #pragma unroll
-    for (int j = 0; j < 4; j++) rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+    for (int j = 0; j < 4; j++) {
+      rowj[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + j);
+      rowt[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + (j ^ s));
+    }
     float4 Fc[4];
-    const int bp = decide4<WIDE, true>(feat, target, rowj, D, S, k, Fc, &exact);
+    const int bp = decide4<WIDE, true>(feat, target, rowj, rowt, D, S, k, Fc, &exact);
     int dst[4];
     bool mv[4];
 #pragma unroll
@@ -831,6 +995,55 @@ __global__ void __launch_bounds__(256) groups_kernel(float* __restrict__ feat,
       __syncwarp();
     }
     if (my_mv) idx[pick4(rowj, pick4(dst, s))] = my_idx;
+  }
+}
+
+// ABI kernel for _assign_groups with a float64 target (plas.py:129-137 as
+// numba compiles it when `target` is float64: feat[pi, d] - target[pj, d] is
+// an fp64 difference of the widened fp32 feature, squared and summed in fp64;
+// the cost is stored to the float32 cost matrix).  One thread per group (an
+// API path, not the sort's hot loop); same first-strict-minimum rule.
+__global__ void __launch_bounds__(256) groups_f64t_kernel(float* __restrict__ feat, long long* __restrict__ idx,
+                                                          const double* __restrict__ target, int D, int S,
+                                                          const long long* __restrict__ groups, long long G,
+                                                          int kk) {
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < G;
+       g += (long long)gridDim.x * blockDim.x) {
+    long long cell[4] = {0, 0, 0, 0};
+    for (int i = 0; i < kk; i++) cell[i] = groups[g * kk + i];
+    float cost[4][4];
+    for (int i = 0; i < kk; i++)
+      for (int j = 0; j < kk; j++) {
+        double acc = 0.0;
+        for (int d = 0; d < D; d++) {
+          const double df = __dsub_rn((double)feat[cell[i] * S + d], target[cell[j] * S + d]);
+          acc = __dadd_rn(acc, __dmul_rn(df, df));
+        }
+        cost[i][j] = __double2float_rn(__dsqrt_rn(acc));
+      }
+    int nperm = kk == 4 ? 24 : (kk == 3 ? 6 : 2);
+    int best = 0;
+    double best_cost = __longlong_as_double(0x7ff0000000000000ll);
+    for (int p = 0; p < nperm; p++) {
+      double c = 0.0;
+      for (int i = 0; i < kk; i++) c = __dadd_rn(c, (double)cost[i][perm_dest(kk, p, i)]);
+      if (c < best_cost) {
+        best_cost = c;
+        best = p;
+      }
+    }
+    if (best == 0) continue;
+    float held[4][64];  // rows of up to 64 channels on this path (checked by the ABI)
+    long long hidx[4];
+    for (int i = 0; i < kk; i++) {
+      for (int d = 0; d < D; d++) held[i][d] = feat[cell[i] * S + d];
+      hidx[i] = idx[cell[i]];
+    }
+    for (int i = 0; i < kk; i++) {
+      const long long dst = cell[perm_dest(kk, best, i)];
+      for (int d = 0; d < D; d++) feat[dst * S + d] = held[i][d];
+      idx[dst] = hidx[i];
+    }
   }
 }
 

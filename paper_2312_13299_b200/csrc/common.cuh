@@ -90,8 +90,18 @@ __device__ __forceinline__ void gtrace_mark(const Ctrl* c, int slot) {
 }
 
 constexpr int PDRAW_MAX = 1024;  // passes per level with precomputed draws (beyond: computed on the fly)
-// per-pass grouping record: m[9], lbits[9], rbits[9], keys[9][6]
+// per-pass grouping record: m[9], lbits[9], rbits[9], keys[9][6], ww[9]
 constexpr int PREC_INTS = 96;
+constexpr int PREC_WW = 81;
+
+// Grouping-table entry of local block index l (row-major in a block of width
+// ww): (ly << 16) | lx, so the pass kernels get the cell's offset from the
+// block origin (ly * side + lx) and its staged row (ly * ww + lx) without a
+// division per group.  side < 2^16 (n < 2^31).
+__host__ __device__ __forceinline__ int pack_local(unsigned l, unsigned ww) {
+  const unsigned ly = l / ww;
+  return (int)((ly << 16) | (l - ly * ww));
+}
 
 // Blocks whose feature + target rows fit in TILE_SMEM_MAX bytes of shared
 // memory are processed by the tile kernel (coalesced staging), larger blocks

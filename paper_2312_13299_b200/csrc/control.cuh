@@ -233,6 +233,7 @@ __device__ __forceinline__ void pass_draw_item(const Ctrl* c, int level, int bet
   r[cls] = (exists(ty, nby) && exists(tx, nbx)) ? (int)m : 0;
   r[9 + cls] = fe.lbits;
   r[18 + cls] = fe.rbits;
+  r[PREC_WW + cls] = ww;
   for (int k = 0; k < 6; k++) r[27 + 6 * cls + k] = (int)fe.keys[k];
 }
 
@@ -319,8 +320,9 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
         if (!m) continue;
         Feistel fe;
         fe.init_keys(reinterpret_cast<const unsigned*>(rec + 27 + 6 * cls), rec[9 + cls], rec[18 + cls], m);
+        const unsigned ww = (unsigned)rec[PREC_WW + cls];
         for (long long l = worker * (long long)blockDim.x + threadIdx.x; l < m; l += per)
-          tab[cls * stride + l] = (int)fe((unsigned)l);
+          tab[cls * stride + l] = pack_local(fe((unsigned)l), ww);
       }
       return;
     }
@@ -350,8 +352,9 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
     if (!m) continue;
     Feistel fe;
     fe.init_keys(nx.fe_keys[cls], nx.fe_lbits[cls], nx.fe_rbits[cls], m);
+    const unsigned ww = (unsigned)nx.seg_w[cls % 3];
     for (long long l = worker * (long long)blockDim.x + threadIdx.x; l < m; l += per)
-      tab[cls * stride + l] = (int)fe((unsigned)l);
+      tab[cls * stride + l] = pack_local(fe((unsigned)l), ww);
   }
 }
 

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -99,6 +100,26 @@ struct Carver {
     return p;
   }
 };
+
+// Dynamic shared-memory limits are per-kernel process state: concurrent calls
+// from several host threads may need different amounts for one kernel, so the
+// limit only ever grows (a lower request never shrinks it under another
+// thread's pending launch).
+std::mutex g_smem_mu;
+std::vector<std::pair<const void*, int>> g_smem_limits;
+cudaError_t raise_smem_limit(const void* fn, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  for (auto& e : g_smem_limits)
+    if (e.first == fn) {
+      if (e.second >= (int)bytes) return cudaSuccess;
+      const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (r == cudaSuccess) e.second = (int)bytes;
+      return r;
+    }
+  const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (r == cudaSuccess) g_smem_limits.push_back({fn, (int)bytes});
+  return r;
+}
 
 int row_stride(int dim) { return (dim + 3) / 4 * 4; }
 
@@ -476,9 +497,15 @@ struct Launch {
   Sched sched;
 };
 
+// PLAS_K3_PLAIN=1 selects the unpipelined gather kernel for rows <= 16 floats (A/B)
+bool k3_plain() {
+  static int v = -1;
+  if (v < 0) v = getenv("PLAS_K3_PLAIN") && atoi(getenv("PLAS_K3_PLAIN")) ? 1 : 0;
+  return v == 1;
+}
 template <bool PARITY>
 void* pass_kernel_ptr(int S) {
-  if (S <= 16) return (void*)pass_kernel<false, PARITY>;
+  if (S <= 16) return k3_plain() ? (void*)pass_kernel<false, PARITY> : (void*)pass_kernel_pipe<PARITY>;
   return (void*)pass_kernel<true, PARITY>;
 }
 
@@ -508,24 +535,31 @@ struct GraphKey {
            tcap == o.tcap && mode == o.mode && device == o.device;
   }
 };
+// An entry is shared by its users: eviction only drops the cache's reference,
+// and the exec is destroyed when the last sort that fetched it returns (never
+// while another thread is launching it).
+struct GraphExecHolder {
+  cudaGraphExec_t ge = nullptr;
+  ~GraphExecHolder() {
+    if (ge) cudaGraphExecDestroy(ge);
+  }
+};
+using GraphExecRef = std::shared_ptr<GraphExecHolder>;
 std::mutex g_graph_mu;
-std::vector<std::pair<GraphKey, cudaGraphExec_t>> g_graphs;
+std::vector<std::pair<GraphKey, GraphExecRef>> g_graphs;
 int cudaGetDevice_or(int dflt) {
   int d = dflt;
   return cudaGetDevice(&d) == cudaSuccess ? d : dflt;
 }
-cudaGraphExec_t graph_cache_get(const GraphKey& k) {
+GraphExecRef graph_cache_get(const GraphKey& k) {
   std::lock_guard<std::mutex> lk(g_graph_mu);
   for (auto& e : g_graphs)
     if (e.first == k) return e.second;
   return nullptr;
 }
-void graph_cache_put(const GraphKey& k, cudaGraphExec_t ge) {
+void graph_cache_put(const GraphKey& k, const GraphExecRef& ge) {
   std::lock_guard<std::mutex> lk(g_graph_mu);
-  if (g_graphs.size() >= 4) {
-    cudaGraphExecDestroy(g_graphs.front().second);
-    g_graphs.erase(g_graphs.begin());
-  }
+  if (g_graphs.size() >= 4) g_graphs.erase(g_graphs.begin());
   g_graphs.push_back({k, ge});
 }
 
@@ -562,15 +596,15 @@ int tile_beta_max(int S) {
   while (use_tile(b + 1, S)) b++;
   return b;
 }
-size_t tile_smem_bytes(int S) { return (size_t)(2 * tile_stage_bytes(tile_beta_max(S), S)); }
+size_t tile_smem_bytes(int S) { return (size_t)(TILE_NST * tile_stage_bytes(tile_beta_max(S), S)); }
 
 int tile_grid_size(int S) {
   static int cached[65] = {0};
   const int key = S <= 64 ? S : 64;
   // the attribute is per kernel, so set it for this S on every sort
   const size_t smem = tile_smem_bytes(S);
-  cudaFuncSetAttribute(tile_kernel_ptr<false>(S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(tile_kernel_ptr<true>(S), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  raise_smem_limit((const void*)tile_kernel_ptr<false>(S), smem);
+  raise_smem_limit((const void*)tile_kernel_ptr<true>(S), smem);
   if (!cached[key]) {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel_ptr<false>(S), TILE_THREADS, smem);
@@ -656,6 +690,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   const int side = (int)llround(sqrt((double)n));
   if (D < 1 || side < 2 || (long long)side * side != n || n >= (1LL << 31))
     return fail(PLAS_ERR_INVALID, "features must be (side^2, D) with side >= 2, D >= 1");
+  if ((unsigned long long)n * (unsigned long long)row_stride(D) >= (1ULL << 32))
+    return fail(PLAS_ERR_INVALID, "n * padded row width must be < 2^32 (32-bit row offsets in the pass kernels)");
   if (!(a->improvement_threshold > 0.0) || a->min_block_size < 2)
     return fail(PLAS_ERR_INVALID, "bad SortConfig");
   if (a->features_dtype != PLAS_F32 && a->features_dtype != PLAS_F64)
@@ -815,8 +851,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     fft1s[i] = fft_kernel_ptr<1, 1>(lcode);
     fft_nthreads[i] = fft_threads(fft_len(lcode));
     fft_smems[i] = fft_smem_bytes(lcode);
-    CK(cudaFuncSetAttribute(fft0s[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smems[i]));
-    CK(cudaFuncSetAttribute(fft1s[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smems[i]));
+    CK(raise_smem_limit((const void*)fft0s[i], fft_smems[i]));
+    CK(raise_smem_limit((const void*)fft1s[i], fft_smems[i]));
   }
   const int fft_grid = side * ((D + 1) / 2);  // one CTA per line pair
   std::vector<int> hmode(std::max(L, 1));
@@ -835,8 +871,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   if (NPL) CK(cudaMemcpyAsync(w.fft_plans, fplans, sizeof(FftPlan) * NPL, cudaMemcpyHostToDevice, st));
   lc.tb_grid = dim3((side + TB_T - 1) / TB_T, (side + TB_T - 1) / TB_T);
   if (hc.tile_blur_hmax > 0)
-    CK(cudaFuncSetAttribute(blur_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)tile_blur_smem_bytes(hc.tile_blur_hmax)));
+    CK(raise_smem_limit((const void*)blur_tile_kernel, tile_blur_smem_bytes(hc.tile_blur_hmax)));
   lc.sched = Sched{w.radii, w.betas, w.hs, w.level_counts, w.trace};
 
   auto vad_launch = [&](double* out) -> int {
@@ -865,8 +900,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     // a workspace pointer or a shape constant), so an instantiated graph is
     // reused by later sorts of the same shape on the same workspace
     const GraphKey gkey{wsp, ws_bytes, n, D, L, (long long)sch.weights.size(), tcap, mode, cudaGetDevice_or(-1)};
-    cudaGraphExec_t ge = graph_cache_get(gkey);
-    if (!ge) {
+    GraphExecRef ger = graph_cache_get(gkey);
+    if (!ger) {
+    cudaGraphExec_t ge = nullptr;
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle outer_h, tile_h;
@@ -1027,10 +1063,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     if (htrace) fprintf(stderr, "host: graph built at %.3f ms\n", hms());
     CK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    graph_cache_put(gkey, ge);
+    ger = std::make_shared<GraphExecHolder>();
+    ger->ge = ge;
+    graph_cache_put(gkey, ger);
     if (htrace) fprintf(stderr, "host: instantiated at %.3f ms\n", hms());
     }
-    CK(cudaGraphLaunch(ge, st));
+    CK(cudaGraphLaunch(ger->ge, st));
     if (htrace) fprintf(stderr, "host: launched at %.3f ms\n", hms());
     CK(cudaStreamSynchronize(st));
   } else {
@@ -1183,7 +1221,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           if (use_tile(beta, S))
             timed(K_PASS, [&] {
               le = cudaLaunchKernel(tfn, dim3(lc.tile_grid), dim3(TILE_THREADS), args,
-                                    (size_t)(2 * tile_stage_bytes(beta, S)), st);
+                                    (size_t)(TILE_NST * tile_stage_bytes(beta, S)), st);
             });
           else
             timed(K_PASS, [&] { le = cudaLaunchKernel(kpc.fn, dim3(kpc.grid), dim3(kpc.block), args, kpc.smem, st); });
@@ -1343,6 +1381,18 @@ int plas_assign_groups(float* feat, int64_t* point_idx, const float* target, int
   return PLAS_OK;
 }
 
+int plas_assign_groups_f64t(float* feat, int64_t* point_idx, const double* target, int dim, int stride,
+                            const int64_t* groups, int64_t num_groups, int group_size, void* stream) {
+  if (dim < 1 || dim > 64 || stride < dim || group_size < 2 || group_size > 4)
+    return fail(PLAS_ERR_INVALID, "bad assign_groups_f64t arguments");
+  if (num_groups <= 0) return PLAS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  groups_f64t_kernel<<<grid_for(num_groups, 256, 4), 256, 0, st>>>(
+      feat, (long long*)point_idx, target, dim, stride, (const long long*)groups, num_groups, group_size);
+  CKL();
+  return PLAS_OK;
+}
+
 size_t plas_aux_workspace_bytes(int H, int W, int C) {
   size_t cells = (size_t)H * W, tot = cells * C;
   size_t b = 0;
@@ -1493,7 +1543,7 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
   int hc[2];
   if (tier == 2) {
     const size_t smem = tile_blur_smem_bytes(half_width);
-    CK(cudaFuncSetAttribute(blur_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(raise_smem_limit((const void*)blur_tile_kernel, smem));
     hc[0] = hc[1] = 0;
     blur_tile_kernel<<<dim3((W + TB_T - 1) / TB_T, (H + TB_T - 1) / TB_T), TB_THREADS, smem, st>>>(t.feat, t.target, pg,
                                                                                                   lv, t.den32);
@@ -1514,8 +1564,8 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
     void* f0 = fft_kernel_ptr<0, 0>(lg);
     void* f1 = fft_kernel_ptr<1, 1>(lg);
     const size_t smem = fft_smem_bytes(t.lc);
-    CK(cudaFuncSetAttribute(f0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(raise_smem_limit((const void*)f0, smem));
+    CK(raise_smem_limit((const void*)f1, smem));
     const int nt = fft_threads(t.L);
     fft_spectrum_kernel<<<std::max(1, t.L / 128), 128, 0, st>>>(lv, plan);
     const float *i0 = t.feat, *i1 = t.tmp, *dn = nullptr, *den = t.den32;
@@ -1629,7 +1679,7 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
       case 3: fn = (void*)smooth_fused_kernel<3>; smem = SmoothTile<3>::smem_doubles * 8; break;
       default: fn = (void*)smooth_fused_kernel<4>; smem = SmoothTile<4>::smem_doubles * 8; break;
     }
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(raise_smem_limit((const void*)fn, smem));
     const double* pl = plane;
     double* gr = grad;
     const double* wd = a.w;

@@ -125,9 +125,15 @@ def reassign_block(feat, point_idx, target, positions, grouping):
     """Re-assign one block's cells in place (plas.py:173-193) on the GPU.
 
     ``feat`` (float32, (n, D)) and ``point_idx`` (int64, (n,)) are updated in
-    place exactly as the reference's numba kernel updates them.
+    place exactly as the reference's numba kernel updates them.  A float32
+    ``target`` (what the reference's sort passes, plas.py:252-254) takes the
+    fused K3 group kernel; any other target dtype makes the reference's numba
+    code difference and square in float64, which ``plas_assign_groups_f64t``
+    reproduces (the target is widened to float64 first, as numba promotes it).
     """
     import torch
+    tgt = np.asarray(target)
+    f64t = tgt.dtype != np.float32
     m = len(positions)
     grouping = np.asarray(grouping, dtype=np.int64)
     local = grouping[grouping < m]
@@ -142,20 +148,23 @@ def reassign_block(feat, point_idx, target, positions, grouping):
     S = _row_stride(D)
     fpad = np.zeros((n, S), dtype=np.float32)
     fpad[:, :D] = feat_np
-    tpad = np.zeros((n, S), dtype=np.float32)
-    tpad[:, :D] = np.asarray(target, dtype=np.float32)
+    tpad = np.zeros((n, S), dtype=np.float64 if f64t else np.float32)
+    tpad[:, :D] = tgt
     f_dev = torch.from_numpy(fpad).cuda()
     t_dev = torch.from_numpy(tpad).cuda()
     i_dev = torch.from_numpy(np.ascontiguousarray(point_idx, dtype=np.int64)).cuda()
     st = _lib.stream_handle()
+    fn = L.plas_assign_groups_f64t if f64t else L.plas_assign_groups
+    if f64t and D > 64:
+        raise ValueError("reassign_block: a float64 target supports at most 64 channels")
     if g4:
         groups = torch.from_numpy(np.ascontiguousarray(ordered[:g4].reshape(-1, 4))).cuda()
-        _lib.check(L.plas_assign_groups(_lib.ptr(f_dev), _lib.ptr(i_dev), _lib.ptr(t_dev), D, S,
-                                        _lib.ptr(groups), g4 // 4, 4, st), "assign_groups")
+        _lib.check(fn(_lib.ptr(f_dev), _lib.ptr(i_dev), _lib.ptr(t_dev), D, S,
+                      _lib.ptr(groups), g4 // 4, 4, st), "assign_groups")
     if rest >= 2:
         groups = torch.from_numpy(np.ascontiguousarray(ordered[g4:].reshape(1, rest))).cuda()
-        _lib.check(L.plas_assign_groups(_lib.ptr(f_dev), _lib.ptr(i_dev), _lib.ptr(t_dev), D, S,
-                                        _lib.ptr(groups), 1, rest, st), "assign_groups")
+        _lib.check(fn(_lib.ptr(f_dev), _lib.ptr(i_dev), _lib.ptr(t_dev), D, S,
+                      _lib.ptr(groups), 1, rest, st), "assign_groups")
     feat[...] = f_dev.cpu().numpy()[:, :D]
     point_idx[...] = i_dev.cpu().numpy()
 
@@ -240,7 +249,7 @@ class SortPlan:
         while True:
             wsb = L.plas_sort_workspace_bytes_sharded(self.n, self.dim, sch.num_levels, len(sch.weights),
                                                       self.trace_capacity, self.mode, world)
-            ws = _lib.workspace(wsb, "sort" if world == 1 else f"sort{shard.rank}")
+            ws = _lib.workspace(wsb, "sort")  # per thread and stream (_lib.workspace)
             args = _lib.SortArgs()
             args.features = _lib.ptr(features_dev)
             args.features_dtype = _lib.PLAS_F32 if features_dev.dtype == torch.float32 else _lib.PLAS_F64

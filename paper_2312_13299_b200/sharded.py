@@ -49,11 +49,16 @@ class DistExchange:
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
+        # the collective is chosen once, from the backend: NCCL has the fused
+        # all_gather_into_tensor; other backends (gloo in the CPU tests) take
+        # the list form.  Runtime errors propagate (a retry on a broken
+        # communicator could leave the ranks in different collectives).
+        self.fused = str(dist.get_backend(group)).lower() == "nccl"
 
     def _all_gather(self, out, inp):
-        try:
+        if self.fused:
             self.dist.all_gather_into_tensor(out, inp, group=self.group)
-        except (RuntimeError, AttributeError, NotImplementedError):  # backends without the fused op
+        else:
             self.dist.all_gather(list(out.chunk(self.world)), inp, group=self.group)
 
     def __call__(self, send, recv, part, part_all):

@@ -518,3 +518,88 @@ def test_device_graph_cache_reuse_and_eviction():
             p_step, r_step = run(f, True)
             np.testing.assert_array_equal(p_graph, p_step)
             assert r_graph == r_step
+
+
+def test_reassign_overflowing_costs_keep_identity():
+    """fp32 F - T overflows to inf for every (slot, target) pair: every
+    arrangement sum is +inf, so the reference keeps best = 0 (plas.py:138-146);
+    the same for quads and leftovers, against the oracle."""
+    for k in (4, 3, 2):
+        feat = np.full((k, 2), 3.0e38, dtype=np.float32)
+        feat[:, 1] = np.arange(k, dtype=np.float32)[::-1]
+        target = np.full((k, 2), -3.0e38, dtype=np.float32)
+        target[:, 1] = np.arange(k, dtype=np.float32)
+        f, idx = run_reassign(feat, target, list(range(k)))
+        assert idx.tolist() == list(range(k)), k
+        fo, io = feat.copy(), np.arange(k, dtype=np.int64)
+        O.reassign_block(fo, io, target, np.arange(k), np.arange(k))
+        assert np.array_equal(idx, io) and np.array_equal(f, fo)
+
+
+def test_concurrent_sorts_from_threads():
+    """ctypes releases the GIL: sorts started from several threads at once use
+    private workspaces (_lib.workspace) and cached graphs that stay alive while
+    launched; each result equals the same sort run alone."""
+    import threading
+    g = np.random.default_rng(21)
+    shapes = [(48, 3), (64, 4), (48, 3), (32, 6), (64, 4), (40, 2)]
+    feats = [g.uniform(size=(s * s, d)).astype(np.float32) for s, d in shapes]
+    cfgs = [plas.SortConfig(rng_seed=i, rng_mode="device" if i % 2 else "parity") for i in range(len(shapes))]
+    alone = [plas.sort_grid(f, c) for f, c in zip(feats, cfgs)]
+    out = [None] * len(shapes)
+    errs = []
+
+    def run(i):
+        try:
+            import torch
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for _ in range(3):
+                    out[i] = plas.sort_grid(feats[i], cfgs[i])
+        except Exception as exc:  # surfaced below
+            errs.append(exc)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(shapes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(alone, out):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_reassign_float64_target_matches_numba_promotion():
+    """A float64 target: the reference's numba kernel differences the widened
+    fp32 feature against the fp64 target and sums the squares in fp64
+    (plas.py:134-137); the costs are stored as float32.  Restated here with
+    sequential Python sums (small cases)."""
+    rng = np.random.default_rng(17)
+    for trial in range(60):
+        k = (2, 3, 4)[trial % 3]
+        D = int(rng.integers(1, 9))
+        feat = rng.normal(size=(k, D)).astype(np.float32)
+        target = feat.astype(np.float64) + rng.normal(scale=1e-7, size=(k, D))  # near-ties in fp32
+        cost = np.empty((k, k), dtype=np.float32)
+        for i in range(k):
+            for j in range(k):
+                s = 0.0
+                for d in range(D):
+                    df = float(feat[i, d]) - float(target[j, d])
+                    s += df * df
+                cost[i, j] = np.float32(math.sqrt(s))
+        best, bc = 0, np.inf
+        for p, perm in enumerate(itertools.permutations(range(k))):
+            c = 0.0
+            for i in range(k):
+                c += float(cost[i, perm[i]])
+            if c < bc:
+                bc, best = c, p
+        perm = list(itertools.permutations(range(k)))[best]
+        f = feat.copy()
+        idx = np.arange(k, dtype=np.int64)
+        plas.reassign_block(f, idx, target, np.arange(k), np.arange(k))
+        want = np.empty(k, dtype=np.int64)
+        for i in range(k):
+            want[perm[i]] = i
+        assert idx.tolist() == want.tolist(), (trial, k, D)
+        np.testing.assert_array_equal(f, feat[want])
