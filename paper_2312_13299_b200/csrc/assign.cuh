@@ -696,21 +696,22 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
 }
 
 // Tile-regime pass kernel (small blocks).  A CTA walks blocks b = blockIdx.x,
-// +gridDim.x, ... through a TILE_NST-stage shared-memory ring: while the
-// groups of block b are decided from shared memory, the feature and target
-// rows of the next blocks arrive by bulk copies (cp.async.bulk, one per block
-// row and array, issued by the lanes of warp 0 and counted on the stage's
-// "full" mbarrier), so the staging costs a few instructions per block instead
-// of one per 16 bytes.  Each warp releases a stage on its "empty" mbarrier
-// when it has read it, and the producer refills a stage only after all warps
-// released it: no CTA-wide barrier per block, warps drift apart by up to
-// TILE_NST - 1 blocks.
-// Every block row is contiguous in HBM (ww * S floats), so the copies stream.
-// Element indices are read per group from global memory (only moved cells
-// write them back).  Only moved rows are written back, from registers (rows
-// <= 16 floats) or the staged copy, so in-place swaps need no ordering.  Same
-// decisions as pass_kernel.
-constexpr int TILE_THREADS = 256;
+// +gridDim.x, ... through a TILE_NST-stage shared-memory ring.  A dedicated
+// producer warp (warp 8) streams each block's feature and target rows in with
+// bulk copies (cp.async.bulk, one per block row and array, counted on the
+// stage's "full" mbarrier) as soon as the eight consumer warps have released
+// the stage on its "empty" mbarrier; the consumers decide the block's groups
+// from shared memory.  Staging costs a few producer instructions per block
+// row, no CTA-wide barrier per block, and every block row is contiguous in HBM
+// (ww * S floats), so the copies stream.  Element indices are read per group
+// from global memory (only moved cells write them back).  Only moved rows are
+// written back, from registers (rows <= 16 floats) or the staged copy, so
+// in-place swaps need no ordering.  Same decisions as pass_kernel.
+// Measured at C2 (beta = 16 passes): 42.6 us with warp 0's lanes issuing the
+// copies between their own decisions, 39.6 us with the producer warp; three
+// or four stages (fewer CTAs per SM) 48 / 73 us.
+constexpr int TILE_THREADS = 256;                    // consumer threads (8 warps)
+constexpr int TILE_CTA_THREADS = TILE_THREADS + 32;  // + the producer warp
 constexpr int TILE_WARP_LIST = 128;  // moved-cell staging per warp in the tile kernel
 #ifndef TILE_NST
 #define TILE_NST 2
@@ -769,13 +770,13 @@ __device__ __forceinline__ TileGeom tile_geom(int b, int nbx, unsigned nbx_m, in
 }
 
 template <bool WIDE, bool PARITY>
-__global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : TILE_MINB) tile_pass_kernel(
+__global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_pass_kernel(
     float* __restrict__ feat, int* __restrict__ idx, const float* __restrict__ target, int D, int S,
     const Ctrl* __restrict__ ctrl, const int* __restrict__ sel, long long sel_stride, MoveOut mo,
     int* __restrict__ counters) {
   extern __shared__ __align__(128) float4 smem4[];
   __shared__ PassShared ps;
-  __shared__ int s_list[8 * TILE_WARP_LIST];  // small lists: 3 CTAs per SM fit in shared memory
+  __shared__ int s_list[9 * TILE_WARP_LIST];  // small lists: 3 CTAs per SM fit in shared memory
   __shared__ unsigned long long s_full[TILE_NST], s_empty[TILE_NST];
   if (ctrl->level_done) return;  // an unrolled pass slot after the level ended
   gtrace_mark(ctrl, 0);
@@ -807,33 +808,32 @@ __global__ void __launch_bounds__(TILE_THREADS, WIDE ? 2 : TILE_MINB) tile_pass_
   const int first = b_lo + blockIdx.x;
   const int G = gridDim.x;
 
-  // warp 0: the CTA's it-th block into stage it % TILE_NST once every warp
-  // released that stage's previous block (lane r copies row r of both arrays;
-  // lane 0 first announces the byte count)
-  auto produce = [&](int it) {
-    const int b = first + it * G;
-    if (threadIdx.x < 32 && b < nblocks) {
-      const int st = it % TILE_NST;
-      if (it >= TILE_NST) mbar_wait(&s_empty[st], (unsigned)((it / TILE_NST - 1) & 1));
-      const TileGeom g = tile_geom(b, nbx, nbx_m, nbx_l, nby, fy, fx, beta, ps.seg);
-      const unsigned rowb = (unsigned)(g.ww * S * 4);
-      if (lane == 0) mbar_expect_tx(&s_full[st], 2u * rowb * (unsigned)g.hh);
-      __syncwarp();
-      float* sF = stage_base + st * stage_floats;
-      float* sT = sF + mmax * S;
-      for (int r = lane; r < g.hh; r += 32) {
-        const unsigned go = ((unsigned)(g.y0 + r) * (unsigned)side + (unsigned)g.x0) * (unsigned)S;
-        const unsigned so = (unsigned)(r * g.ww * S);
-        bulk_g2s(sF + so, feat + go, rowb, &s_full[st]);
-        bulk_g2s(sT + so, target + go, rowb, &s_full[st]);
+  int exact = 0;
+  if (threadIdx.x >= TILE_THREADS) {
+    // ---- producer warp: block it of this CTA into stage it % TILE_NST once
+    // the consumers released that stage's previous block (bulk copies are
+    // uniform-datapath instructions, so one lane issues them all)
+    if (lane == 0) {
+      for (int it = 0; first + it * G < nblocks; it++) {
+        const int b = first + it * G;
+        const int st = it % TILE_NST;
+        if (it >= TILE_NST) mbar_wait(&s_empty[st], (unsigned)((it / TILE_NST - 1) & 1));
+        const TileGeom g = tile_geom(b, nbx, nbx_m, nbx_l, nby, fy, fx, beta, ps.seg);
+        const unsigned rowb = (unsigned)(g.ww * S * 4);
+        mbar_expect_tx(&s_full[st], 2u * rowb * (unsigned)g.hh);
+        float* sF = stage_base + st * stage_floats;
+        float* sT = sF + mmax * S;
+        unsigned go = ((unsigned)g.y0 * (unsigned)side + (unsigned)g.x0) * (unsigned)S;
+        const unsigned gstep = (unsigned)side * (unsigned)S, sstep = (unsigned)(g.ww * S);
+        unsigned so = 0u;
+        for (int r = 0; r < g.hh; r++, go += gstep, so += sstep) {
+          bulk_g2s(sF + so, feat + go, rowb, &s_full[st]);
+          bulk_g2s(sT + so, target + go, rowb, &s_full[st]);
+        }
       }
     }
-  };
-
-  int exact = 0;
-  for (int it = 0; it < TILE_NST - 1; it++) produce(it);
+  } else
   for (int it = 0; first + it * G < nblocks; it++) {
-    produce(it + TILE_NST - 1);
     const int b = first + it * G;
     const int st = it % TILE_NST;
     mbar_wait(&s_full[st], (unsigned)((it / TILE_NST) & 1));  // block b's rows have landed

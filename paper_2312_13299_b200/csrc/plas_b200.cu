@@ -607,7 +607,7 @@ int tile_grid_size(int S) {
   raise_smem_limit((const void*)tile_kernel_ptr<true>(S), smem);
   if (!cached[key]) {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel_ptr<false>(S), TILE_THREADS, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel_ptr<false>(S), TILE_CTA_THREADS, smem);
     if (occ <= 0) occ = 1;
     cached[key] = std::min(num_sms() * occ, MAX_PARTS);
   }
@@ -1037,7 +1037,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       if (rg == 0) {
         kp.func = tile_kernel_ptr<false>(S);
         kp.gridDim = dim3(lc.tile_grid);
-        kp.blockDim = dim3(TILE_THREADS);
+        kp.blockDim = dim3(TILE_CTA_THREADS);
         kp.sharedMemBytes = (unsigned)tile_smem_bytes(S);
       } else {
         const PassCfg pc = pass_cfg<false>(S);
@@ -1220,7 +1220,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           cudaError_t le = cudaSuccess;
           if (use_tile(beta, S))
             timed(K_PASS, [&] {
-              le = cudaLaunchKernel(tfn, dim3(lc.tile_grid), dim3(TILE_THREADS), args,
+              le = cudaLaunchKernel(tfn, dim3(lc.tile_grid), dim3(TILE_CTA_THREADS), args,
                                     (size_t)(TILE_NST * tile_stage_bytes(beta, S)), st);
             });
           else
