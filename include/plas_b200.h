@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PLAS_ABI_VERSION 4
+#define PLAS_ABI_VERSION 5
 
 enum plas_status {
   PLAS_OK = 0,
@@ -41,6 +41,9 @@ enum plas_dtype { PLAS_F32 = 0, PLAS_F64 = 1 };
  *         (SeedSequence state); grouping by a keyed bijection per block class;
  *         the whole sort runs as one CUDA graph with no host round trip. */
 enum plas_rng_mode { PLAS_RNG_PARITY = 0, PLAS_RNG_DEVICE = 1 };
+
+/* exchange callback operations of a sharded sort (plas_sort_args.exchange) */
+enum plas_xchg_op { PLAS_XCHG_PASS = 0, PLAS_XCHG_ALLGATHER = 1, PLAS_XCHG_ALLTOALL = 2 };
 
 enum plas_blur_op {
   PLAS_BLUR_SEPARABLE = 0,     /* blur.py:7-10   separable_blur            */
@@ -79,26 +82,40 @@ typedef struct plas_sort_args {
   void* profile;
   /* Multi-GPU sharding (world > 1; 0 or 1 = single GPU).  Every rank runs
    * plas_sort on its own device with identical arguments and keeps a full
-   * replica of the grid; each pass's groups are split into contiguous,
-   * balanced per-rank ranges.  After each pass the library writes this
-   * rank's (fp64 distance change, moved-cell count) to xchg_part[0..1] and
-   * its (cell, element) int32 pairs to xchg_send, then calls
-   * exchange(exchange_ctx), which must all-gather xchg_part into
-   * xchg_part_all[2 * world] (rank order) and the first m pairs of every
-   * rank's xchg_send into xchg_recv (rank r's pairs at r * m), with m >= the
-   * largest moved-cell count, and return m (< 0 = error).  Collectives must be
-   * ordered after the work already enqueued on `stream` and before work
-   * enqueued after the call returns (torch.distributed over NCCL does this).
-   * Every rank then applies the others' updates and runs the identical
-   * controller on the partials summed in rank order. */
+   * replica of the grid (features and element indices).  Per level: when
+   * beta * world <= side (banded levels) rank r owns rows [Y_r, Y_r+1),
+   * Y_r = side * r / world, processes the pass's block rows that start there
+   * (row bands aligned to the pass's block tiling) and computes the target
+   * only on [Y_r, Y_r+1 + beta); on the FFT blur tier the axis-0 transforms
+   * are split by columns and exchanged by one all-to-all.  Other levels split
+   * each pass's groups evenly and blur the whole grid.  The level-start
+   * distance sum and every pass's distance change are exchanged as exact
+   * 128-bit fixed-point partials, so the result is bit-identical to one GPU.
+   * The library calls exchange(exchange_ctx, op, a, b, sizes):
+   *   PLAS_XCHG_PASS: after each pass the library wrote this rank's
+   *     (int128 distance change as two 64-bit words, moved-cell count, 0) to
+   *     xchg_part[0..3] and its (cell, element) int32 pairs to xchg_send; the
+   *     callback all-gathers xchg_part into xchg_part_all[4 * world] (rank
+   *     order) and the first m pairs of every rank's xchg_send into
+   *     xchg_recv (rank r's pairs at r * m), m >= the largest moved-cell count
+   *     (xchg_part_all[4 r + 2]), and returns m.
+   *   PLAS_XCHG_ALLGATHER: in-place all-gather of a bytes per rank inside the
+   *     workspace: rank r's piece is at ws + b + r * a; returns 0.
+   *   PLAS_XCHG_ALLTOALL: workspace byte offsets a (send) and b (recv); host
+   *     sizes[q] = bytes sent to rank q (send segments in rank order),
+   *     sizes[world + q] = bytes received from rank q (recv segments in rank
+   *     order); returns 0.
+   * Negative returns abort the sort.  Collectives must be ordered after the
+   * work already enqueued on `stream` and before work enqueued after the call
+   * returns (torch.distributed over NCCL on the current stream does this). */
   int rank;
   int world;
-  int (*exchange)(void* exchange_ctx);
+  int (*exchange)(void* exchange_ctx, int op, int64_t a, int64_t b, const int64_t* sizes);
   void* exchange_ctx;
   void* xchg_send;        /* device int32 [2 * n] */
   void* xchg_recv;        /* device int32 [2 * n * world] */
-  double* xchg_part;      /* device [2] */
-  double* xchg_part_all;  /* device [2 * world] */
+  double* xchg_part;      /* device [4] */
+  double* xchg_part_all;  /* device [4 * world] */
 } plas_sort_args;
 
 /* Per-kernel device time (CUDA events, ms) summed over all launches. */
@@ -124,6 +141,7 @@ typedef struct plas_sort_result {
   double gpu_ms;                 /* device time from init gather to perm ready */
   int64_t cells_moved;           /* elements that changed cell, summed over passes */
   int64_t exact_warps;           /* warps whose decision needed the exact fp64 tier */
+  int64_t banded_levels;         /* sharded sorts: levels run in row bands (the rest replicated) */
 } plas_sort_result;
 
 int plas_abi_version(void);

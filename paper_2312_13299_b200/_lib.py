@@ -30,8 +30,12 @@ PLAS_BLUR_SEPARABLE, PLAS_BLUR_RENORMALIZED, PLAS_BLUR_BORDER_WEIGHT = 0, 1, 2
 P = ctypes.c_void_p
 i32, i64, u64, f64, sz = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_size_t
 
-# int (*exchange)(void* ctx) of plas_sort_args (multi-GPU sharding)
-EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+# int (*exchange)(void* ctx, int op, int64_t a, int64_t b, const int64_t* sizes) of
+# plas_sort_args (multi-GPU sharding)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                               ctypes.POINTER(ctypes.c_int64))
+PLAS_XCHG_PASS, PLAS_XCHG_ALLGATHER, PLAS_XCHG_ALLTOALL = 0, 1, 2
+XPART = 4  # doubles per rank in the pass exchange (int128 change as 2 words, moved count, pad)
 
 
 class SortArgs(ctypes.Structure):
@@ -56,7 +60,7 @@ class SortResult(ctypes.Structure):
     _fields_ = [
         ("perm", P), ("initial_vad", f64), ("final_vad", f64), ("reorders", i64),
         ("levels_done", i32), ("level_counts", P), ("trace", P), ("trace_len", i64),
-        ("gpu_ms", f64), ("cells_moved", i64), ("exact_warps", i64),
+        ("gpu_ms", f64), ("cells_moved", i64), ("exact_warps", i64), ("banded_levels", i64),
     ]
 
 

@@ -45,7 +45,15 @@ __device__ __forceinline__ void fb_append(bool need, int entry, int* __restrict_
 struct PadGeom {
   int H, W, C, S;
   int pad;        // zero elements before/after every line (>= hmax + BPAD_R)
+  // output rows [r0, r1) the level needs (axis-0 outputs of the direct and
+  // tile tiers, axis-1 lines of every tier) and the columns [c0, c1) of the
+  // FFT tier's axis-0 lines: the whole grid on one GPU, a rank's row band /
+  // column share in a sharded sort
+  int r0, r1, c0, c1;
 };
+__host__ __device__ inline PadGeom make_pad_geom(int H, int W, int C, int S, int pad) {
+  return PadGeom{H, W, C, S, pad, 0, H, 0, W};
+}
 
 // AXIS 0: in = feat interior (row stride W*S, PAD zero rows above/below),
 //         out = tmp interior (row stride (W + 2 pad) * S).
@@ -72,13 +80,16 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
   const long long WSP = (long long)(W + 2 * pg.pad) * S;  // tmp row stride
   const long long in_stride = AXIS == 0 ? WS : (long long)S;
   const long long out_stride = AXIS == 0 ? WSP : (long long)S;
-  const int nchunks = (n + R - 1) / R;
+  // axis 0: the chunks of R outputs covering rows [r0, r1); axis 1: every chunk of lines r0 .. r1-1
+  const int chunk0 = AXIS == 0 ? pg.r0 / R : 0;
+  const int nchunks = AXIS == 0 ? (pg.r1 + R - 1) / R - chunk0 : (n + R - 1) / R;
+  const int nlines = pg.r1 - pg.r0;
   const double w0 = __ldg(w);
   const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
   // 32-bit index math with multiply-shift division (every count < 2^31)
   const unsigned nstrips = (unsigned)((WS + 31) / 32);
   const unsigned ncg = (unsigned)((nchunks + 7) / 8);
-  const unsigned total = AXIS == 0 ? nstrips * ncg * 256u : (unsigned)S * (unsigned)nchunks * (unsigned)H;
+  const unsigned total = AXIS == 0 ? nstrips * ncg * 256u : (unsigned)S * (unsigned)nchunks * (unsigned)nlines;
   unsigned ns_m, s_m, nc_m;
   int ns_l, s_l, nc_l;
   make_fastdiv(nstrips, &ns_m, &ns_l);
@@ -97,6 +108,7 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
       chunk = (int)(q * 8 + (lt >> 5));
       const unsigned f = strip * 32 + (lt & 31);
       if ((long long)f >= WS || chunk >= nchunks) continue;
+      chunk += chunk0;
       const unsigned cell = fastdiv(f, s_m, s_l);
       c = (int)(f - cell * (unsigned)S);
       in_base = f;
@@ -105,8 +117,9 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
     } else {
       const unsigned rest = fastdiv(t, s_m, s_l);
       c = (int)(t - rest * (unsigned)S);
-      const unsigned y = fastdiv(rest, nc_m, nc_l);
-      chunk = (int)(rest - y * (unsigned)nchunks);
+      const unsigned yl = fastdiv(rest, nc_m, nc_l);
+      chunk = (int)(rest - yl * (unsigned)nchunks);
+      const unsigned y = yl + (unsigned)pg.r0;
       in_base = (long long)y * WSP + c;
       out_base = (long long)y * WS + c;
       cellbase = (long long)y * W;
@@ -196,15 +209,15 @@ __global__ void __launch_bounds__(32 * FB_WARPS) blur_pad_fallback_kernel(
   const double* w;
   lvl.get(&h, &w);
   const int count = *(volatile int*)fb;
-  const int H = pg.H, W = pg.W, C = pg.C, S = pg.S;
+  const int W = pg.W, C = pg.C, S = pg.S;
   const long long WS = (long long)W * S;
   const long long WSP = (long long)(W + 2 * pg.pad) * S;
   const bool all = count > fb_cap;
-  const long long total = all ? (long long)H * WS : count;
+  const long long total = all ? (long long)(pg.r1 - pg.r0) * WS : count;  // overflow: every element of rows [r0, r1)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* tm = terms[wid];
   for (long long e = (long long)blockIdx.x * FB_WARPS + wid; e < total; e += (long long)gridDim.x * FB_WARPS) {
-    const long long o = all ? e : (long long)fb[FB_HEADER + e];
+    const long long o = all ? (long long)pg.r0 * WS + e : (long long)fb[FB_HEADER + e];
     const int c = (int)(o % S);
     if (c >= C) continue;  // warp-uniform
     const long long y = o / WS;
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(TB_THREADS) blur_tile_kernel(const float* __re
   const int NI = TB_T + 2 * h;   // staged side
   double2* in = tsm2;            // [NI][NI]
   double2* tmp = tsm2 + NI * NI;  // [TB_T][NI] (fp32-rounded axis-0 values)
-  const int y0 = blockIdx.y * TB_T, x0 = blockIdx.x * TB_T;
+  const int y0 = (blockIdx.y + pg.r0 / TB_T) * TB_T, x0 = blockIdx.x * TB_T;  // tile rows covering [r0, r1)
   const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned ni_m;  // multiply-shift division by the staged side (no integer division per element)

@@ -461,8 +461,10 @@ __global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blo
   const long long WS = (long long)W * S;
   const long long WSP = (long long)(W + 2 * pg.pad) * S;
   const int cpairs = (C + 1) >> 1;
-  const long long line = blockIdx.x / cpairs;
-  const int c = (int)(blockIdx.x - line * cpairs) * 2;
+  // lines: columns [c0, c1) (axis 0) or rows [r0, r1) (axis 1), grid = lines x channel pairs
+  const long long lline = blockIdx.x / cpairs;
+  const long long line = lline + (AXIS == 0 ? pg.c0 : pg.r0);
+  const int c = (int)(blockIdx.x - lline * cpairs) * 2;
   const bool has_b = c + 1 < C;
   // ---- forward FFT pass 0 straight from global memory (+ raw copy, ||z||^2, max|x|)
   {

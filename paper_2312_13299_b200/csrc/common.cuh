@@ -73,6 +73,12 @@ struct Ctrl {
   unsigned lv_cap_m, lv_seg_m[2];
   int lv_cap_l, lv_seg_l[2], lv_seg_base, lv_cap;
   int gen_pass;                    // pass whose grouping tables gen_tables_kernel builds
+  // multi-GPU, per level (set_level_shard_kernel): banded = this level's
+  // passes split by block rows whose first row lies in [own_lo, own_hi) (the
+  // rank's share of rows); the rank keeps target / distance cache valid on
+  // rows [band_lo, band_hi) (its blocks' rows for any offset of the level)
+  int banded;
+  int own_lo, own_hi, band_lo, band_hi;
   unsigned long long* gtrace;      // diagnostics (PLAS_GTRACE): per pass ~K3 start, K3 end, ~stats start, stats end
 };
 
@@ -340,6 +346,20 @@ __host__ __device__ __forceinline__ void set_pass_geometry_base(Ctrl* c, int dy,
     c->g_hi = c->total_groups;
     c->b_lo = 0;
     c->b_hi = (int)nb;
+  } else if (c->banded) {
+    // row bands aligned to this pass's block tiling: the block rows whose
+    // first row y0(by) lies in [own_lo, own_hi) (y0(0) = 0, y0(by) = first_y +
+    // (by - 1) beta), so a rank's cells are rows [own_lo, own_hi + beta)
+    auto first_by = [&](int Y) {
+      if (Y <= 0) return 0;
+      int by = Y <= c->first_y ? 1 : 1 + (Y - c->first_y + c->beta - 1) / c->beta;
+      return by < c->nby ? by : c->nby;
+    };
+    const int by_lo = first_by(c->own_lo), by_hi = c->own_hi >= c->side ? c->nby : first_by(c->own_hi);
+    c->b_lo = by_lo * c->nbx;
+    c->b_hi = by_hi * c->nbx;
+    c->g_lo = (long long)c->b_lo * c->cap;
+    c->g_hi = (long long)c->b_hi * c->cap;
   } else {
     c->g_lo = c->total_groups * c->rank / W;
     c->g_hi = c->total_groups * (c->rank + 1) / W;

@@ -420,8 +420,17 @@ __device__ __forceinline__ __int128 shfl_xor_i128(__int128 v, int m) {
 // into a 128-bit accumulator acc[0..1] (low word, then high word plus the
 // carry its own low-word add produced -- exact modulo 2^128 in any order); the
 // last CTA reads it and clears it for the next pass (zeroed at sort start).
+__device__ __forceinline__ void store_i128(double* dst, __int128 v) {  // raw bits in two fp64 slots
+  reinterpret_cast<unsigned long long*>(dst)[0] = (unsigned long long)v;
+  reinterpret_cast<unsigned long long*>(dst)[1] = (unsigned long long)((unsigned __int128)v >> 64);
+}
+__device__ __forceinline__ __int128 load_i128(const double* src) {
+  const unsigned long long lo = reinterpret_cast<const unsigned long long*>(src)[0];
+  const unsigned long long hi = reinterpret_cast<const unsigned long long*>(src)[1];
+  return (__int128)(((unsigned __int128)hi << 64) | (unsigned __int128)lo);
+}
 __device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, unsigned long long* acc, int* done, double* total,
-                                                   int* ticket) {
+                                                   int* ticket, __int128* raw = nullptr) {
   __shared__ __int128 sq[32];
   __shared__ int s_last, s_ticket;
 #pragma unroll
@@ -449,7 +458,9 @@ __device__ __forceinline__ bool last_cta_reduce_fx(__int128 v, unsigned long lon
     const unsigned long long lo = va[0], hi = va[1];
     va[0] = 0ull;
     va[1] = 0ull;
-    *total = fx64_to_double((__int128)(((unsigned __int128)hi << 64) | (unsigned __int128)lo));
+    const __int128 q = (__int128)(((unsigned __int128)hi << 64) | (unsigned __int128)lo);
+    *total = fx64_to_double(q);
+    if (raw) *raw = q;
     *done = 0;
   }
   __syncthreads();
@@ -467,26 +478,56 @@ __device__ __forceinline__ void level_end_work(Ctrl* c, Sched s, unsigned long l
 
 // Level start (plas.py:256-258): fp64 distance of every cell to the fresh
 // target into the cache, sum -> previous, trace, open the pass loop.
+// The sum is taken in 128-bit fixed point (fx64 per cell, exact integer adds),
+// so it does not depend on how cells are split across CTAs or GPUs: a sharded
+// sort sums each rank's own rows [own_lo, own_hi) and adds the ranks'
+// integers (level_start_shard_kernel), bit-identical to one GPU.  The cache
+// covers the rows whose target this rank holds, [band_lo, band_hi).
+// Sharded (world > 1): the last CTA only publishes the raw 128-bit partial to
+// xpart[0..1]; level_start_shard_kernel runs the controller after the exchange.
+__device__ __forceinline__ void level_start_control(Ctrl* c, Sched s, double tot, long long n,
+                                                    unsigned long long inner, unsigned long long outer, bool* go) {
+  c->dist_sum = tot;
+  c->previous = tot / (double)n;
+  if (c->trace_pos >= c->trace_cap) {
+    c->status = 1;
+    c->level_done = 1;
+    set_cond(inner, 0);
+    if (outer) level_end_work(c, s, outer);
+  } else {
+    s.trace[c->trace_pos++] = c->previous;
+    *go = true;
+  }
+}
+
 __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
     Ctrl* c, Sched s, const float* __restrict__ feat, const float* __restrict__ target,
-    double* __restrict__ dcache, long long n, int D, int S, double* partials, int* done,
-    unsigned long long inner, unsigned long long outer, int* tab, long long tab_stride) {
-  __shared__ double sh[32];
+    double* __restrict__ dcache, long long n, int D, int S, double* acc, int* done,
+    unsigned long long inner, unsigned long long outer, int* tab, long long tab_stride, double* xpart) {
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
-  double sum = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+  const int side = c->side;
+  const long long i0 = (long long)c->band_lo * side, i1 = (long long)c->band_hi * side;
+  const long long o0 = (long long)c->own_lo * side, o1 = (long long)c->own_hi * side;
+  __int128 sum = 0;
+  for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < i1;
        i += (long long)gridDim.x * blockDim.x) {
     const double d = sqrt(S == 16 ? cell_dist2_s16(feat + i * 16, target + i * 16, D)
                                    : cell_dist2(feat + i * S, target + i * S, D, S));
     dcache[i] = d;
-    sum += d;
+    if (i >= o0 && i < o1) sum += fx64(d);
   }
   const bool gen = tab && c->rng_mode == 1;
   int ticket = 0;
-  if (!last_cta_reduce(sum, partials, done, &s_tot, sh, &ticket)) {
+  __int128 raw = 0;
+  if (!last_cta_reduce_fx(sum, reinterpret_cast<unsigned long long*>(acc), done, &s_tot, &ticket, &raw)) {
     // pass 0's tables, built by the other CTAs (ticket order) while the last one finishes
     if (gen) gen_class_tables(c, 0, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
+    return;
+  }
+  if (c->world > 1) {
+    if (threadIdx.x == 0) store_i128(xpart, raw);
+    if (gen && gridDim.x == 1) gen_class_tables(c, 0, tab, tab_stride, 0, 1);
     return;
   }
   __shared__ Ctrl sc;
@@ -494,20 +535,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
   ctrl_to_smem(&sc, cg);
   c = &sc;
   bool go = false;
-  if (threadIdx.x == 0) {
-    const double tot = s_tot;
-    c->dist_sum = tot;
-    c->previous = tot / (double)n;
-    if (c->trace_pos >= c->trace_cap) {
-      c->status = 1;
-      c->level_done = 1;
-      set_cond(inner, 0);
-      if (outer) level_end_work(c, s, outer);
-    } else {
-      s.trace[c->trace_pos++] = c->previous;
-      go = true;
-    }
-  }
+  if (threadIdx.x == 0) level_start_control(c, s, s_tot, n, inner, outer, &go);
   go = __syncthreads_or(go);
   if (go) {
     if (c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
@@ -669,7 +697,8 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   // the controller's writes to Ctrl leave the fields read here unchanged)
   const bool gen = tab && c->rng_mode == 1;
   int ticket = 0;
-  if (!last_cta_reduce_fx(sum, reinterpret_cast<unsigned long long*>(partials), done, &s_tot, &ticket)) {
+  __int128 raw = 0;
+  if (!last_cta_reduce_fx(sum, reinterpret_cast<unsigned long long*>(partials), done, &s_tot, &ticket, &raw)) {
     if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
     if (c->gtrace) {
       __syncthreads();
@@ -680,8 +709,9 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   gtrace_mark(c, 4);  // the last CTA has its ticket
   if (c->world > 1) {
     if (threadIdx.x == 0) {
-      xpart[0] = s_tot;
-      xpart[1] = (double)count;
+      store_i128(xpart, raw);  // exact partial: the ranks' integers add up to the 1-GPU total
+      xpart[2] = (double)count;
+      xpart[3] = 0.0;
     }
     return;
   }
@@ -715,17 +745,20 @@ __global__ void shard_pack_kernel(const int* __restrict__ list, const int* __res
 }
 
 // Every other rank's updates: element idx now sits in cell -> its f32 row
-// (orig32, the working copy in element order), the index and the cached
-// distance to the cell's target.  recv holds world segments of `stride`
-// pairs; counts come with the exchanged partials (xall[2 s + 1]).
+// (orig32, the working copy in element order) and the index; the cached
+// distance to the cell's target where this rank holds the target (rows
+// [band_lo, band_hi)).  recv holds world segments of `stride` pairs; counts
+// come with the exchanged partials (xall[XPART * r + 2]).
+constexpr int XPART = 4;  // doubles per rank in the pass exchange: int128 change (2 slots), count, pad
 __global__ void shard_apply_kernel(const int2* __restrict__ recv, long long stride, const double* __restrict__ xall,
                                    int world, int rank, const float* __restrict__ orig32, float* __restrict__ feat,
                                    int* __restrict__ idx, const float* __restrict__ target,
-                                   double* __restrict__ dcache, int D, int S) {
+                                   double* __restrict__ dcache, int D, int S, const Ctrl* __restrict__ ctrl) {
   const int nch = S >> 2;
+  const long long c0 = (long long)ctrl->band_lo * ctrl->side, c1 = (long long)ctrl->band_hi * ctrl->side;
   for (int r = 0; r < world; r++) {
     if (r == rank) continue;
-    const long long cnt = (long long)xall[2 * r + 1];
+    const long long cnt = (long long)xall[XPART * r + 2];
     const int2* seg = recv + (long long)r * stride;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cnt;
          e += (long long)gridDim.x * blockDim.x) {
@@ -734,31 +767,92 @@ __global__ void shard_apply_kernel(const int2* __restrict__ recv, long long stri
       for (int c = 0; c < nch; c++)
         reinterpret_cast<float4*>(feat + cell * S)[c] = reinterpret_cast<const float4*>(orig32 + el * S)[c];
       idx[cell] = (int)el;
-      dcache[cell] = sqrt(cell_dist2(feat + cell * S, target + cell * S, D, S));
+      if (cell >= c0 && cell < c1) dcache[cell] = sqrt(cell_dist2(feat + cell * S, target + cell * S, D, S));
     }
   }
 }
 
-// The controller on the exchanged partials, summed in rank order (identical on
-// every rank), then the next pass's draws and geometry.
+// The controller on the exchanged partials: the ranks' 128-bit changes added
+// exactly (any order gives the 1-GPU total), then the next pass's draws and
+// geometry -- identical on every rank.
 __global__ void __launch_bounds__(RED_THREADS) shard_control_kernel(Ctrl* c, Sched s, const double* __restrict__ xall,
                                                                     int world, int* counters, long long n) {
   __shared__ unsigned long long s_gkey;
   bool more = false;
   if (threadIdx.x == 0) {
-    double tot = 0.0;
+    __int128 tot = 0;
     long long moved = 0;
     for (int r = 0; r < world; r++) {
-      tot += xall[2 * r];
-      moved += (long long)xall[2 * r + 1];
+      tot += load_i128(xall + XPART * r);
+      moved += (long long)xall[XPART * r + 2];
     }
     counters[0] += (int)moved;
     counters[2] = 0;
-    more = controller_step(c, s, tot, n, 0ull);
+    more = controller_step(c, s, fx64_to_double(tot), n, 0ull);
   }
   more = __syncthreads_or(more);
   if (!more || c->rng_mode != 1) return;
   prepare_device_pass_cta(c, &s_gkey);
+}
+
+// Sharded level start: the ranks' 128-bit distance partials (exchanged,
+// XPART doubles per rank) added exactly -> the level-start controller
+// (previous, trace), then the first pass's draws and geometry.
+__global__ void __launch_bounds__(RED_THREADS) level_start_shard_kernel(Ctrl* c, Sched s, const double* __restrict__ xall,
+                                                                        int world, long long n) {
+  __shared__ unsigned long long s_gkey;
+  bool go = false;
+  if (threadIdx.x == 0) {
+    __int128 tot = 0;
+    for (int r = 0; r < world; r++) tot += load_i128(xall + XPART * r);
+    level_start_control(c, s, fx64_to_double(tot), n, 0ull, 0ull, &go);
+  }
+  go = __syncthreads_or(go);
+  if (go && c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
+}
+
+// This level's sharding (host-stepped multi-GPU loop, before the blur).
+__global__ void set_level_shard_kernel(Ctrl* c, int banded, int own_lo, int own_hi, int band_lo, int band_hi) {
+  if (threadIdx.x) return;
+  c->banded = banded;
+  c->own_lo = own_lo;
+  c->own_hi = own_hi;
+  c->band_lo = band_lo;
+  c->band_hi = band_hi;
+}
+
+// FFT-tier axis-0 exchange of a banded level: this rank computed the axis-0
+// output (tmp) of columns [c0, c1) on every row; rank q needs rows
+// [lo[q], hi[q]) of every column.  pack: segment q of `buf` = tmp rows
+// [lo[q], hi[q]) x columns [c0, c1) (row-major); unpack: segment j = rows
+// [lo[rank], hi[rank]) x columns [cs[j], cs[j + 1]) from rank j.  Offsets
+// in floats; WSP = tmp row stride (floats), S = floats per cell.
+__global__ void band_pack_kernel(const float* __restrict__ tmp, float* __restrict__ buf, const int* __restrict__ lo,
+                                 const int* __restrict__ hi, int world, int c0, int c1, long long WSP, int S) {
+  const int wc = (c1 - c0) * S;
+  long long off = 0;
+  for (int q = 0; q < world; q++) {
+    const long long cnt = (long long)(hi[q] - lo[q]) * wc;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cnt; e += (long long)gridDim.x * blockDim.x) {
+      const long long r = e / wc, k = e - r * wc;
+      buf[off + e] = tmp[(lo[q] + r) * WSP + (long long)c0 * S + k];
+    }
+    off += cnt;
+  }
+}
+__global__ void band_unpack_kernel(float* __restrict__ tmp, const float* __restrict__ buf, int lo, int hi,
+                                   const int* __restrict__ cs, int world, int rank, long long WSP, int S) {
+  long long off = 0;
+  for (int j = 0; j < world; j++) {
+    const int wc = (cs[j + 1] - cs[j]) * S;
+    const long long cnt = (long long)(hi - lo) * wc;
+    if (j != rank)
+      for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < cnt; e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e / wc, k = e - r * wc;
+        tmp[(lo + r) * WSP + (long long)cs[j] * S + k] = buf[off + e];
+      }
+    off += cnt;
+  }
 }
 
 // level bookkeeping (plas.py:273-274); radius decay is the schedule table

@@ -204,6 +204,9 @@ struct SortWs {
   int* list;      // moved-cell list of the current pass
   double* spart;  // statistic-kernel partials
   float* orig32;      // sharding: f32 features in element order
+  float *xsend, *xrecv;  // sharding: FFT-tier axis-0 band exchange (all-to-all) buffers
+  double* lvl_part;      // sharding: level-start partials, XPART doubles per rank (all-gathered in place)
+  int* bands;            // sharding: per level [lo[world], hi[world], cs[world + 1]] for the pack kernels
   // FFT tier: up to FFT_PLANS lengths (the shortest that fits each level's h)
   int fft_count;                   // number of lengths
   int fft_codes[4];                // length codes, increasing length
@@ -393,6 +396,14 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->list = c.take<int>((size_t)std::max(list_cap, 1LL));
   w->spart = c.take<double>(MAX_PARTS + 2);  // [MAX_PARTS, +2): the pass statistic's 128-bit accumulator
   w->orig32 = world > 1 ? c.take<float>((size_t)n * S) : nullptr;
+  // banded FFT levels: a rank sends its columns of every rank's band (<= 2 side
+  // rows in total: bands are side / world + beta <= 2 side / world rows) and
+  // receives its band of every column
+  const size_t xfl = world > 1 ? (size_t)n * S * 2 / world + (size_t)side * S : 1;
+  w->xsend = c.take<float>(xfl);
+  w->xrecv = c.take<float>(xfl);
+  w->lvl_part = c.take<double>((size_t)XPART * std::max(world, 1));
+  w->bands = c.take<int>((size_t)3 * std::max(world, 1) + 1);
   fft_plan_codes(side, row_stride(dim), &w->fft_count, w->fft_codes);
   w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
   for (int i = 0; i < 4; i++)
@@ -754,6 +765,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.tile_blur_hmax = tile_blur_hmax(S);
   hc.rank = world > 1 ? a->rank : 0;
   hc.world = world;
+  hc.banded = 0;  // whole grid (set per level by set_level_shard_kernel when world > 1)
+  hc.own_lo = hc.band_lo = 0;
+  hc.own_hi = hc.band_hi = side;
   hc.pdraw = nullptr;
   hc.prec = nullptr;
   hc.pdraw_level = -1;
@@ -829,7 +843,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   lc.blur_grid = grid_for((long long)side * S * ((side + BPAD_R - 1) / BPAD_R), 256, 8);
   lc.den_grid = std::min(side, num_sms() * 8);  // border_weight32_kernel: rows per CTA
   lc.fb_grid = num_sms() * 2;
-  lc.pg = PadGeom{side, side, D, S, w.pad};
+  lc.pg = make_pad_geom(side, side, D, S, w.pad);
   lc.rows_grid = grid_for(side, 128, 1);
   lc.dist_grid = grid_for(n, RED_THREADS, 4);
   lc.vad_grid = grid_for(n * D, RED_THREADS, 4);
@@ -891,6 +905,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   MoveOut ml{w.list, counters + 2};
   int* done = w.flags + 6;      // last-CTA ticket of the statistic kernels
   if (htrace) fprintf(stderr, "host: graph/loop start at %.3f ms\n", hms());
+  long long banded_levels = 0;
   if (mode == PLAS_RNG_DEVICE && !a->profile && world == 1) {
     // ------------------------------------------------------------ graph
     // outer WHILE (levels): level_begin, border weight, blur axis 0, blur axis 1,
@@ -1022,7 +1037,8 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaGraphNode_t ls, wl, kn, sn;
       CK(add_kernel(&ls, rb, nullptr, 0, level_stats_kernel, dim3(lc.dist_grid), dim3(RED_THREADS),
                     w.ctrl, lc.sched, (const float*)w.feat, (const float*)w.target, w.dcache, n, D, S,
-                    w.spart, done, (unsigned long long)loop_h, (unsigned long long)outer_h, w.sel, w.sel_stride));
+                    w.spart + MAX_PARTS, done, (unsigned long long)loop_h, (unsigned long long)outer_h, w.sel,
+                    w.sel_stride, (double*)nullptr));
       cudaGraph_t lb;
       CK(add_while(&wl, rb, &ls, 1, loop_h, &lb));
       float* feat = w.feat;
@@ -1123,6 +1139,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     };
     int pp = 0;
     const PassCfg kpc = parity ? pass_cfg<true>(S) : pass_cfg<false>(S);
+    banded_levels = 0;
     void* tfn = parity ? tile_kernel_ptr<true>(S) : tile_kernel_ptr<false>(S);
     for (int lv = 0; lv < L; lv++) {
       const int beta = sch.betas[lv];
@@ -1133,66 +1150,142 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       });
       const int mode = hmode[lv];
       const bool use_fft = mode < NPL;
+      // ---- sharding of this level (world > 1).  Banded
+      // (beta * world <= side): rank r owns rows [Y_r, Y_r+1), Y_r = side r /
+      // world, takes the pass's block rows starting there and needs the target
+      // on [Y_r, Y_r+1 + beta); otherwise (top levels) every rank holds the
+      // whole target and the groups are split evenly.
+      PadGeom pgl = lc.pg;  // this rank's output rows [r0, r1) / FFT columns [c0, c1)
+      bool fft_split = false;
+      std::vector<int> blo(world), bhi(world), bcs(world + 1);
+      if (world > 1) {
+        const bool banded = (long long)beta * world <= side;
+        banded_levels += banded ? 1 : 0;
+        for (int q = 0; q <= world; q++) bcs[q] = (int)((long long)side * q / world);
+        for (int q = 0; q < world; q++) {
+          blo[q] = banded ? bcs[q] : 0;
+          bhi[q] = banded ? std::min(side, bcs[q + 1] + beta) : side;
+        }
+        const int r = a->rank;
+        set_level_shard_kernel<<<1, 32, 0, st>>>(w.ctrl, banded ? 1 : 0, bcs[r], bcs[r + 1], blo[r], bhi[r]);
+        pgl.r0 = blo[r];
+        pgl.r1 = bhi[r];
+        fft_split = banded && use_fft;
+        if (fft_split) {
+          std::vector<int> hb(3 * world + 1);
+          for (int q = 0; q < world; q++) hb[q] = blo[q], hb[world + q] = bhi[q];
+          for (int q = 0; q <= world; q++) hb[2 * world + q] = bcs[q];
+          CK(cudaMemcpyAsync(w.bands, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice, st));
+          CK(cudaStreamSynchronize(st));  // hb is pageable and local
+        }
+      }
       timed(K_BORDER, [&] {
         border_rows_kernel<<<lc.rows_grid, 128, 0, st>>>(w.rowweight, side, lc.lvl);
         border_weight32_kernel<<<lc.den_grid, 256, 0, st>>>(w.rowweight, w.rowweight, w.den32, side, side, lc.lvl);
       });
+      const int cpairs = (D + 1) / 2;
       if (use_fft) {
         timed(K_BLUR0, [&] {
           fft_spectrum_kernel<<<std::max(1, fplans[mode].L / 128), 128, 0, st>>>(lc.lvl, fplans[mode]);
+          // axis 0: every column (one GPU, replicated levels) or this rank's
+          // columns [c0, c1) on every row (banded levels, exchanged below)
+          PadGeom pg0 = lc.pg;
+          if (fft_split) {
+            pg0.c0 = bcs[a->rank];
+            pg0.c1 = bcs[a->rank + 1];
+          }
           {
             const float* in0 = w.feat;
             float* out0 = w.tmp;
             const float* dnull = nullptr;
-            PadGeom pg = lc.pg;
             BlurLevelRef lv = lc.lvl;
             FftPlan pl = fplans[mode];
             int cap = w.fb_cap;
-            void* a0[] = {&in0, &out0, &pg, &lv, &pl, &dnull, &w.fb0, &cap, &w.fb1};
-            cudaLaunchKernel(fft0s[mode], dim3(fft_grid), dim3(fft_nthreads[mode]), a0, fft_smems[mode], st);
+            void* a0[] = {&in0, &out0, &pg0, &lv, &pl, &dnull, &w.fb0, &cap, &w.fb1};
+            cudaLaunchKernel(fft0s[mode], dim3((pg0.c1 - pg0.c0) * cpairs), dim3(fft_nthreads[mode]), a0,
+                             fft_smems[mode], st);
           }
-          blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
+          blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, pg0, lc.lvl, nullptr, w.fb0,
                                                                      w.fb_cap);
         });
+        if (fft_split) {
+          // every rank's band rows of this rank's columns out, this rank's band
+          // of every other rank's columns in (one all-to-all)
+          const int r = a->rank;
+          const long long WSP = (long long)(side + 2 * w.pad) * S;
+          const int* dlo = w.bands;
+          const int* dhi = w.bands + world;
+          const int* dcs = w.bands + 2 * world;
+          band_pack_kernel<<<num_sms() * 4, 256, 0, st>>>(w.tmp, w.xsend, dlo, dhi, world, bcs[r], bcs[r + 1], WSP,
+                                                           S);
+          CKL();
+          std::vector<int64_t> sizes(2 * world);
+          for (int q = 0; q < world; q++) {
+            sizes[q] = (int64_t)(bhi[q] - blo[q]) * (bcs[r + 1] - bcs[r]) * S * 4;
+            sizes[world + q] = (int64_t)(bhi[r] - blo[r]) * (bcs[q + 1] - bcs[q]) * S * 4;
+          }
+          const int xr = a->exchange(a->exchange_ctx, PLAS_XCHG_ALLTOALL, (int64_t)((char*)w.xsend - (char*)wsp),
+                                     (int64_t)((char*)w.xrecv - (char*)wsp), sizes.data());
+          if (xr < 0) {
+            cleanup();
+            return fail(PLAS_ERR_CUDA, "exchange callback failed (band all-to-all)");
+          }
+          band_unpack_kernel<<<num_sms() * 4, 256, 0, st>>>(w.tmp, w.xrecv, blo[r], bhi[r], dcs, world, r, WSP, S);
+          CKL();
+        }
         timed(K_BLUR1, [&] {
           {
             const float* in1 = w.tmp;
             float* out1 = w.target;
             const float* den = w.den32;
-            PadGeom pg = lc.pg;
+            PadGeom pg = pgl;
             BlurLevelRef lv = lc.lvl;
             FftPlan pl = fplans[mode];
             int cap = w.fb_cap;
             void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &w.fb1, &cap, &w.fb0};
-            cudaLaunchKernel(fft1s[mode], dim3(fft_grid), dim3(fft_nthreads[mode]), a1, fft_smems[mode], st);
+            cudaLaunchKernel(fft1s[mode], dim3((pgl.r1 - pgl.r0) * cpairs), dim3(fft_nthreads[mode]), a1,
+                             fft_smems[mode], st);
           }
-          blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+          blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1,
                                                                      w.fb_cap);
         });
       } else if (mode == NPL) {
         timed(K_BLUR0, [&] {
-          blur_tile_kernel<<<lc.tb_grid, TB_THREADS, tile_blur_smem_bytes(hc.tile_blur_hmax), st>>>(
-              w.feat, w.target, lc.pg, lc.lvl, w.den32);
+          const dim3 tg(lc.tb_grid.x, (pgl.r1 + TB_T - 1) / TB_T - pgl.r0 / TB_T);
+          blur_tile_kernel<<<tg, TB_THREADS, tile_blur_smem_bytes(hc.tile_blur_hmax), st>>>(
+              w.feat, w.target, pgl, lc.lvl, w.den32);
         });
       } else {
         timed(K_BLUR0, [&] {
-          blur_pad_kernel<0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0, w.fb_cap,
+          blur_pad_kernel<0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, pgl, lc.lvl, nullptr, w.fb0, w.fb_cap,
                                                               w.fb1);
-          blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, lc.pg, lc.lvl, nullptr, w.fb0,
+          blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, pgl, lc.lvl, nullptr, w.fb0,
                                                                      w.fb_cap);
         });
         timed(K_BLUR1, [&] {
-          blur_pad_kernel<1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+          blur_pad_kernel<1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1,
                                                               w.fb_cap, w.fb0);
-          blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, lc.pg, lc.lvl, w.den32, w.fb1,
+          blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1,
                                                                      w.fb_cap);
         });
       }
       timed(K_DIST, [&] {
-        level_stats_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.feat, w.target, w.dcache, n,
-                                                                 D, S, w.spart, done, 0, 0,
-                                                                 parity ? nullptr : w.sel, w.sel_stride);
+        level_stats_kernel<<<lc.dist_grid, RED_THREADS, 0, st>>>(
+            w.ctrl, lc.sched, w.feat, w.target, w.dcache, n, D, S, w.spart + MAX_PARTS, done, 0, 0,
+            parity ? nullptr : w.sel, w.sel_stride, world > 1 ? w.lvl_part + XPART * a->rank : nullptr);
       });
+      CKL();
+      if (world > 1) {
+        // the ranks' exact 128-bit partials, all-gathered in place, then the
+        // identical level-start controller on every rank
+        const int xr = a->exchange(a->exchange_ctx, PLAS_XCHG_ALLGATHER, (int64_t)(XPART * sizeof(double)),
+                                   (int64_t)((char*)w.lvl_part - (char*)wsp), nullptr);
+        if (xr < 0) {
+          cleanup();
+          return fail(PLAS_ERR_CUDA, "exchange callback failed (level partials)");
+        }
+        level_start_shard_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, w.lvl_part, world, n);
+      }
       CKL();
       int dy = 0, dx = 0;
       if (parity) {  // draws for the first pass of the level
@@ -1241,14 +1334,14 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           // exchange this rank's updates + partial, apply the others', run the controller
           shard_pack_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(w.list, counters, w.idx, (int2*)a->xchg_send);
           CKL();
-          const int m = a->exchange(a->exchange_ctx);
+          const int m = a->exchange(a->exchange_ctx, PLAS_XCHG_PASS, 0, 0, nullptr);
           if (m < 0) {
             cleanup();
             return fail(PLAS_ERR_CUDA, "exchange callback failed");
           }
           shard_apply_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>((const int2*)a->xchg_recv, m, a->xchg_part_all,
                                                                   world, a->rank, w.orig32, w.feat, w.idx, w.target,
-                                                                  w.dcache, D, S);
+                                                                  w.dcache, D, S, w.ctrl);
           shard_control_kernel<<<1, RED_THREADS, 0, st>>>(w.ctrl, lc.sched, a->xchg_part_all, world, counters, n);
           CKL();
         }
@@ -1323,6 +1416,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   res->trace_len = out.trace_pos;
   res->cells_moved = fl[2];
   res->exact_warps = fl[3];
+  res->banded_levels = banded_levels;
   if (gtr) {
     std::vector<unsigned long long> g(6 * (size_t)out.reorders);
     cudaMemcpy(g.data(), gtr, sizeof(unsigned long long) * g.size(), cudaMemcpyDeviceToHost);
@@ -1534,7 +1628,7 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
   CK(cudaMemcpyAsync(t.w, weights, sizeof(double) * (half_width + 1), cudaMemcpyHostToDevice, st));
   pad_rows_kernel<<<grid_for(cells * S, 256, 8), 256, 0, st>>>(in, t.feat, cells, C, S);
   BlurLevelRef lv{nullptr, nullptr, nullptr, nullptr, half_width, t.w};
-  PadGeom pg{H, W, C, S, t.pad};
+  PadGeom pg = make_pad_geom(H, W, C, S, t.pad);
   border_rows_kernel<<<grid_for(H, 128, 1), 128, 0, st>>>(t.rows, H, lv);
   border_weight_kernel<<<grid_for((long long)H * ((W + 1) / 2), 256, 8), 256, 0, st>>>(t.rows, t.den32, nullptr, H,
                                                                                         W, lv);

@@ -236,12 +236,22 @@ class SortPlan:
             dev = features_dev.device
             xb = {"send": torch.zeros(2 * self.n, dtype=torch.int32, device=dev),
                   "recv": torch.zeros(2 * self.n * world, dtype=torch.int32, device=dev),
-                  "part": torch.zeros(2, dtype=torch.float64, device=dev),
-                  "part_all": torch.zeros(2 * world, dtype=torch.float64, device=dev)}
+                  "part": torch.zeros(_lib.XPART, dtype=torch.float64, device=dev),
+                  "part_all": torch.zeros(_lib.XPART * world, dtype=torch.float64, device=dev)}
 
-            def _cb(_ctx):
+            def _cb(_ctx, op, a, b, sizes):
+                ex = shard.exchange
                 try:
-                    return int(shard.exchange(xb["send"], xb["recv"], xb["part"], xb["part_all"]))
+                    if op == _lib.PLAS_XCHG_PASS:
+                        return int(ex(xb["send"], xb["recv"], xb["part"], xb["part_all"]))
+                    if op == _lib.PLAS_XCHG_ALLGATHER:
+                        ex.allgather(xb["ws"], int(b), int(a))
+                        return 0
+                    if op == _lib.PLAS_XCHG_ALLTOALL:
+                        sz = [int(sizes[i]) for i in range(2 * world)]
+                        ex.alltoall(xb["ws"], int(a), int(b), sz[:world], sz[world:])
+                        return 0
+                    raise ValueError(f"unknown exchange op {op}")
                 except Exception as exc:  # never raise through the C ABI
                     xb["error"] = exc
                     return -1
@@ -250,6 +260,8 @@ class SortPlan:
             wsb = L.plas_sort_workspace_bytes_sharded(self.n, self.dim, sch.num_levels, len(sch.weights),
                                                       self.trace_capacity, self.mode, world)
             ws = _lib.workspace(wsb, "sort")  # per thread and stream (_lib.workspace)
+            if xb is not None:
+                xb["ws"] = ws
             args = _lib.SortArgs()
             args.features = _lib.ptr(features_dev)
             args.features_dtype = _lib.PLAS_F32 if features_dev.dtype == torch.float32 else _lib.PLAS_F64
@@ -303,6 +315,7 @@ class SortPlan:
             "gpu_ms": float(res.gpu_ms),
             "cells_moved": int(res.cells_moved),
             "exact_warps": int(res.exact_warps),
+            "banded_levels": int(res.banded_levels),
         }
 
 

@@ -1,24 +1,33 @@
 """Multi-GPU PLAS sort: one grid sharded across the ranks of a process group.
 
-Design.  Every rank keeps a full replica of the sort
-state and runs the same level/pass loop.  Each pass's groups -- which are
-disjoint by construction (plas.py:118-121, 196-223) -- are split into
-contiguous, balanced per-rank ranges; a rank reassigns only its own groups,
-then the ranks all-gather
-  * their fp64 partial distance changes and moved-cell counts (16 B each), and
-  * their moved cells as (cell, element) int32 pairs (~3.6 % of their cells),
-every rank applies the others' moves (the moved element's f32 row comes from
-its own element-order copy of the features, so rows never travel) and runs
-the identical controller on the partials summed in rank order.  Draws are
-identical on every rank (NumPy-exact host draws in PARITY mode, counter-based
-Philox in DEVICE mode), so all replicas stay bit-identical.  The level blur and
-level statistics are computed redundantly per rank in this version.
+Design.  Every rank keeps a replica of the grid
+(features and element indices) and runs the same level/pass loop:
+
+* banded levels (beta * world <= side): rank r owns rows
+  [Y_r, Y_r+1), Y_r = side r / world, and each pass it takes the block rows
+  that start there -- row bands aligned to the pass's block tiling, which
+  move with the pass offset dy.  It computes the level's target only on the
+  rows its blocks can reach, [Y_r, Y_r+1 + beta): the direct and tile blur
+  tiers read the halo rows from the replica, the FFT tier splits its axis-0
+  transforms by columns and swaps band pieces with one all-to-all;
+* replicated levels (the top levels, beta * world > side): each pass's groups
+  are split into even contiguous ranges and every rank blurs the whole grid.
+
+After each pass the ranks all-gather their exact 128-bit distance changes and
+moved-cell counts (32 B each) and their moved cells as (cell, element) int32
+pairs (~3.6 % of their cells); every rank applies the others' moves (the
+moved element's f32 row comes from its own element-order copy of the
+features, so rows never travel) and runs the identical controller.  The level
+start distance sum is exchanged the same way (128-bit partials of each rank's
+own rows).  Fixed-point partials add exactly, so the sort is bit-identical to
+one GPU for any world size.  Draws are identical on every rank (NumPy-exact
+host draws in PARITY mode, counter-based Philox in DEVICE mode).
 
 The exchange runs through torch.distributed (NCCL over NVLink on one box); the
-library calls back into Python at the exchange point of each pass.
-``EmulatedGroup`` runs the same protocol for `world` ranks as threads on one
-device (tests: no kernel ever waits on another rank's kernel, the host
-rendezvous orders them).
+library calls back into Python at the exchange points (plas_sort_args.exchange,
+include/plas_b200.h).  ``EmulatedGroup`` runs the same protocol for `world`
+ranks as threads on one device (tests: no kernel ever waits on another rank's
+kernel, the host rendezvous orders them).
 """
 
 import threading
@@ -42,13 +51,14 @@ def shard_ranges(total_groups, nblocks, rank, world):
 
 
 class DistExchange:
-    """The exchange step over a torch.distributed process group (NCCL on GPUs)."""
+    """The exchange steps over a torch.distributed process group (NCCL on GPUs)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
         # the collective is chosen once, from the backend: NCCL has the fused
         # all_gather_into_tensor; other backends (gloo in the CPU tests) take
         # the list form.  Runtime errors propagate (a retry on a broken
@@ -62,15 +72,81 @@ class DistExchange:
             self.dist.all_gather(list(out.chunk(self.world)), inp, group=self.group)
 
     def __call__(self, send, recv, part, part_all):
+        """PLAS_XCHG_PASS: partials (XPART doubles per rank), then the moved cells."""
+        from ._lib import XPART
         self._all_gather(part_all, part)
-        m = int(part_all.view(self.world, 2)[:, 1].max().item())
+        m = int(part_all.view(self.world, XPART)[:, 2].max().item())
         if m > 0:
             self._all_gather(recv[: 2 * m * self.world], send[: 2 * m].contiguous())
         return m
 
+    def allgather(self, ws, off, nbytes):
+        """PLAS_XCHG_ALLGATHER: in place, rank r's piece at ws[off + r nbytes]."""
+        view = ws[off: off + self.world * nbytes]
+        mine = view[self.rank * nbytes: (self.rank + 1) * nbytes].clone()
+        self._all_gather(view, mine)
+
+    def alltoall(self, ws, send_off, recv_off, send_sizes, recv_sizes):
+        """PLAS_XCHG_ALLTOALL: byte segments in rank order at ws[send_off], ws[recv_off]."""
+        send = ws[send_off: send_off + sum(send_sizes)]
+        recv = ws[recv_off: recv_off + sum(recv_sizes)]
+        self.dist.all_to_all_single(recv, send, output_split_sizes=list(recv_sizes),
+                                    input_split_sizes=list(send_sizes), group=self.group)
+
+
+class _EmulatedRank:
+    """One rank's exchange endpoints of an EmulatedGroup (copies between the ranks' buffers)."""
+
+    def __init__(self, grp, rank):
+        self.grp = grp
+        self.rank = rank
+        self.world = grp.world
+
+    def _rendezvous(self, item):
+        import torch
+        torch.cuda.synchronize()
+        self.grp.slots[self.rank] = item
+        self.grp.barrier.wait()
+
+    def _done(self):
+        import torch
+        torch.cuda.synchronize()
+        self.grp.barrier.wait()  # every rank has read the slots before they are refilled
+
+    def __call__(self, send, recv, part, part_all):
+        import torch
+        from ._lib import XPART
+        self._rendezvous((send, part))
+        slots = self.grp.slots
+        part_all.copy_(torch.cat([slots[r][1] for r in range(self.world)]))
+        m = int(part_all.view(self.world, XPART)[:, 2].max().item())
+        for r in range(self.world):
+            recv[2 * m * r: 2 * m * (r + 1)].copy_(slots[r][0][: 2 * m])
+        self._done()
+        return m
+
+    def allgather(self, ws, off, nbytes):
+        self._rendezvous(ws)
+        for r in range(self.world):
+            if r != self.rank:
+                ws[off + r * nbytes: off + (r + 1) * nbytes].copy_(
+                    self.grp.slots[r][off + r * nbytes: off + (r + 1) * nbytes])
+        self._done()
+
+    def alltoall(self, ws, send_off, recv_off, send_sizes, recv_sizes):
+        self._rendezvous((ws, send_off, list(send_sizes)))
+        pos = recv_off
+        for j in range(self.world):
+            wsj, soff, ssz = self.grp.slots[j]
+            src = soff + sum(ssz[: self.rank])
+            assert ssz[self.rank] == recv_sizes[j]
+            ws[pos: pos + recv_sizes[j]].copy_(wsj[src: src + recv_sizes[j]])
+            pos += recv_sizes[j]
+        self._done()
+
 
 class EmulatedGroup:
-    """`world` ranks as host threads on one device: the all-gathers are copies."""
+    """`world` ranks as host threads on one device: the collectives are copies."""
 
     def __init__(self, world):
         self.world = world
@@ -78,19 +154,7 @@ class EmulatedGroup:
         self.slots = [None] * world
 
     def exchange(self, rank):
-        def ex(send, recv, part, part_all):
-            import torch
-            torch.cuda.synchronize()
-            self.slots[rank] = (send, part)
-            self.barrier.wait()
-            part_all.copy_(torch.cat([self.slots[r][1] for r in range(self.world)]))
-            m = int(part_all.view(self.world, 2)[:, 1].max().item())
-            for r in range(self.world):
-                recv[2 * m * r: 2 * m * (r + 1)].copy_(self.slots[r][0][: 2 * m])
-            torch.cuda.synchronize()
-            self.barrier.wait()  # every rank has read the slots before the next pass refills them
-            return m
-        return ex
+        return _EmulatedRank(self, rank)
 
 
 def sort_on_device_sharded(features, config, rank, world, exchange, initial_perm=None):

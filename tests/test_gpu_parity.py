@@ -391,9 +391,10 @@ def test_blur_fft_tier_top_level_c2_shape():
 # ------------------------------------------------------------------ multi-GPU sharding (emulated ranks)
 @pytest.mark.parametrize("mode,world", [("parity", 2), ("parity", 3), ("device", 2), ("device", 4)])
 def test_sharded_sort_matches_single_gpu(mode, world):
-    """The sharded protocol (per-rank group ranges + exchange of moved cells and
-    partials, sharded.py) reproduces the single-GPU sort: same permutation on every
-    rank, same pass count, trace equal up to fp64 summation order."""
+    """The sharded protocol (row bands aligned to the block tiling on banded
+    levels, even group ranges on the top levels, exact 128-bit partials,
+    sharded.py) reproduces the single-GPU sort bit for bit: same permutation on
+    every rank, same pass count, identical trace."""
     from paper_2312_13299_b200 import sharded
     f = synthetic.c1(0, side=96)
     cfg = plas.SortConfig(rng_seed=3, rng_mode=mode)
@@ -402,8 +403,30 @@ def test_sharded_sort_matches_single_gpu(mode, world):
     for perm, rep in outs:
         np.testing.assert_array_equal(perm, p1)
         assert rep["reorders"] == r1.reorders
-        np.testing.assert_allclose([v for _, t in rep["radius_trace"] for v in t],
-                                   [v for _, t in r1.radius_trace for v in t], rtol=1e-12)
+        assert rep["banded_levels"] > 0
+        np.testing.assert_array_equal([v for _, t in rep["radius_trace"] for v in t],
+                                      [v for _, t in r1.radius_trace for v in t])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_sort_banded_fft_levels(world):
+    """A 512^2 grid: banded levels on every blur tier -- FFT (axis-0 columns
+    split + band all-to-all), direct fold and tile -- and replicated top levels;
+    bit-identical to the single-GPU graph."""
+    import torch
+    from paper_2312_13299_b200 import sharded
+    f = synthetic.c1(0, side=512)
+    cfg = plas.SortConfig(rng_seed=1, rng_mode="device")
+    p1, r1 = plas.sort_on_device(torch.from_numpy(f).cuda(), cfg)
+    p1 = p1.cpu().numpy()
+    for perm, rep in sharded.sort_emulated(f, cfg, world):
+        np.testing.assert_array_equal(perm, p1)
+        assert rep["reorders"] == r1["reorders"]
+        assert 0 < rep["banded_levels"] <= len(rep["radius_trace"])
+        if world == 3:  # beta * 3 > 512 on the top levels: replicated there
+            assert rep["banded_levels"] < len(rep["radius_trace"])
+        np.testing.assert_array_equal([v for _, t in rep["radius_trace"] for v in t],
+                                      [v for _, t in r1["radius_trace"] for v in t])
 
 
 def test_sharded_sort_c0_parity_golden():

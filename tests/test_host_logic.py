@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(L, name), name
     assert set(names) == set(_lib.SIGNATURES), "ctypes signature table out of sync with the header"
-    assert L.plas_abi_version() == 4
+    assert L.plas_abi_version() == 5
     assert L.plas_sizeof_sort_args() == ctypes.sizeof(_lib.SortArgs)
     assert L.plas_sizeof_sort_result() == ctypes.sizeof(_lib.SortResult)
 

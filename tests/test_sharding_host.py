@@ -40,6 +40,7 @@ def _worker(rank, world, port, q):
         ex = sharded.DistExchange()
         n = 64
         res = []
+        # PLAS_XCHG_PASS: XPART = 4 doubles per rank (int128 change as two words, count, pad)
         for step, counts in enumerate([(3, 5), (0, 0), (7, 2)]):
             cnt = counts[rank]
             send = torch.zeros(2 * n, dtype=torch.int32)
@@ -47,11 +48,28 @@ def _worker(rank, world, port, q):
                 send[2 * e] = 100 * rank + e          # cell
                 send[2 * e + 1] = 1000 * rank + step  # element
             recv = torch.full((2 * n * world,), -1, dtype=torch.int32)
-            part = torch.tensor([0.25 * (rank + 1) + step, float(cnt)], dtype=torch.float64)
-            part_all = torch.zeros(2 * world, dtype=torch.float64)
+            part = torch.tensor([0.25 * (rank + 1) + step, -1.5 * rank, float(cnt), 0.0], dtype=torch.float64)
+            part_all = torch.zeros(4 * world, dtype=torch.float64)
             m = ex(send, recv, part, part_all)
             res.append((m, part_all.tolist(), recv[: 2 * m * world].tolist()))
-        q.put((rank, res))
+        # PLAS_XCHG_ALLGATHER: in place inside a byte workspace
+        ws = torch.zeros(256, dtype=torch.uint8)
+        off, nb = 40, 12
+        ws[off + rank * nb: off + (rank + 1) * nb] = torch.arange(nb, dtype=torch.uint8) + 50 * rank
+        ex.allgather(ws, off, nb)
+        ag = ws[off: off + world * nb].tolist()
+        # PLAS_XCHG_ALLTOALL: rank r sends (q + 1) * (r + 2) bytes of value 10 r + q to rank q
+        ws2 = torch.zeros(512, dtype=torch.uint8)
+        soff, roff = 8, 200
+        send_sizes = [(q + 1) * (rank + 2) for q in range(world)]
+        recv_sizes = [(rank + 1) * (j + 2) for j in range(world)]
+        pos = soff
+        for qq in range(world):
+            ws2[pos: pos + send_sizes[qq]] = 10 * rank + qq
+            pos += send_sizes[qq]
+        ex.alltoall(ws2, soff, roff, send_sizes, recv_sizes)
+        a2a = ws2[roff: roff + sum(recv_sizes)].tolist()
+        q.put((rank, res, ag, a2a))
     finally:
         dist.destroy_process_group()
 
@@ -64,18 +82,29 @@ def test_dist_exchange_gloo_world2():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = dict(q.get(timeout=120) for _ in range(world))
+    got = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    out = {g[0]: g[1] for g in got}
+    ags = {g[0]: g[2] for g in got}
+    a2as = {g[0]: g[3] for g in got}
     for step, counts in enumerate([(3, 5), (0, 0), (7, 2)]):
         m = max(counts)
         for rank in range(world):
             got_m, part_all, recv = out[rank][step]
             assert got_m == m
-            assert part_all == [0.25 * 1 + step, float(counts[0]), 0.25 * 2 + step, float(counts[1])]
+            assert part_all == [0.25 * 1 + step, 0.0, float(counts[0]), 0.0,
+                                0.25 * 2 + step, -1.5, float(counts[1]), 0.0]
             for r in range(world):
                 seg = recv[2 * m * r: 2 * m * (r + 1)]
                 for e in range(counts[r]):
                     assert seg[2 * e] == 100 * r + e and seg[2 * e + 1] == 1000 * r + step
         assert out[0][step] == out[1][step]  # identical on every rank
+    want = sum(([50 * r + i for i in range(12)] for r in range(world)), [])
+    assert ags[0] == want and ags[1] == want
+    for rank in range(world):
+        exp = []
+        for j in range(world):
+            exp += [10 * j + rank] * ((rank + 1) * (j + 2))
+        assert a2as[rank] == exp
