@@ -19,6 +19,7 @@
 // new "lo" and one new "hi" value through pointers that move by one stride.
 #pragma once
 #include "blur.cuh"
+#include "fold_cert.cuh"
 
 namespace plas {
 
@@ -193,18 +194,17 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
 // exact SciPy fold for the listed elements (or every element after an overflow).
 // List entries: AXIS 0 -> feat-interior offset (y*W*S + x*S + c);
 //               AXIS 1 -> target offset (same layout).
-// One warp per element: the lanes form the tap terms
-// p_j = RN(RN(x[i-j] + x[i+j]) * w_j) in parallel (they do not depend on the
-// running sum) into shared memory, then lane 0 adds them in SciPy's order
-// j = h .. 1 onto acc = RN(x[i] w_0) -- the same roundings as the reference.
-constexpr int FB_CHUNK = 256;
+// One warp per element: the certified parallel fold of fold_cert.cuh (the
+// lanes form the tap terms p_j = RN(RN(x[i-j] + x[i+j]) * w_j) and settle
+// fp32 of SciPy's ordered sum from their double-double total and a rigorous
+// bound on its roundings); lane 0 runs the ordered sum itself only for an
+// output within that bound of an fp32 rounding boundary.
 constexpr int FB_WARPS = 8;
 
 template <int AXIS, int EPI>
 __global__ void __launch_bounds__(32 * FB_WARPS) blur_pad_fallback_kernel(
     const float* __restrict__ in, float* __restrict__ out, PadGeom pg, BlurLevelRef lvl,
     const float* __restrict__ den32, int* __restrict__ fb, int fb_cap) {
-  __shared__ double terms[FB_WARPS][FB_CHUNK];
   int h;
   const double* w;
   lvl.get(&h, &w);
@@ -215,7 +215,6 @@ __global__ void __launch_bounds__(32 * FB_WARPS) blur_pad_fallback_kernel(
   const bool all = count > fb_cap;
   const long long total = all ? (long long)(pg.r1 - pg.r0) * WS : count;  // overflow: every element of rows [r0, r1)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* tm = terms[wid];
   for (long long e = (long long)blockIdx.x * FB_WARPS + wid; e < total; e += (long long)gridDim.x * FB_WARPS) {
     const long long o = all ? (long long)pg.r0 * WS + e : (long long)fb[FB_HEADER + e];
     const int c = (int)(o % S);
@@ -236,22 +235,13 @@ __global__ void __launch_bounds__(32 * FB_WARPS) blur_pad_fallback_kernel(
       i = x;
       oo = o;
     }
-    double acc = __dmul_rn((double)__ldg(line + (long long)i * stride), __ldg(w));
-    for (int j0 = h; j0 >= 1; j0 -= FB_CHUNK) {
-      const int nt = j0 < FB_CHUNK ? j0 : FB_CHUNK;  // taps j0, j0-1, ..., j0-nt+1
-      for (int t = lane; t < nt; t += 32) {
-        const int j = j0 - t;
-        tm[t] = __dmul_rn(__dadd_rn((double)__ldg(line + (long long)(i - j) * stride),
-                                    (double)__ldg(line + (long long)(i + j) * stride)),
-                          __ldg(w + j));
-      }
-      __syncwarp();
-      if (lane == 0)
-        for (int t = 0; t < nt; t++) acc = __dadd_rn(acc, tm[t]);
-      __syncwarp();
-    }
+    // certified parallel fold (fold_cert.cuh); the padded buffers hold zeros
+    // beyond the grid, so the taps need no bounds checks
+    auto X = [&](int k) { return __ldg(line + (long long)k * stride); };
+    float r;
+    const bool ok = fold_certified_warp(X, i, h, w, &r);
     if (lane == 0) {
-      float r = __double2float_rn(acc);
+      if (!ok) r = fold_sequential(X, i, h, w);
       if (EPI == 1) r = __fdiv_rn(r, den32[y * W + x]);
       out[oo] = r;
     }

@@ -436,7 +436,70 @@ __device__ __forceinline__ double warp_max_sum(double v, double m, double* out_m
 // uncertain outputs with the exact SciPy fold from a shared-memory copy of
 // the two input lines (FB_LOCAL of them; any excess goes to the global list).
 // Callers guarantee n + h <= L and n <= fft_out_max(lc).
-constexpr int FB_LOCAL = 512;
+// In-CTA list capacity: 512 entries for L <= 4096 (several CTAs per SM), 4096
+// for the long lengths (one CTA per SM, shared memory to spare; the first
+// levels of an unsorted grid have hundreds of uncertain outputs per line pair).
+#ifndef FFT_FB_LOCAL
+#define FFT_FB_LOCAL 512
+#endif
+#ifndef FFT_FB_LOCAL_LONG
+#define FFT_FB_LOCAL_LONG 4096
+#endif
+template <int L> __host__ __device__ constexpr int fft_fb_local() { return L > 4096 ? FFT_FB_LOCAL_LONG : FFT_FB_LOCAL; }
+
+// A line pair's uncertain outputs: one warp per output runs the certified
+// parallel fold (fold_cert.cuh) on the shared copy of its input line; the rare
+// output it cannot settle takes the sequential SciPy fold on lane 0.  Not
+// inlined: the FFT passes keep their register allocation (inlined, the fold's
+// double-double state pushed the 1536 / 2560 / 3072 kernels into spills).
+#ifndef FFT_WARP_FOLD_HMIN
+#define FFT_WARP_FOLD_HMIN 0
+#endif
+struct SmemLine {
+  const float* x;
+  int n;
+  __device__ __forceinline__ float operator()(int k) const { return (k >= 0 && k < n) ? x[k] : 0.f; }
+};
+template <int AXIS, int EPI>
+__device__ __noinline__ void fft_cta_folds(const float* raw, int n, const int* flist, int nf, int h,
+                                           const double* w, const float* __restrict__ den32, float* out,
+                                           long long out_base, long long out_stride, long long line, int W, int nwarps,
+                                           int* fb) {
+  // cost model (cycles, measured shape): the sequential chain is ~10 per tap
+  // on every thread at once; the warp fold ~40 per 32 taps + ~300 fixed, one
+  // output per warp at a time.  Many uncertain outputs and short kernels favour
+  // the threads (C3's 2560 / 3072 lines), few outputs and long kernels the
+  // warps (C4's 5120 / 6144 lines).
+  const long long seq_cost = (long long)((nf + nwarps * 32 - 1) / (nwarps * 32)) * h * 10;
+  const long long warp_cost = (long long)((nf + nwarps - 1) / nwarps) * (((h + 31) >> 5) * 40 + 300);
+  if (h < FFT_WARP_FOLD_HMIN || seq_cost <= warp_cost) {
+    // one thread per output runs the sequential fold
+    for (int t = threadIdx.x; t < nf; t += nwarps * 32) {
+      const int e = flist[t];
+      const int q = e >> 30, i = e & 0x3fffffff;
+      float res = fold_sequential(SmemLine{raw + q * n, n}, i, h, w);
+      if (EPI == 1) res = __fdiv_rn(res, den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)]);
+      out[out_base + q + (long long)i * out_stride] = res;
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < nf; t += nwarps) {
+    const int e = flist[t];
+    const int q = e >> 30, i = e & 0x3fffffff;
+    const SmemLine X{raw + q * n, n};
+    float res;
+    const bool ok = fold_certified_warp(X, i, h, w, &res);
+    if (lane == 0) {
+      if (!ok) res = fold_sequential(X, i, h, w);
+#ifdef PLAS_FB_STATS
+      if (!ok) atomicAdd(fb + 3, 1);  // diagnostics: sequential folds (header slot 3)
+#endif
+      if (EPI == 1) res = __fdiv_rn(res, den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)]);
+      out[out_base + q + (long long)i * out_stride] = res;
+    }
+  }
+}
 
 template <int AXIS, int EPI, int LOG2L>
 __global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blocks<fft_len(LOG2L)>())
@@ -451,7 +514,8 @@ __global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blo
   double2* bufB = fft_inplace<LOG2L>() ? fbuf : fbuf + fft_buf_len(L);
   float* raw = reinterpret_cast<float*>(fbuf + (fft_inplace<LOG2L>() ? 1 : 2) * fft_buf_len(L));  // [2][n] lines
   __shared__ double red[64];
-  __shared__ int flist[FB_LOCAL];
+  constexpr int FB_LOCAL = fft_fb_local<L>();
+  __shared__ int flist[FB_LOCAL > 0 ? FB_LOCAL : 1];
   __shared__ int nflag;
   if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) fb_other[0] = 0;
   if (threadIdx.x == 0) nflag = 0;
@@ -603,36 +667,18 @@ __global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blo
     }
   }
   __syncthreads();
-  // ---- exact SciPy fold for this CTA's uncertain outputs (blur.cuh contract)
+  // ---- this CTA's uncertain outputs: one warp per output runs the certified
+  // parallel fold (fold_cert.cuh) on the shared copy of its input line; the
+  // rare output it cannot settle takes the sequential SciPy fold on lane 0
+#ifdef FFT_DEBUG_NO_FOLD
+  const int nf = 0;  // diagnostics only (timing without the exact folds): outputs are wrong
+#else
   const int nf = min(nflag, FB_LOCAL);
-  for (int t = tid; t < nf; t += T) {
-    const int e = flist[t];
-    const int q = e >> 30, i = e & 0x3fffffff;
-    const float* x = raw + q * n;
-    double acc = __dmul_rn((double)x[i], __ldg(w));
-    // the terms do not depend on acc: 8 at a time, then the ordered adds
-    int j = h;
-    for (; j >= 8; j -= 8) {
-      double p[8];
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const int jj = j - u;
-        const double a = i - jj >= 0 ? (double)x[i - jj] : 0.0;
-        const double b = i + jj < n ? (double)x[i + jj] : 0.0;
-        p[u] = __dmul_rn(__dadd_rn(a, b), __ldg(w + jj));
-      }
-#pragma unroll
-      for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, p[u]);
-    }
-    for (; j >= 1; j--) {
-      const double a = i - j >= 0 ? (double)x[i - j] : 0.0;
-      const double b = i + j < n ? (double)x[i + j] : 0.0;
-      acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(a, b), __ldg(w + j)));
-    }
-    float res = __double2float_rn(acc);
-    if (EPI == 1) res = __fdiv_rn(res, den32[(AXIS == 0 ? (long long)i * W + line : line * W + i)]);
-    out[out_base + q + (long long)i * out_stride] = res;
-  }
+#endif
+#ifdef PLAS_FB_STATS
+  if (tid == 0 && nf) atomicAdd(fb + 2, nf);  // diagnostics: in-CTA folds (header slot 2)
+#endif
+  if (nf) fft_cta_folds<AXIS, EPI>(raw, n, flist, nf, h, w, den32, out, out_base, out_stride, line, W, T / 32, fb);
 }
 
 // shared memory of blur_fft_kernel for an L-point FFT

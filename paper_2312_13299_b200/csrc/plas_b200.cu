@@ -1114,6 +1114,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     // PLAS_LEVEL_TRACE=1 (with a profile): one stderr line per level, diagnostics only
     const bool level_trace = prof && getenv("PLAS_LEVEL_TRACE") && atoi(getenv("PLAS_LEVEL_TRACE"));
     double lvl_ms[7] = {0, 0, 0, 0, 0, 0, 0};
+    int fbstat[6] = {0, 0, 0, 0, 0, 0};
     int lvl_n[7] = {0, 0, 0, 0, 0, 0, 0};
     auto flush_profile = [&]() {
       if (!prof) return;
@@ -1233,6 +1234,15 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           band_unpack_kernel<<<num_sms() * 4, 256, 0, st>>>(w.tmp, w.xrecv, blo[r], bhi[r], dcs, world, r, WSP, S);
           CKL();
         }
+        if (level_trace) {
+          int h2[4];
+          cudaMemcpyAsync(h2, w.fb0, sizeof(int) * 4, cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fbstat[0] = h2[0];
+          fbstat[1] = h2[2];
+          fbstat[4] = h2[3];
+          cudaMemsetAsync(w.fb0 + 2, 0, sizeof(int) * 2, st);
+        }
         timed(K_BLUR1, [&] {
           {
             const float* in1 = w.tmp;
@@ -1249,6 +1259,15 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1,
                                                                      w.fb_cap);
         });
+        if (level_trace) {
+          int h2[4];
+          cudaMemcpyAsync(h2, w.fb1, sizeof(int) * 4, cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fbstat[2] = h2[0];
+          fbstat[3] = h2[2];
+          fbstat[5] = h2[3];
+          cudaMemsetAsync(w.fb1 + 2, 0, sizeof(int) * 2, st);
+        }
       } else if (mode == NPL) {
         timed(K_BLUR0, [&] {
           const dim3 tg(lc.tb_grid.x, (pgl.r1 + TB_T - 1) / TB_T - pgl.r0 / TB_T);
@@ -1378,6 +1397,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
           snprintf(lab, sizeof(lab), "f%d", fplans[mode].L);
         else
           snprintf(lab, sizeof(lab), "%s", mode == NPL ? "tile" : "dir");
+        if (getenv("PLAS_FB_TRACE")) {  // uncertain blur outputs of the level (FFT: needs -DPLAS_FB_STATS)
+          fprintf(stderr, "  fallbacks: axis0 list %d local %d (sequential %d)   axis1 list %d local %d (sequential %d)\n",
+                  fbstat[0], fbstat[1], fbstat[4], fbstat[2], fbstat[3], fbstat[5]);
+        }
         fprintf(stderr, "level %3d h %4d beta %4d %-5s passes %3d pass %7.1f us blur0 %7.1f blur1 %7.1f border %6.1f "
                 "dist %6.1f ctrl %7.1f us (%d)\n", lv, sch.hs[lv], beta,
                 lab,
