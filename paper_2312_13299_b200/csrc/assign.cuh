@@ -387,6 +387,21 @@ __device__ __forceinline__ unsigned group_entry(const int* __restrict__ sel, lon
 __device__ __forceinline__ int entry_cell_off(unsigned e, int side) { return (int)(e >> 16) * side + (int)(e & 0xffffu); }
 __device__ __forceinline__ int entry_row(unsigned e, int ww) { return (int)(e >> 16) * ww + (int)(e & 0xffffu); }
 
+// Element indices follow their rows.  Lazy (Ctrl.lazy_idx, large grids): a
+// lane reads its cell's index only when its element moves (after the
+// decision, ~4-6 % of cells per pass) instead of gathering every cell's index
+// with the rows -- a random 4-byte read costs a 32-byte sector, ~130 MB per
+// C4 pass from DRAM (C4 2.245 -> 2.205 s); on small grids the index array
+// stays in L2 and the early read hides its latency (C2 110.4 vs 111.6 ms
+// lazy).  The warp reads all moving indices before any lane writes.
+__device__ __forceinline__ void move_index(int* __restrict__ idx, bool my_mv, int cell, int dcell, int eager,
+                                           bool lazy) {
+  int v = eager;
+  if (lazy && my_mv) v = idx[cell];
+  __syncwarp();
+  if (my_mv) idx[dcell] = v;
+}
+
 // Moved-cell list: CTAs stage the destination cells of their moves in shared
 // memory and append them to list[] with one reservation on *count per flush.
 struct MoveOut {
@@ -476,6 +491,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
   int wcnt = 0;
   const int side = ctrl->side;
   const int beta = ctrl->beta;
+  const bool lazy = ctrl->lazy_idx != 0;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
   const unsigned cap = (unsigned)ctrl->cap;
@@ -519,7 +535,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
     const int k = gc.k;
     const int cell = s < k ? gc.base + entry_cell_off(gc.e, side) : 0;
     // this lane's element index, needed only if its cell moves (loaded with the rows)
-    const int my_idx0 = s < k ? idx[cell] : 0;
+    const int my_idx0 = (!lazy && s < k) ? idx[cell] : 0;
     int rowj[4], rowt[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -562,7 +578,7 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
       }
     }
     const int dcell = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + my_dst);
-    if (my_mv) idx[dcell] = my_idx;
+    move_index(idx, my_mv, cell, dcell, my_idx, lazy);
     stage_move(my_mv, dcell, wlist, &wcnt, mo);
   }
   flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
@@ -599,6 +615,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
   int wcnt = 0;
   const int side = ctrl->side;
   const int beta = ctrl->beta;
+  const bool lazy = ctrl->lazy_idx != 0;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
   const unsigned cap = (unsigned)ctrl->cap;
@@ -643,7 +660,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
   }
   float4 Fc[4], Tc[4];
   load_chunks<true>(feat, target, rowj, rowt, S, s, cvalid, Fc, Tc);
-  int my_idx = s < k ? idx[cell] : 0;
+  int my_idx = (!lazy && s < k) ? idx[cell] : 0;
   for (unsigned base = g_lo + blockIdx.x * 64u; base < total; base += stride) {
     // ---- the next group's gathers go out first
     g += stride;
@@ -657,7 +674,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
     }
     float4 nFc[4], nTc[4];
     load_chunks<true>(feat, target, nrowj, nrowt, S, s, cvalid, nFc, nTc);
-    const int nidx = s < nk ? idx[ncell] : 0;
+    const int nidx = (!lazy && s < nk) ? idx[ncell] : 0;
     // ---- decide and apply the current group
     unsigned long long acc[4][4];
 #pragma unroll
@@ -676,7 +693,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
     const int my_dst = (int)((code >> (2 * s)) & 3u);
     const bool my_mv = my_dst != s;
     const int dcell = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + my_dst);
-    if (my_mv) idx[dcell] = my_idx;
+    move_index(idx, my_mv, cell, dcell, my_idx, lazy);
     stage_move(my_mv, dcell, wlist, &wcnt, mo);
     // ---- rotate
     k = nk;
@@ -795,6 +812,7 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
   int wcnt = 0;
   const int side = ctrl->side;
   const int beta = ctrl->beta;
+  const bool lazy = ctrl->lazy_idx != 0;
   const int fy = ctrl->first_y, fx = ctrl->first_x;
   const int nby = ctrl->nby, nbx = ctrl->nbx;
   const unsigned nbx_m = ctrl->nbx_m;
@@ -862,7 +880,7 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
       const unsigned e = enext;
       group_at(q0 + TILE_THREADS / 4 + gl, &knext, &enext);
       const int mycell = origin + entry_cell_off(e, side);
-      const int my_idx = s < k ? __ldg(idx + mycell) : 0;  // consumed after the decision
+      const int my_idx = (!lazy && s < k) ? __ldg(idx + mycell) : 0;  // consumed after the decision
       const int myrow = entry_row(e, g.ww);
       int rowj[4], rowt[4];
 #pragma unroll
@@ -899,7 +917,7 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
       const int my_dst = (int)((code >> (2 * s)) & 3u);
       const bool my_mv = my_dst != s;
       const int dcell = __shfl_sync(PLAS_FULL_MASK, mycell, (lane & ~3) + my_dst);
-      if (my_mv) idx[dcell] = my_idx;
+      move_index(idx, my_mv, mycell, dcell, my_idx, lazy);
       stage_move<TILE_WARP_LIST>(my_mv, dcell, wlist, &wcnt, mo);
     }
     __syncwarp();

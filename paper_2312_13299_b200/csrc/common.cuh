@@ -79,6 +79,7 @@ struct Ctrl {
   // rows [band_lo, band_hi) (its blocks' rows for any offset of the level)
   int banded;
   int own_lo, own_hi, band_lo, band_hi;
+  int lazy_idx;                    // pass kernels read element indices of moving cells only (large grids)
   unsigned long long* gtrace;      // diagnostics (PLAS_GTRACE): per pass ~K3 start, K3 end, ~stats start, stats end
 };
 

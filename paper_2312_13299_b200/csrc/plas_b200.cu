@@ -766,6 +766,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   hc.rank = world > 1 ? a->rank : 0;
   hc.world = world;
   hc.banded = 0;  // whole grid (set per level by set_level_shard_kernel when world > 1)
+  // lazy element-index reads in the pass kernels once the index array outgrows
+  // what stays in L2 across a pass (PLAS_LAZY_IDX=0/1 overrides)
+  hc.lazy_idx = getenv("PLAS_LAZY_IDX") ? (atoi(getenv("PLAS_LAZY_IDX")) != 0) : (n * 4 > (32LL << 20) ? 1 : 0);
   hc.own_lo = hc.band_lo = 0;
   hc.own_hi = hc.band_hi = side;
   hc.pdraw = nullptr;

@@ -626,3 +626,17 @@ def test_reassign_float64_target_matches_numba_promotion():
             want[perm[i]] = i
         assert idx.tolist() == want.tolist(), (trial, k, D)
         np.testing.assert_array_equal(f, feat[want])
+
+
+def test_blur_fft_certified_folds_near_zero_outputs():
+    """Zero-mean lines blurred at the largest radii: many FFT outputs land near
+    zero, where the FFT's norm-wise bound cannot certify them; the in-CTA
+    certified folds (fold_cert.cuh, warp double-double + rounding bound, with
+    the sequential fold as last resort) must still give SciPy's bits."""
+    rng = np.random.default_rng(31)
+    for width, radii in ((4096, (1200.0, 2047.0)), (1024, (300.0, 511.0))):
+        g = rng.normal(0, 1, (3, width, 2)).astype(np.float32)
+        g -= g.mean(axis=1, keepdims=True)  # zero-mean rows: blurred values hover near zero
+        for r in radii:
+            got, fb = gblur.blur_target_tiers(g, r, 1)
+            np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"width={width} r={r} fb={fb}")
