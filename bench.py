@@ -291,10 +291,10 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-NCU_LISTS = {"C2": "ncu_summary.json", "C3": "r01_launches_c3.json", "C4": "r01_launches_c4.json"}  # per workload
+NCU_LISTS = {"C2": "r02_launches_c2.json", "C3": "r02_launches_c3.json", "C4": "r02_launches_c4.json"}  # per workload (round 2 build)
 
 
-def ncu_traffic(config, prefixes=("pass_kernel", "tile_pass_kernel")):
+def ncu_traffic(config, prefixes=("pass_kernel", "pass_kernel_pipe", "tile_pass_kernel")):
     """DRAM bytes (read + write) per K3 launch from the committed ncu launch list of
     this workload (profiles/, tools/launch_summary.py), launch-weighted over the
     gather and tile variants; None if that workload has no list."""
@@ -554,7 +554,7 @@ def run_ours(args):
         blur_total = prof.ms_blur0 + prof.ms_blur1
         dominant = "pass_kernel" if prof.ms_pass >= blur_total else "blur"
         achieved = alg_pass / avg_pass_s / 1e9
-        roofline = {"bound": "hbm", "kernel": "pass_kernel (K3 fused assign+swap+distance)",
+        roofline = {"bound": "hbm", "kernel": "K3 pass kernels (pass_kernel_pipe gather + tile_pass_kernel: fused assign+swap)",
                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
                     "algorithmic_bytes_per_launch": alg_pass, "avg_launch_us": round(avg_pass_s * 1e6, 2),
