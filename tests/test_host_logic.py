@@ -155,3 +155,23 @@ def test_device_mode_feistel_is_a_bijection():
     for m in (2, 3, 5, 16, 17, 255, 256, 1000, 4096):
         f = feistel(0x1234567 + m, m)
         assert sorted(f(i) for i in range(m)) == list(range(m))
+
+
+def test_integration_ctypes_stub_matches_library():
+    """The ctypes stub INTEGRATION.md shows a maintainer declares the same
+    plas_sort_args / plas_sort_result layout as the library (sizeof checks; no
+    CUDA call)."""
+    import ctypes
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "INTEGRATION.md")).read()
+    i = src.index("## 2. Binding the C ABI directly")
+    j = src.index("```python", i) + len("```python")
+    code = src[j: src.index("```", j)].split("def sort_grid")[0]
+    code = code.replace('ctypes.CDLL("paper_2312_13299_b200/libplas_b200.so")',
+                        f'ctypes.CDLL("{os.path.join(root, "paper_2312_13299_b200", "libplas_b200.so")}")')
+    ns = {}
+    exec(code, ns)
+    L = ns["L"]
+    L.plas_sizeof_sort_result.restype = ctypes.c_size_t
+    assert ctypes.sizeof(ns["SortArgs"]) == L.plas_sizeof_sort_args()
+    assert ctypes.sizeof(ns["SortResult"]) == L.plas_sizeof_sort_result()
