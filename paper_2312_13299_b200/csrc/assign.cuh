@@ -250,9 +250,69 @@ __device__ __forceinline__ void load_chunks(const float* Fb, const float* Tb, co
   }
 }
 
+template <bool OOL>  // exact tier out of line (wide rows)
 __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4][4], const float* Fb,
                                                const float* Tb, const int (&rowj)[4], int D, int S, int k,
                                                int* exact);
+
+// Exact tier for the whole warp (same decision wherever the fast one was
+// certain): lane s recomputes row s of the cost matrix with the reference
+// arithmetic, then the first strict minimum over the lexicographic
+// arrangements (~1.7 % of warps take it at C2).
+__device__ __forceinline__ int decide_exact_body(const float* Fb, const float* Tb, const int (&rowj)[4], int D,
+                                                 int S, int k) {
+  const int lane = threadIdx.x & 31;
+  const int s = lane & 3;
+  const int gbase = lane & ~3;
+  const int nch = S >> 2;
+  double dacc[4] = {0.0, 0.0, 0.0, 0.0};
+  float cst[4];
+  const long long fo = (long long)pick4(rowj, s) * S;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    if (s < k && j < k) {
+      const long long to = (long long)rowj[j] * S;
+      for (int c = 0; c < nch; c++) {
+        const float4 f = ld4v(Fb + fo + 4 * c);
+        const float4 t = ld4v(Tb + to + 4 * c);
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+          if (4 * c + e < D) {
+            const float df = __fsub_rn(f4get(f, e), f4get(t, e));
+            dacc[j] = __dadd_rn(dacc[j], (double)__fmul_rn(df, df));
+          }
+      }
+    }
+    cst[j] = __double2float_rn(__dsqrt_rn(dacc[j]));
+  }
+  CostMat C;
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) C.v[i][j] = __shfl_sync(PLAS_FULL_MASK, cst[j], gbase + i);
+  double bc;
+  int bp;
+  lane_best_exact(C, k, s, &bc, &bp);
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    const double oc = __shfl_xor_sync(PLAS_FULL_MASK, bc, o);
+    const int op = __shfl_xor_sync(PLAS_FULL_MASK, bp, o);
+    if (oc < bc || (oc == bc && op < bp)) {
+      bc = oc;
+      bp = op;
+    }
+  }
+  // every arrangement sum +inf (fp32 costs overflowed): the reference keeps
+  // best = 0, the identity (plas.py:138-146, strict < against best_cost = inf)
+  return bp == 0x7fffffff ? 0 : bp;
+}
+// Out of line for the wide-row kernels (C3: 1.687 -> 1.664 s); inlined in the
+// 16-float kernels, where the call's register save cost more (C2 110.7 ->
+// 111.6 ms, C4 2.204 -> 2.248 s).
+__device__ __noinline__ int decide_exact_call(const float* Fb, const float* Tb, const int (&rowj)[4], int D, int S,
+                                              int k) {
+  return decide_exact_body(Fb, Tb, rowj, D, S, k);
+}
 
 template <bool WIDE, bool TNC>
 __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const int (&rowj)[4],
@@ -274,9 +334,10 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
     load_chunks<TNC>(Fb, Tb, rowj, rowt, S, c, c < nch, Fc, Tc);
     accum_chunks(acc, Fc, Tc);
   }
-  return decide_from_acc(acc, Fb, Tb, rowj, D, S, k, exact);
+  return decide_from_acc<WIDE>(acc, Fb, Tb, rowj, D, S, k, exact);
 }
 
+template <bool OOL>  // exact tier out of line (wide rows)
 __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4][4], const float* Fb,
                                                const float* Tb, const int (&rowj)[4], int D, int S, int k,
                                                int* exact) {
@@ -330,47 +391,7 @@ __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4
   const bool certain =
       k < 2 || (b2 < __int_as_float(0x7f800000) && b2 > 1e-30f && (b2 - b1) > margin * b2);
   if (__any_sync(PLAS_FULL_MASK, !certain)) {
-    // ---- exact tier for the whole warp (same decision wherever the fast one was
-    // certain): lane s recomputes row s with the reference arithmetic
-    double dacc[4] = {0.0, 0.0, 0.0, 0.0};
-    float cst[4];
-    const long long fo = (long long)pick4(rowj, s) * S;
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      if (s < k && j < k) {
-        const long long to = (long long)rowj[j] * S;
-        for (int c = 0; c < nch; c++) {
-          const float4 f = ld4v(Fb + fo + 4 * c);
-          const float4 t = ld4v(Tb + to + 4 * c);
-#pragma unroll
-          for (int e = 0; e < 4; e++)
-            if (4 * c + e < D) {
-              const float df = __fsub_rn(f4get(f, e), f4get(t, e));
-              dacc[j] = __dadd_rn(dacc[j], (double)__fmul_rn(df, df));
-            }
-        }
-      }
-      cst[j] = __double2float_rn(__dsqrt_rn(dacc[j]));
-    }
-    CostMat C;
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-#pragma unroll
-      for (int j = 0; j < 4; j++) C.v[i][j] = __shfl_sync(PLAS_FULL_MASK, cst[j], gbase + i);
-    double bc;
-    lane_best_exact(C, k, s, &bc, &bp);
-#pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-      const double oc = __shfl_xor_sync(PLAS_FULL_MASK, bc, o);
-      const int op = __shfl_xor_sync(PLAS_FULL_MASK, bp, o);
-      if (oc < bc || (oc == bc && op < bp)) {
-        bc = oc;
-        bp = op;
-      }
-    }
-    // every arrangement sum +inf (fp32 costs overflowed): the reference keeps
-    // best = 0, the identity (plas.py:138-146, strict < against best_cost = inf)
-    if (bp == 0x7fffffff) bp = 0;
+    bp = OOL ? decide_exact_call(Fb, Tb, rowj, D, S, k) : decide_exact_body(Fb, Tb, rowj, D, S, k);
     if (s == 0 && k >= 2 && !certain) *exact += 1;
   }
   return k < 2 ? 0 : bp;
@@ -682,7 +703,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
 #pragma unroll
       for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
     accum_chunks(acc, Fc, Tc);
-    const int bp = decide_from_acc(acc, feat, target, rowj, D, S, k, &exact);
+    const int bp = decide_from_acc<false>(acc, feat, target, rowj, D, S, k, &exact);
     const unsigned code = perm_dest_code(k, bp);
 #pragma unroll
     for (int i = 0; i < 4; i++) {

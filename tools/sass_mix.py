@@ -15,7 +15,10 @@ for r in rows[2:]:
         continue
     op = toks[1] if toks[0].startswith("@") else toks[0]
     base = op.split(".")[0] if "--full" not in sys.argv else op
-    n, s = int(r[ie] or 0), int(r[st] or 0)
+    try:
+        n, s = int(r[ie] or 0), int(r[st] or 0)
+    except ValueError:
+        continue
     cnt[base] += n; stall[base] += s; tot += n; stot += s
 print("total warp-inst", tot, "stall samples", stot)
 for k, v in cnt.most_common(40):
