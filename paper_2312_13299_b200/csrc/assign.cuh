@@ -344,7 +344,6 @@ __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4
   const int lane = threadIdx.x & 31;
   const int s = lane & 3;
   const int gbase = lane & ~3;
-  const int nch = S >> 2;
   float part[4][4];
 #pragma unroll
   for (int i = 0; i < 4; i++)
