@@ -63,7 +63,11 @@ __host__ __device__ inline PadGeom make_pad_geom(int H, int W, int C, int S, int
 #define BPAD_R 8  // outputs per thread of the direct fold (register rings of BPAD_R)
 #endif
 
-template <int AXIS, int EPI>
+// HC > 0: the level's half-width as a compile-time constant (small radii):
+// the tap loop is fully static -- no partial tap block whose R unrolled steps
+// are all issued under predicates -- which halves the instructions per output
+// at h <= 8 (the direct tier's fixed cost dominated below h ~ 16).
+template <int AXIS, int EPI, int HC = 0>
 __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                        PadGeom pg, BlurLevelRef lvl,
                                                        const float* __restrict__ den32,
@@ -72,9 +76,10 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
   constexpr int R = BPAD_R;
   // the other axis' fallback list has been consumed by now: clear its counter
   if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) fb_other[0] = 0;
-  int h;
+  int hrt;
   const double* w;
-  lvl.get(&h, &w);
+  lvl.get(&hrt, &w);
+  const int h = HC > 0 ? HC : hrt;
   const int H = pg.H, W = pg.W, C = pg.C, S = pg.S;
   const int n = AXIS == 0 ? H : W;
   const long long WS = (long long)W * S;

@@ -217,6 +217,43 @@ struct SortWs {
   int fft_L;                       // longest length (0: no FFT tier)
 };
 
+// ---------------------------------------------------------------- direct fold, compile-time h
+// Direct-tier levels with h <= PAD_SMALL_HMAX run blur_pad_kernel<AXIS, EPI, h>
+// (static tap loop); larger h the runtime-h kernel.  PLAS_PAD_SMALL=0 turns
+// the specialisations off (A/B).
+constexpr int PAD_SMALL_HMAX = 16;
+using PadFn = void (*)(const float*, float*, PadGeom, BlurLevelRef, const float*, int*, int, int*);
+template <int H>
+PadFn pad_small_fn(int axis) {
+  return axis == 0 ? (PadFn)blur_pad_kernel<0, 0, H> : (PadFn)blur_pad_kernel<1, 1, H>;
+}
+int pad_small_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("PLAS_PAD_SMALL") ? (atoi(getenv("PLAS_PAD_SMALL")) != 0) : 1;
+  return v;
+}
+PadFn pad_fn(int axis, int h) {
+  if (pad_small_enabled()) switch (h) {
+      case 1: return pad_small_fn<1>(axis);
+      case 2: return pad_small_fn<2>(axis);
+      case 3: return pad_small_fn<3>(axis);
+      case 4: return pad_small_fn<4>(axis);
+      case 5: return pad_small_fn<5>(axis);
+      case 6: return pad_small_fn<6>(axis);
+      case 7: return pad_small_fn<7>(axis);
+      case 8: return pad_small_fn<8>(axis);
+      case 9: return pad_small_fn<9>(axis);
+      case 10: return pad_small_fn<10>(axis);
+      case 11: return pad_small_fn<11>(axis);
+      case 12: return pad_small_fn<12>(axis);
+      case 13: return pad_small_fn<13>(axis);
+      case 14: return pad_small_fn<14>(axis);
+      case 15: return pad_small_fn<15>(axis);
+      case 16: return pad_small_fn<16>(axis);
+    }
+  return axis == 0 ? (PadFn)blur_pad_kernel<0, 0> : (PadFn)blur_pad_kernel<1, 1>;
+}
+
 // ---------------------------------------------------------------- FFT blur tier
 constexpr int FFT_PLANS = 4;  // 32 <= L <= 8192 (16 L bytes of shared memory per CTA)
 
@@ -876,6 +913,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   for (int lv = 0; lv < L; lv++) {
     const int h = sch.hs[lv];
     int m = level_uses_tile_blur(h, side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax) ? NPL : NPL + 1;
+    if (m == NPL + 1 && h <= PAD_SMALL_HMAX && pad_small_enabled()) m = NPL + 1 + h;  // direct, compile-time h
     if (NPL && level_uses_fft(h, side, hc.fft_min_h, hc.fft_L)) {
       const int lcode = fft_choose_code(side, h);
       m = NPL - 1;  // the longest length covers every FFT level
@@ -948,15 +986,15 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     // SWITCH (blur mode of the level) { FFT at length 0 | ... | FFT at length
     // NPL - 1 | one tile kernel | direct fold + fallbacks }
     cudaGraphNode_t blur_if;
-    cudaGraph_t bbody[FFT_PLANS + 2];
+    cudaGraph_t bbody[FFT_PLANS + 2 + PAD_SMALL_HMAX];
     {
       cudaGraphNodeParams p{};
       p.type = cudaGraphNodeTypeConditional;
       p.conditional.handle = blur_h;
       p.conditional.type = cudaGraphCondTypeSwitch;
-      p.conditional.size = NPL + 2;
+      p.conditional.size = NPL + 2 + PAD_SMALL_HMAX;
       CK(cudaGraphAddNode(&blur_if, obody, &nd[2], 1, &p));
-      for (int i = 0; i < NPL + 2; i++) bbody[i] = p.conditional.phGraph_out[i];
+      for (int i = 0; i < NPL + 2 + PAD_SMALL_HMAX; i++) bbody[i] = p.conditional.phGraph_out[i];
     }
     for (int i = 0; i < NPL; i++) {
       cudaGraphNode_t fn[5];
@@ -1005,14 +1043,18 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       cudaGraphNode_t tn;
       CK(cudaGraphAddKernelNode(&tn, bbody[NPL], nullptr, 0, &kp));
     }
-    {
-      cudaGraph_t db = bbody[NPL + 1];
+    // direct fold: the runtime-h kernels (case NPL + 1) and the compile-time-h
+    // kernels of h = 1 .. PAD_SMALL_HMAX (case NPL + 1 + h)
+    for (int hb = 0; hb <= PAD_SMALL_HMAX; hb++) {
+      cudaGraph_t db = bbody[NPL + 1 + hb];
       cudaGraphNode_t bn[4];
-      CK(add_kernel(&bn[0], db, nullptr, 0, blur_pad_kernel<0, 0>, dim3(lc.blur_grid), dim3(256),
+      const PadFn p0 = hb ? pad_fn(0, hb) : (PadFn)blur_pad_kernel<0, 0>;
+      const PadFn p1 = hb ? pad_fn(1, hb) : (PadFn)blur_pad_kernel<1, 1>;
+      CK(add_kernel(&bn[0], db, nullptr, 0, p0, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
       CK(add_kernel(&bn[1], db, &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
-      CK(add_kernel(&bn[2], db, &bn[1], 1, blur_pad_kernel<1, 1>, dim3(lc.blur_grid), dim3(256),
+      CK(add_kernel(&bn[2], db, &bn[1], 1, p1, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
       CK(add_kernel(&bn[3], db, &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
@@ -1278,15 +1320,15 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
               w.feat, w.target, pgl, lc.lvl, w.den32);
         });
       } else {
+        const int hl = sch.hs[lv];
+        const PadFn p0 = pad_fn(0, hl), p1 = pad_fn(1, hl);
         timed(K_BLUR0, [&] {
-          blur_pad_kernel<0, 0><<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, pgl, lc.lvl, nullptr, w.fb0, w.fb_cap,
-                                                              w.fb1);
+          p0<<<lc.blur_grid, 256, 0, st>>>(w.feat, w.tmp, pgl, lc.lvl, nullptr, w.fb0, w.fb_cap, w.fb1);
           blur_pad_fallback_kernel<0, 0><<<lc.fb_grid, 256, 0, st>>>(w.feat, w.tmp, pgl, lc.lvl, nullptr, w.fb0,
                                                                      w.fb_cap);
         });
         timed(K_BLUR1, [&] {
-          blur_pad_kernel<1, 1><<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1,
-                                                              w.fb_cap, w.fb0);
+          p1<<<lc.blur_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1, w.fb_cap, w.fb0);
           blur_pad_fallback_kernel<1, 1><<<lc.fb_grid, 256, 0, st>>>(w.tmp, w.target, pgl, lc.lvl, w.den32, w.fb1,
                                                                      w.fb_cap);
         });
@@ -1399,7 +1441,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
         if (use_fft)
           snprintf(lab, sizeof(lab), "f%d", fplans[mode].L);
         else
-          snprintf(lab, sizeof(lab), "%s", mode == NPL ? "tile" : "dir");
+          snprintf(lab, sizeof(lab), "%s", mode == NPL ? "tile" : (mode == NPL + 1 ? "dir" : "dirH"));
         if (getenv("PLAS_FB_TRACE")) {  // uncertain blur outputs of the level (FFT: needs -DPLAS_FB_STATS)
           fprintf(stderr, "  fallbacks: axis0 list %d local %d (sequential %d)   axis1 list %d local %d (sequential %d)\n",
                   fbstat[0], fbstat[1], fbstat[4], fbstat[2], fbstat[3], fbstat[5]);
@@ -1669,10 +1711,10 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
                                                                                                   lv, t.den32);
   } else if (tier == 0) {
     const int g0 = grid_for((long long)W * S * ((H + BPAD_R - 1) / BPAD_R), 256, 8);
-    blur_pad_kernel<0, 0><<<g0, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap, t.fb1);
+    pad_fn(0, half_width)<<<g0, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap, t.fb1);
     CK(cudaMemcpyAsync(&hc[0], t.fb0, sizeof(int), cudaMemcpyDeviceToHost, st));
     blur_pad_fallback_kernel<0, 0><<<fbg, 256, 0, st>>>(t.feat, t.tmp, pg, lv, nullptr, t.fb0, t.fb_cap);
-    blur_pad_kernel<1, 1><<<g0, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap, t.fb0);
+    pad_fn(1, half_width)<<<g0, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap, t.fb0);
     CK(cudaMemcpyAsync(&hc[1], t.fb1, sizeof(int), cudaMemcpyDeviceToHost, st));
     blur_pad_fallback_kernel<1, 1><<<fbg, 256, 0, st>>>(t.tmp, t.target, pg, lv, t.den32, t.fb1, t.fb_cap);
   } else {
