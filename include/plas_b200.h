@@ -198,7 +198,10 @@ int plas_blur_target_tiers(const float* in, float* out, int H, int W, int C, con
                            void* stream);
 
 /* grid_distance (plas.py:71-84): fp64 (n, dim) inputs, optional device
- * weights [dim]; result written to *out_dev (device double). */
+ * weights [dim]; result written to *out_dev (device double).  Summed in
+ * NumPy's pairwise order, so the value equals the reference's bit for bit;
+ * ws of plas_grid_distance_workspace_bytes(n) bytes. */
+size_t plas_grid_distance_workspace_bytes(int64_t n);
 int plas_grid_distance(const double* a, const double* b, const double* weights, int64_t n, int dim,
                        double* out_dev, void* ws, size_t ws_bytes, void* stream);
 

@@ -80,6 +80,7 @@ struct Ctrl {
   int banded;
   int own_lo, own_hi, band_lo, band_hi;
   int lazy_idx;                    // pass kernels read element indices of moving cells only (large grids)
+  int exact_stats;                 // PARITY on one GPU: strike decisions on NumPy-order grid_distance (np_sum.cuh)
   unsigned long long* gtrace;      // diagnostics (PLAS_GTRACE): per pass ~K3 start, K3 end, ~stats start, stats end
 };
 

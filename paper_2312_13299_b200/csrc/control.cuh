@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
     if (gen && gridDim.x == 1) gen_class_tables(c, 0, tab, tab_stride, 0, 1);
     return;
   }
+  if (c->exact_stats) return;  // PARITY, one GPU: np_level_start_kernel on NumPy's grid_distance
   __shared__ Ctrl sc;
   Ctrl* const cg = c;
   ctrl_to_smem(&sc, cg);
@@ -549,10 +550,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
 // distance change `tot` of its moved cells: current = (level-start sum +
 // changes) / n, trace append, strikes, level end.  Thread 0 only; returns
 // whether the level continues.
-__device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, long long n,
-                                                unsigned long long inner) {
-  c->dist_sum += tot;
-  const double current = c->dist_sum / (double)n;
+__device__ __forceinline__ bool controller_step_cur(Ctrl* c, Sched s, double current, unsigned long long inner) {
   const double previous = c->previous;
   c->current = current;
   c->reorders++;
@@ -575,6 +573,11 @@ __device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, lo
     return false;
   }
   return true;
+}
+__device__ __forceinline__ bool controller_step(Ctrl* c, Sched s, double tot, long long n,
+                                                unsigned long long inner) {
+  c->dist_sum += tot;
+  return controller_step_cur(c, s, c->dist_sum / (double)n, inner);
 }
 
 // After a pass: exact fp64 distance change of the moved cells (cells that
@@ -715,6 +718,13 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     }
     return;
   }
+  if (c->exact_stats) {  // PARITY, one GPU: np_pass_control_kernel decides on NumPy's grid_distance
+    if (threadIdx.x == 0) {
+      counters[0] += count;
+      counters[2] = 0;
+    }
+    return;
+  }
   __shared__ Ctrl sc;
   Ctrl* const cg = c;
   ctrl_to_smem(&sc, cg);
@@ -809,6 +819,21 @@ __global__ void __launch_bounds__(RED_THREADS) level_start_shard_kernel(Ctrl* c,
   }
   go = __syncthreads_or(go);
   if (go && c->rng_mode == 1) prepare_device_pass_cta(c, &s_gkey);
+}
+
+// PARITY mode on one GPU: the level-start and per-pass controller on the
+// reference's own grid_distance (np_sum.cuh: NumPy's summation order, so
+// previous / current and every strike decision match plas.py:256-272 bit for
+// bit); exact = (sum, sum / n) from np_tree_kernel.
+__global__ void np_level_start_kernel(Ctrl* c, Sched s, const double* __restrict__ exact, long long n) {
+  if (threadIdx.x) return;
+  bool go = false;
+  level_start_control(c, s, exact[0], n, 0ull, 0ull, &go);
+}
+__global__ void np_pass_control_kernel(Ctrl* c, Sched s, const double* __restrict__ exact) {
+  if (threadIdx.x) return;
+  c->dist_sum = exact[0];
+  controller_step_cur(c, s, exact[1], 0ull);
 }
 
 // This level's sharding (host-stepped multi-GPU loop, before the blur).
@@ -917,25 +942,5 @@ __global__ void __launch_bounds__(RED_THREADS) mean_finalize_kernel(const double
   if (threadIdx.x == 0) *out = tot / count;
 }
 
-// ---------------------------------------------------------------- API grid_distance
-// fp64 inputs, optional per-channel weights (plas.py:71-84)
-__global__ void __launch_bounds__(RED_THREADS) grid_distance_f64_kernel(
-    const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ w,
-    long long n, int D, double* __restrict__ partials) {
-  __shared__ double sh[32];
-  double sum = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int d = 0; d < D; d++) {
-      double df = a[i * D + d] - b[i * D + d];
-      if (w) df = df * w[d];
-      s += df * df;
-    }
-    sum += sqrt(s);
-  }
-  double tot = block_sum<RED_THREADS>(sum, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
-}
-
+// (the API's grid_distance is np_sum.cuh: NumPy's summation order)
 }  // namespace plas

@@ -36,6 +36,7 @@
 #include "common.cuh"
 #include "control.cuh"
 #include "host_rng.h"
+#include "np_sum.cuh"
 #include "smooth.cuh"
 
 using namespace plas;
@@ -207,6 +208,12 @@ struct SortWs {
   float *xsend, *xrecv;  // sharding: FFT-tier axis-0 band exchange (all-to-all) buffers
   double* lvl_part;      // sharding: level-start partials, XPART doubles per rank (all-gathered in place)
   int* bands;            // sharding: per level [lo[world], hi[world], cs[world + 1]] for the pack kernels
+  // PARITY on one GPU: NumPy-order grid_distance (np_sum.cuh)
+  double* np_v;          // per-cell sqrt(row sum) [n]
+  double* np_vals;       // tree node values [leaves + internal]
+  long long* np_lstart;  // leaf starts
+  int *np_llen, *np_left, *np_right, *np_order, *np_hoff;
+  double* np_out;        // (sum, sum / n)
   // FFT tier: up to FFT_PLANS lengths (the shortest that fits each level's h)
   int fft_count;                   // number of lengths
   int fft_codes[4];                // length codes, increasing length
@@ -441,6 +448,19 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->xrecv = c.take<float>(xfl);
   w->lvl_part = c.take<double>((size_t)XPART * std::max(world, 1));
   w->bands = c.take<int>((size_t)3 * std::max(world, 1) + 1);
+  // NumPy tree: leaves hold 8..128 cells (more than n / 128 + 2 of them), as
+  // many internal nodes, heights <= 64
+  const bool npx = rng_mode == PLAS_RNG_PARITY && world <= 1;
+  const size_t nleaf = npx ? (size_t)(n / 64 + 4) : 1;
+  w->np_v = c.take<double>(npx ? (size_t)n : 1);
+  w->np_vals = c.take<double>(2 * nleaf);
+  w->np_lstart = c.take<long long>(nleaf);
+  w->np_llen = c.take<int>(nleaf);
+  w->np_left = c.take<int>(nleaf);
+  w->np_right = c.take<int>(nleaf);
+  w->np_order = c.take<int>(nleaf);
+  w->np_hoff = c.take<int>(72);
+  w->np_out = c.take<double>(2);
   fft_plan_codes(side, row_stride(dim), &w->fft_count, w->fft_codes);
   w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
   for (int i = 0; i < 4; i++)
@@ -806,12 +826,39 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   // lazy element-index reads in the pass kernels once the index array outgrows
   // what stays in L2 across a pass (PLAS_LAZY_IDX=0/1 overrides)
   hc.lazy_idx = getenv("PLAS_LAZY_IDX") ? (atoi(getenv("PLAS_LAZY_IDX")) != 0) : (n * 4 > (32LL << 20) ? 1 : 0);
+  // PARITY on one GPU: strike decisions on the reference's own (NumPy-order)
+  // grid_distance, so the trace and every pass count are bit-identical
+  // (PLAS_NP_STATS=0: the fixed-point running sum instead, as the sharded path uses)
+  hc.exact_stats = (mode == PLAS_RNG_PARITY && world == 1 &&
+                    !(getenv("PLAS_NP_STATS") && atoi(getenv("PLAS_NP_STATS")) == 0)) ? 1 : 0;
   hc.own_lo = hc.band_lo = 0;
   hc.own_hi = hc.band_hi = side;
   hc.pdraw = nullptr;
   hc.prec = nullptr;
   hc.pdraw_level = -1;
   CK(cudaMemcpyAsync(w.ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  NpTree npt;
+  if (hc.exact_stats) {  // the n-cell pairwise tree of NumPy's mean (depends on n only)
+    np_tree_make(&npt, n);
+    const size_t nl = npt.leaf_start.size(), ni = npt.left.size();
+    if ((long long)nl > n / 64 + 4 || npt.hoff.size() > 72) return fail(PLAS_ERR_INVALID, "numpy tree sizing");
+    CK(cudaMemcpyAsync(w.np_lstart, npt.leaf_start.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.np_llen, npt.leaf_len.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st));
+    if (ni) {
+      CK(cudaMemcpyAsync(w.np_left, npt.left.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(w.np_right, npt.right.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(w.np_order, npt.order.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(w.np_hoff, npt.hoff.data(), sizeof(int) * npt.hoff.size(), cudaMemcpyHostToDevice, st));
+  }
+  // NumPy's grid_distance of the current grid vs target into np_out
+  auto np_distance = [&]() {
+    np_cell_sort_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(w.feat, w.target, n, D, S, w.np_v);
+    const int nl = (int)npt.leaf_start.size();
+    np_leaf_kernel<<<std::max(1, (nl + 255) / 256), 256, 0, st>>>(w.np_v, w.np_lstart, w.np_llen, nl, w.np_vals);
+    np_tree_kernel<<<1, 1024, 0, st>>>(w.np_vals, w.np_left, w.np_right, w.np_order, w.np_hoff,
+                                       (int)npt.hoff.size() - 1, nl, npt.root, n, w.np_out);
+  };
   CK(cudaMemsetAsync(w.flags, 0, sizeof(int) * 8, st));
   CK(cudaMemsetAsync(w.spart + MAX_PARTS, 0, 2 * sizeof(double), st));  // pass statistic's 128-bit accumulator
   // zero halos of the padded blur buffers, pad channels, fallback counters
@@ -1338,6 +1385,12 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
             w.ctrl, lc.sched, w.feat, w.target, w.dcache, n, D, S, w.spart + MAX_PARTS, done, 0, 0,
             parity ? nullptr : w.sel, w.sel_stride, world > 1 ? w.lvl_part + XPART * a->rank : nullptr);
       });
+      if (hc.exact_stats) {
+        timed(K_DIST, [&] {
+          np_distance();
+          np_level_start_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, w.np_out, n);
+        });
+      }
       CKL();
       if (world > 1) {
         // the ranks' exact 128-bit partials, all-gathered in place, then the
@@ -1392,6 +1445,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                                                            w.list, counters, w.spart + MAX_PARTS, done, n, 0, 0, a->xchg_part,
                                                            parity || world > 1 ? nullptr : w.sel, w.sel_stride);
           if (!parity && world > 1) gen_tables_kernel<<<num_sms(), 256, 0, st>>>(w.ctrl, w.sel, w.sel_stride);
+          if (hc.exact_stats) {
+            np_distance();
+            np_pass_control_kernel<<<1, 32, 0, st>>>(w.ctrl, lc.sched, w.np_out);
+          }
         });
         CKL();
         if (world > 1) {
@@ -1776,15 +1833,56 @@ int plas_blur(const void* in, void* out, int dtype, int H, int W, int C, const d
   return launch_blur(in, out, dtype, H, W, C, C, half_width, a, op == PLAS_BLUR_RENORMALIZED, st);
 }
 
+// workspace of plas_grid_distance: per-cell values + the NumPy tree
+static size_t carve_np(char* base, long long n, double** v, double** vals, long long** lstart, int** llen,
+                       int** left, int** right, int** order, int** hoff, double** out) {
+  Carver c{base};
+  const size_t nleaf = (size_t)(n / 64 + 4);
+  *v = c.take<double>((size_t)n);
+  *vals = c.take<double>(2 * nleaf);
+  *lstart = c.take<long long>(nleaf);
+  *llen = c.take<int>(nleaf);
+  *left = c.take<int>(nleaf);
+  *right = c.take<int>(nleaf);
+  *order = c.take<int>(nleaf);
+  *hoff = c.take<int>(72);
+  *out = c.take<double>(2);
+  return align_up(c.off);
+}
+
+size_t plas_grid_distance_workspace_bytes(int64_t n) {
+  double *v, *vals, *out;
+  long long* ls;
+  int *ll, *l, *r, *o, *h;
+  return carve_np(nullptr, std::max<int64_t>(n, 1), &v, &vals, &ls, &ll, &l, &r, &o, &h, &out);
+}
+
+// grid_distance (plas.py:71-84) in NumPy's summation order (np_sum.cuh):
+// bit-identical to the reference's float
 int plas_grid_distance(const double* a, const double* b, const double* weights, int64_t n, int dim,
                        double* out_dev, void* ws, size_t ws_bytes, void* stream) {
   if (n < 1 || dim < 1) return fail(PLAS_ERR_INVALID, "bad grid_distance arguments");
-  if (!ws || ws_bytes < sizeof(double) * MAX_PARTS) return fail(PLAS_ERR_WORKSPACE, "aux workspace");
+  if (!ws || ws_bytes < plas_grid_distance_workspace_bytes(n)) return fail(PLAS_ERR_WORKSPACE, "grid_distance workspace");
   cudaStream_t st = (cudaStream_t)stream;
-  double* partials = (double*)ws;
-  int grid = grid_for(n, RED_THREADS, 4);
-  grid_distance_f64_kernel<<<grid, RED_THREADS, 0, st>>>(a, b, weights, n, dim, partials);
-  mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, grid, (double)n, out_dev);
+  double *v, *vals, *out;
+  long long* ls;
+  int *ll, *l, *r, *o, *h;
+  carve_np((char*)ws, n, &v, &vals, &ls, &ll, &l, &r, &o, &h, &out);
+  NpTree t;
+  np_tree_make(&t, n);
+  const size_t nl = t.leaf_start.size(), ni = t.left.size();
+  CK(cudaMemcpyAsync(ls, t.leaf_start.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ll, t.leaf_len.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st));
+  if (ni) {
+    CK(cudaMemcpyAsync(l, t.left.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(r, t.right.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(o, t.order.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemcpyAsync(h, t.hoff.data(), sizeof(int) * t.hoff.size(), cudaMemcpyHostToDevice, st));
+  np_cell_f64_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(a, b, weights, n, dim, v);
+  np_leaf_kernel<<<std::max<int>(1, (int)((nl + 255) / 256)), 256, 0, st>>>(v, ls, ll, (int)nl, vals);
+  np_tree_kernel<<<1, 1024, 0, st>>>(vals, l, r, o, h, (int)t.hoff.size() - 1, (int)nl, t.root, n, out);
+  CK(cudaMemcpyAsync(out_dev, out + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
   CKL();
   return PLAS_OK;
 }

@@ -79,7 +79,8 @@ def blur_target(grid, radius):
 
 
 def grid_distance(grid, target, weights=None):
-    """Mean Euclidean distance between grid and target cells (plas.py:71-84)."""
+    """Mean Euclidean distance between grid and target cells (plas.py:71-84),
+    summed in NumPy's pairwise order on the GPU: the same float as the reference."""
     import torch
     grid = np.asarray(grid, dtype=np.float64) if not isinstance(grid, torch.Tensor) else grid
     target = np.asarray(target, dtype=np.float64) if not isinstance(target, torch.Tensor) else target
@@ -92,7 +93,7 @@ def grid_distance(grid, target, weights=None):
     b = _lib.to_device(target, torch.float64).reshape(-1)
     w = None if weights is None else _lib.to_device(np.asarray(weights, dtype=np.float64), torch.float64)
     out = torch.empty(1, dtype=torch.float64, device="cuda")
-    ws = _lib.workspace(L.plas_aux_workspace_bytes(1, 1, 1), "aux")
+    ws = _lib.workspace(L.plas_grid_distance_workspace_bytes(n), "gdist")
     _lib.check(L.plas_grid_distance(_lib.ptr(a), _lib.ptr(b), _lib.ptr(w), n, D, _lib.ptr(out),
                                     _lib.ptr(ws), ws.numel(), _lib.stream_handle()), "grid_distance")
     return float(out.item())
