@@ -13,7 +13,7 @@
  *   plas.py:173-193  reassign_block                          -> oracle_reassign_block
  *   plas.py:113-156  _assign_groups (numba arithmetic)       -> oracle_assign_groups
  *   plas.py:64-68 + blur.py:7-30  blur_target / renormalized_blur (SciPy correlate1d order)
- *   plas.py:71-84    grid_distance                           -> oracle_grid_distance
+ *   plas.py:71-84    grid_distance (NumPy pairwise order)    -> oracle_grid_distance_f32
  *   metrics.py:25-40 vad                                     -> oracle_vad
  *   smoothness.py:57-97 smoothness_loss (one plane)          -> oracle_smoothness_plane
  * and the third-party arithmetic the path delegates to:
@@ -388,17 +388,49 @@ void oracle_reassign_block(float *feat, int64_t *idx, const float *target, int D
 /* ------------------------------------------------------------------ */
 /* grid_distance (plas.py:71-84) and vad (metrics.py:25-40)            */
 /* ------------------------------------------------------------------ */
+/* NumPy's pairwise_sum (numpy/_core/src/umath/loops_utils.h.src), which
+ * np.sum / np.mean use on contiguous float64 runs: m < 8 -> plain loop from
+ * 0.0; m <= 128 -> eight running sums over the multiples of 8, combined
+ * ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)), then the tail in order;
+ * m > 128 -> split at m2 = m / 2 rounded down to a multiple of 8.  grid_distance
+ * (plas.py:83) is np.sqrt((diff ** 2).sum(axis=1)).mean(): row sums over D,
+ * then the mean over n in this order.  Compile without FMA contraction
+ * (-ffp-contract=off). */
+static double np_pairwise(const double *a, int64_t m) {
+    if (m < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < m; i++) res += a[i];
+        return res;
+    }
+    if (m <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int64_t i = 8;
+        for (; i < m - (m % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < m; i++) res += a[i];
+        return res;
+    }
+    int64_t m2 = m / 2;
+    m2 -= m2 % 8;
+    return np_pairwise(a, m2) + np_pairwise(a + m2, m - m2);
+}
+
 double oracle_grid_distance_f32(const float *a, const float *b, int64_t n, int D, int S) {
-    double total = 0.0;
+    double *cell = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *sq = (double *)malloc(sizeof(double) * (size_t)(D > 0 ? D : 1));
     for (int64_t i = 0; i < n; i++) {
-        double s = 0.0;
         for (int d = 0; d < D; d++) {
             double df = (double)a[i * S + d] - (double)b[i * S + d];
-            s += df * df;
+            sq[d] = df * df;
         }
-        total += sqrt(s);
+        cell[i] = sqrt(np_pairwise(sq, D));
     }
-    return total / (double)n;
+    double mean = np_pairwise(cell, n) / (double)n;
+    free(cell);
+    free(sq);
+    return mean;
 }
 
 double oracle_vad_f32(const float *g, int H, int W, int C, int S) {
