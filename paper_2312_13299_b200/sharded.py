@@ -43,6 +43,38 @@ class ShardSpec:
     exchange: object  # callable(send, recv, part, part_all) -> m
 
 
+def level_bands(side, beta, world):
+    """Per rank (own_lo, own_hi, band_lo, band_hi) rows of a level and whether it
+    is banded (host mirror of plas_sort's level set-up): banded when
+    beta * world <= side; own rows [side r / world, side (r+1) / world); the
+    target band adds the beta rows a block can reach below them.  Replicated
+    levels keep the whole grid as band."""
+    banded = beta * world <= side
+    out = []
+    for r in range(world):
+        lo, hi = side * r // world, side * (r + 1) // world
+        out.append((lo, hi, lo if banded else 0, min(side, hi + beta) if banded else side))
+    return banded, out
+
+
+def banded_block_rows(side, beta, dy, world, rank):
+    """This rank's [by_lo, by_hi) block rows of a banded pass with offset dy
+    (host mirror of common.cuh set_pass_geometry_base): the block rows whose
+    first row y0(by) (0 for by = 0, first_y + (by - 1) beta after) lies in the
+    rank's own rows."""
+    first_y = dy if dy > 0 else beta
+    nby = 1 + (side - first_y + beta - 1) // beta if first_y < side else 1
+
+    def first_by(Y):
+        if Y <= 0:
+            return 0
+        by = 1 if Y <= first_y else 1 + (Y - first_y + beta - 1) // beta
+        return min(by, nby)
+
+    own_lo, own_hi = side * rank // world, side * (rank + 1) // world
+    return first_by(own_lo), (nby if own_hi >= side else first_by(own_hi)), nby
+
+
 def shard_ranges(total_groups, nblocks, rank, world):
     """This rank's [g_lo, g_hi) groups and [b_lo, b_hi) blocks of a pass
     (host mirror of common.cuh set_pass_geometry_base)."""

@@ -26,6 +26,33 @@ def test_shard_ranges_partition(world):
         assert max(sizes) - min(sizes) <= 1
 
 
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_banded_block_rows_partition(world):
+    """Banded passes: the ranks' block-row ranges partition the pass's block rows
+    for every offset dy, and every cell a rank processes lies inside the target
+    band it computed for the level (rows [own_lo, own_hi + beta))."""
+    for side in (64, 96, 512, 1000, 1024, 4096):
+        for beta in (16, 17, 33, 64, 128, 512):
+            banded, bands = sharded.level_bands(side, beta, world)
+            if not banded:
+                assert all(b[2] == 0 and b[3] == side for b in bands)
+                continue
+            for dy in sorted({0, 1, beta // 2, beta - 1}):
+                first_y = dy if dy > 0 else beta
+                ranges = [sharded.banded_block_rows(side, beta, dy, world, r) for r in range(world)]
+                nby = ranges[0][2]
+                assert ranges[0][0] == 0 and ranges[-1][1] == nby
+                for a, b in zip(ranges, ranges[1:]):
+                    assert a[1] == b[0]
+                for r, (lo, hi, _) in enumerate(ranges):
+                    if lo == hi:
+                        continue
+                    y_first = 0 if lo == 0 else first_y + (lo - 1) * beta
+                    y_end = min(side, first_y + (hi - 1) * beta)  # end row of block row hi - 1
+                    _, _, band_lo, band_hi = bands[r]
+                    assert band_lo <= y_first and y_end <= band_hi, (side, beta, dy, world, r)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
