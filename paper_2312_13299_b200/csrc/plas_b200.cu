@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <memory>
 #include <mutex>
@@ -68,12 +69,12 @@ int fail(int code, const std::string& msg) {
 constexpr int MAX_PARTS = 4096;
 
 int num_sms() {
-  static int sms = 0;
+  static std::atomic<int> sms{0};  // lazily initialised caches: atomics, written with the same value by any thread
   if (!sms) {
-    int dev = 0;
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms = v > 0 ? v : 148;
   }
   return sms;
 }
@@ -235,7 +236,7 @@ PadFn pad_small_fn(int axis) {
   return axis == 0 ? (PadFn)blur_pad_kernel<0, 0, H> : (PadFn)blur_pad_kernel<1, 1, H>;
 }
 int pad_small_enabled() {
-  static int v = -1;
+  static std::atomic<int> v{-1};
   if (v < 0) v = getenv("PLAS_PAD_SMALL") ? (atoi(getenv("PLAS_PAD_SMALL")) != 0) : 1;
   return v;
 }
@@ -295,7 +296,7 @@ int fft_threads(int L) { return fft_threads_len(L); }
 // (1.895 vs 2.033 s), 1280 loses to 1536 at C2 (114.9 vs 114.3 ms), so 5 * 2^8
 // is not offered; the 9 * 2^k lengths (radix-3 twice) lost at every config.
 int fft_choose_code(long long n, long long hmax) {
-  static int odd_mask = -1;
+  static std::atomic<int> odd_mask{-1};
   if (odd_mask < 0) {
     const char* e = getenv("PLAS_FFT3");
     odd_mask = e ? (atoi(e) & 3) : 3;
@@ -338,7 +339,7 @@ void fft_plan_codes(int side, int S, int* count, int* codes) {
 // PLAS_FFT_MIN_H overrides.  Measured crossovers: 48 at C2 (L = 1536: 114.7 vs
 // 115.5 ms at 64), 64 at C4 (L = 6144: 2.625 vs 2.641 s at 48).
 int fft_min_h(int L, int S) {
-  static int v = -2;
+  static std::atomic<int> v{-2};
   if (v == -2) {
     const char* e = getenv("PLAS_FFT_MIN_H");
     v = e ? std::max(atoi(e), 0) : -1;
@@ -354,7 +355,7 @@ int fft_min_h(int L, int S) {
 // 1.69 s without the tile tier, 1.75 s with h <= 2, 1.80 s with h <= 4 -- the
 // tile kernel reads each row once per channel pair, ~10x its algorithmic bytes)
 int tile_blur_hmax(int S) {
-  static int v = -2;
+  static std::atomic<int> v{-2};
   if (v == -2) {
     const char* e = getenv("PLAS_TILE_BLUR_HMAX");
     v = e ? std::min(std::max(atoi(e), 0), TB_HMAX) : -1;
@@ -567,7 +568,7 @@ struct Launch {
 
 // PLAS_K3_PLAIN=1 selects the unpipelined gather kernel for rows <= 16 floats (A/B)
 bool k3_plain() {
-  static int v = -1;
+  static std::atomic<int> v{-1};
   if (v < 0) v = getenv("PLAS_K3_PLAIN") && atoi(getenv("PLAS_K3_PLAIN")) ? 1 : 0;
   return v == 1;
 }
@@ -578,7 +579,7 @@ void* pass_kernel_ptr(int S) {
 }
 
 int pass_grid_size(int S) {
-  static int cached[3] = {0, 0, 0};
+  static std::atomic<int> cached[3];
   int which = S <= 16 ? 0 : 1;
   if (!cached[which]) {
     int occ = 0;
@@ -633,7 +634,7 @@ void graph_cache_put(const GraphKey& k, const GraphExecRef& ge) {
 
 // passes per iteration of the graph's pass loop (PLAS_PASS_UNROLL, default 3: measured 1 -> 122.1, 2 -> 120.2, 3 -> 119.6, 4 -> 120.0 ms at C2)
 int pass_unroll() {
-  static int v = 0;
+  static std::atomic<int> v{0};
   if (!v) {
     const char* e = getenv("PLAS_PASS_UNROLL");
     v = e ? std::max(1, std::min(8, atoi(e))) : 3;
@@ -667,7 +668,7 @@ int tile_beta_max(int S) {
 size_t tile_smem_bytes(int S) { return (size_t)(TILE_NST * tile_stage_bytes(tile_beta_max(S), S)); }
 
 int tile_grid_size(int S) {
-  static int cached[65] = {0};
+  static std::atomic<int> cached[65];
   const int key = S <= 64 ? S : 64;
   // the attribute is per kernel, so set it for this S on every sort
   const size_t smem = tile_smem_bytes(S);
@@ -686,7 +687,7 @@ int tile_grid_size(int S) {
 long long list_capacity(long long n) { return n; }
 
 int stats_grid_size() {
-  static int g = 0;
+  static std::atomic<int> g{0};
   if (!g) {
     const char* e = getenv("PLAS_STATS_CTAS_PER_SM");
     // measured (C2 / C3 / C4): 1 -> 116.1 ms; 2 -> 115.1 ms / 1.655 s / 2.608 s;
