@@ -666,3 +666,22 @@ def test_grid_distance_numpy_order_exact():
         wts = rng.uniform(0.0, 2.0, D)
         want_w = float(np.sqrt((((a - b) * wts) ** 2).sum(axis=1)).mean())
         assert plas.grid_distance(a, b, weights=wts) == want_w, (n, D)
+
+
+@pytest.mark.parametrize("mode", ["parity", "device"])
+def test_lazy_index_reads_same_sort(mode):
+    """Large grids read element indices only for moving cells (Ctrl.lazy_idx,
+    on by size); forced on for a small grid it must give the same sort."""
+    import os
+    f = synthetic.c1(0, side=96)
+    cfg = plas.SortConfig(rng_seed=4, rng_mode=mode)
+    out = []
+    for v in ("0", "1"):
+        os.environ["PLAS_LAZY_IDX"] = v
+        try:
+            out.append(plas.sort_grid_report(f, cfg))
+        finally:
+            del os.environ["PLAS_LAZY_IDX"]
+    (p0, r0), (p1, r1) = out
+    np.testing.assert_array_equal(p0, p1)
+    assert r0.reorders == r1.reorders and r0.radius_trace == r1.radius_trace
