@@ -311,6 +311,51 @@ def ncu_traffic(config, prefixes=("pass_kernel", "pass_kernel_pipe", "tile_pass_
         return None
 
 
+# fp64 peak of this pool's B200 for the blur's compute roof: tools/fp64_micro.cu
+# measured DADD / DMUL / DFMA at 18.4 Gop/s x 1e3 each (64 per clock per SM at
+# 1.965 GHz), i.e. 36.8 TFLOP/s counting an FMA as two (profiles/r02_fp64_peak.txt)
+FP64_PEAK_TFLOPS = 36.8
+
+
+def _fft_len_for(side, h):
+    """plas_b200.cu fft_choose_code: the shortest 2^k (5..13), 3 2^k (9..11) or
+    5 2^k (9..10) with side + h <= L and side <= the length's output capacity."""
+    best = None
+    for k in range(5, 14):
+        L = 1 << k
+        if side + h <= L and side <= L // 2:
+            best = L if best is None else min(best, L)
+    for m, ks, cap in ((3, range(9, 12), 2), (5, range(9, 11), 4)):
+        for k in ks:
+            L = m << k
+            if side + h <= L and side <= cap << k:
+                best = L if best is None else min(best, L)
+    return best
+
+
+def blur_flops(side, D, radii):
+    """fp64 flops of the sort's level blurs under the library's tier rules
+    (plas_b200.cu: FFT from h >= 48 / 64 (40 for rows wider than 16 floats)
+    while side + h fits the longest length; the one-kernel tile tier for h <= 4
+    on rows of <= 16 floats; the direct fold otherwise).  Direct / tile: 3h + 1
+    per output and axis (a DADD and a DFMA per tap pair, the centre product);
+    FFT: two complex transforms of 5 L log2 L per line pair and axis."""
+    S = (D + 3) // 4 * 4
+    h0 = math.ceil(max(side / 2.0 - 1.0, 2.0))
+    L_top = _fft_len_for(side, h0)
+    min_h = 40 if S > 16 else (48 if (L_top or 0) <= 2048 else 64)
+    pairs = side * ((D + 1) // 2)
+    total = 0.0
+    for r in radii:
+        h = math.ceil(r)
+        if L_top and h >= min_h and side + h <= L_top:
+            L = _fft_len_for(side, h) or L_top
+            total += 2 * pairs * 2 * 5 * L * math.log2(L)
+        else:
+            total += 2 * side * side * D * (3 * h + 1)
+    return total
+
+
 def run_smoothness(feats, perm_np, side, device, peak, steps=5):
     """Smoothness-loss fwd+bwd (smoothness.py:57-97) on the sorted grid, default
     SmoothnessParams (opacity 0.09, rotation 0.91: C_w = 5 channels), fp64 as the
@@ -566,6 +611,14 @@ def run_ours(args):
         alg_blur = n * 8 * D
         b_avg = (prof.ms_blur0 + prof.ms_blur1) / max(1, prof.n_blur0 + prof.n_blur1) / 1e3
         roofline["blur_hbm_frac"] = round(alg_blur / b_avg / 1e9 / peak, 4) if b_avg else None
+        # ... and against its compute roof: analytic fp64 flops of every level's
+        # blur over the blur kernels' CUDA-event time
+        flops = blur_flops(side, D, [r for r, _ in rep["radius_trace"]])
+        tf = flops / (blur_total / 1e3) / 1e12 if blur_total else None
+        roofline["blur_fp64"] = {"flops_per_sort": flops, "achieved_tflops": round(tf, 2) if tf else None,
+                                 "peak_tflops": FP64_PEAK_TFLOPS, "frac": round(tf / FP64_PEAK_TFLOPS, 4) if tf else None,
+                                 "peak_source": "tools/fp64_micro.cu on this pool's B200 (DFMA 64/clk/SM), "
+                                                "profiles/r02_fp64_peak.txt"}
 
     smooth = None
     if args.config == "C2" and not args.no_smoothness:
