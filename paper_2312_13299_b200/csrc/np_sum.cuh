@@ -97,17 +97,16 @@ struct NpTree {
   int root = 0;
   long long n = 0;
 };
-inline int np_tree_build(NpTree* t, long long off, long long m, std::vector<int>* height) {
+inline int np_tree_build(NpTree* t, long long off, long long m) {
   if (m <= 128) {
     t->leaf_start.push_back(off);
     t->leaf_len.push_back((int)m);
-    height->push_back(-1);  // placeholder, leaves are renumbered below
     return -(int)t->leaf_start.size();  // leaf k -> -(k + 1)
   }
   long long m2 = m / 2;
   m2 -= m2 % 8;
-  const int l = np_tree_build(t, off, m2, height);
-  const int r = np_tree_build(t, off + m2, m - m2, height);
+  const int l = np_tree_build(t, off, m2);
+  const int r = np_tree_build(t, off + m2, m - m2);
   t->left.push_back(l);
   t->right.push_back(r);
   return (int)t->left.size() - 1;  // internal k -> k
@@ -120,8 +119,7 @@ inline void np_tree_make(NpTree* t, long long n) {
   t->order.clear();
   t->hoff.clear();
   t->n = n;
-  std::vector<int> dummy;
-  const int root = np_tree_build(t, 0, n, &dummy);
+  const int root = np_tree_build(t, 0, n);
   const int L = (int)t->leaf_start.size(), I = (int)t->left.size();
   auto idx = [&](int v) { return v < 0 ? (-v - 1) : L + v; };  // node index in the value array
   for (int k = 0; k < I; k++) {
@@ -129,7 +127,8 @@ inline void np_tree_make(NpTree* t, long long n) {
     t->right[k] = idx(t->right[k]);
   }
   t->root = idx(root);
-  // heights (children precede parents in construction order)
+  // heights (children precede parents in construction order), then the
+  // internal nodes bucketed by height (counting sort)
   std::vector<int> h(L + I, 0);
   int hmax = 0;
   for (int k = 0; k < I; k++) {
@@ -137,12 +136,17 @@ inline void np_tree_make(NpTree* t, long long n) {
     hmax = std::max(hmax, h[L + k]);
   }
   t->hoff.assign(hmax + 1, 0);
+  for (int k = 0; k < I; k++) t->hoff[h[L + k]]++;  // hoff[lev] counts height lev (1..hmax)
+  int acc = 0;
   for (int lev = 1; lev <= hmax; lev++) {
-    t->hoff[lev - 1] = (int)t->order.size();
-    for (int k = 0; k < I; k++)
-      if (h[L + k] == lev) t->order.push_back(k);
+    const int c = t->hoff[lev];
+    t->hoff[lev - 1] = acc;
+    acc += c;
   }
-  t->hoff[hmax] = (int)t->order.size();
+  t->hoff[hmax] = acc;
+  t->order.assign(I, 0);
+  std::vector<int> pos(t->hoff.begin(), t->hoff.end());
+  for (int k = 0; k < I; k++) t->order[pos[h[L + k] - 1]++] = k;
 }
 
 // leaf sums: vals[k] = pairwise sum of v[leaf_start[k] .. + leaf_len[k])
@@ -173,6 +177,60 @@ __global__ void __launch_bounds__(1024) np_tree_kernel(double* __restrict__ vals
     const double tot = vals[root];
     out[0] = tot;
     out[1] = __ddiv_rn(tot, (double)n);
+  }
+}
+
+// vad (metrics.py:25-40) in NumPy's order: diffs = concatenate(|diff(g, axis=0)|
+// in C order of (H-1, W, C), |diff(g, axis=1)| in C order of (H, W-1, C));
+// var = pairwise((d - mean)^2) / M with mean = pairwise(d) / M (numpy _var:
+// sum, true_divide, subtract, multiply, sum, true_divide).  Element e of the
+// pooled array is formed on the fly from the fp32 grid (row stride S).
+struct VadElems {
+  const float* g;
+  unsigned H, W, C, S;
+  unsigned long long m0;  // (H - 1) W C axis-0 differences first
+  __device__ __forceinline__ double operator()(unsigned long long e) const {
+    unsigned long long y, x, c;
+    const float* a;
+    const float* b;
+    if (e < m0) {
+      const unsigned long long wc = (unsigned long long)W * C;
+      y = e / wc;
+      const unsigned long long r = e - y * wc;
+      x = r / C;
+      c = r - x * C;
+      a = g + ((y + 1) * W + x) * S + c;
+      b = g + (y * W + x) * S + c;
+    } else {
+      e -= m0;
+      const unsigned long long wc = (unsigned long long)(W - 1) * C;
+      y = e / wc;
+      const unsigned long long r = e - y * wc;
+      x = r / C;
+      c = r - x * C;
+      a = g + (y * W + x + 1) * S + c;
+      b = g + (y * W + x) * S + c;
+    }
+    return fabs(__dsub_rn((double)__ldg(a), (double)__ldg(b)));
+  }
+};
+// leaf sums of the pooled differences (PASS 0) or of their squared deviations
+// from mean[1] (PASS 1)
+template <int PASS>
+__global__ void __launch_bounds__(256) np_leaf_vad_kernel(VadElems el, const double* __restrict__ mean,
+                                                          const long long* __restrict__ leaf_start,
+                                                          const int* __restrict__ leaf_len, int nleaves,
+                                                          double* __restrict__ vals) {
+  const double mu = PASS ? mean[1] : 0.0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nleaves; k += gridDim.x * blockDim.x) {
+    const unsigned long long e0 = (unsigned long long)leaf_start[k];
+    auto val = [&](int i) {
+      const double d = el(e0 + (unsigned long long)i);
+      if (PASS == 0) return d;
+      const double x = __dsub_rn(d, mu);
+      return __dmul_rn(x, x);
+    };
+    vals[k] = np_pairwise_small(val, leaf_len[k]);
   }
 }
 

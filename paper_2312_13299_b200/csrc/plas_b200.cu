@@ -215,6 +215,12 @@ struct SortWs {
   long long* np_lstart;  // leaf starts
   int *np_llen, *np_left, *np_right, *np_order, *np_hoff;
   double* np_out;        // (sum, sum / n)
+  // PARITY: NumPy-order vad over M = 2 side (side - 1) D pooled differences
+  size_t vad_cap;        // tree leaves the arrays hold
+  double* vad_vals;
+  long long* vad_lstart;
+  int *vad_llen, *vad_left, *vad_right, *vad_order, *vad_hoff;
+  double* vad_out;       // (sum, mean, sum of squares, var)
   // FFT tier: up to FFT_PLANS lengths (the shortest that fits each level's h)
   int fft_count;                   // number of lengths
   int fft_codes[4];                // length codes, increasing length
@@ -462,6 +468,16 @@ size_t carve_sort(char* base, long long n, int dim, int L, long long wlen, long 
   w->np_order = c.take<int>(nleaf);
   w->np_hoff = c.take<int>(72);
   w->np_out = c.take<double>(2);
+  const long long mv = 2LL * side * (side - 1) * dim;
+  w->vad_cap = rng_mode == PLAS_RNG_PARITY ? (size_t)(mv / 64 + 4) : 1;
+  w->vad_vals = c.take<double>(2 * w->vad_cap);
+  w->vad_lstart = c.take<long long>(w->vad_cap);
+  w->vad_llen = c.take<int>(w->vad_cap);
+  w->vad_left = c.take<int>(w->vad_cap);
+  w->vad_right = c.take<int>(w->vad_cap);
+  w->vad_order = c.take<int>(w->vad_cap);
+  w->vad_hoff = c.take<int>(72);
+  w->vad_out = c.take<double>(4);
   fft_plan_codes(side, row_stride(dim), &w->fft_count, w->fft_codes);
   w->fft_L = w->fft_count ? fft_len(w->fft_codes[w->fft_count - 1]) : 0;
   for (int i = 0; i < 4; i++)
@@ -977,7 +993,41 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
     CK(raise_smem_limit((const void*)blur_tile_kernel, tile_blur_smem_bytes(hc.tile_blur_hmax)));
   lc.sched = Sched{w.radii, w.betas, w.hs, w.level_counts, w.trace};
 
+  // PARITY: the reference's vad float (NumPy order over the pooled
+  // differences, np_sum.cuh); the tree over M = 2 side (side - 1) D values is
+  // built once per size
+  NpTree vtree;
+  const bool np_vad = mode == PLAS_RNG_PARITY && !getenv("PLAS_NP_VAD_OFF");
+  if (np_vad) {
+    np_tree_make(&vtree, 2LL * side * (side - 1) * D);
+    const size_t nl = vtree.leaf_start.size(), ni = vtree.left.size();
+    if (nl > w.vad_cap || vtree.hoff.size() > 72) return fail(PLAS_ERR_INVALID, "vad tree sizing");
+    CK(cudaMemcpyAsync(w.vad_lstart, vtree.leaf_start.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.vad_llen, vtree.leaf_len.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st));
+    if (ni) {
+      CK(cudaMemcpyAsync(w.vad_left, vtree.left.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(w.vad_right, vtree.right.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(w.vad_order, vtree.order.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(w.vad_hoff, vtree.hoff.data(), sizeof(int) * vtree.hoff.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // the host tree vectors live on this frame only
+  }
   auto vad_launch = [&](double* out) -> int {
+    if (np_vad) {
+      const VadElems el{w.feat, (unsigned)side, (unsigned)side, (unsigned)D, (unsigned)S,
+                        (unsigned long long)(side - 1) * side * D};
+      const int nl = (int)vtree.leaf_start.size(), lg = std::max(1, (nl + 255) / 256);
+      const long long M = 2LL * side * (side - 1) * D;
+      np_leaf_vad_kernel<0><<<lg, 256, 0, st>>>(el, nullptr, w.vad_lstart, w.vad_llen, nl, w.vad_vals);
+      np_tree_kernel<<<1, 1024, 0, st>>>(w.vad_vals, w.vad_left, w.vad_right, w.vad_order, w.vad_hoff,
+                                         (int)vtree.hoff.size() - 1, nl, vtree.root, M, w.vad_out);
+      np_leaf_vad_kernel<1><<<lg, 256, 0, st>>>(el, w.vad_out, w.vad_lstart, w.vad_llen, nl, w.vad_vals);
+      np_tree_kernel<<<1, 1024, 0, st>>>(w.vad_vals, w.vad_left, w.vad_right, w.vad_order, w.vad_hoff,
+                                         (int)vtree.hoff.size() - 1, nl, vtree.root, M, w.vad_out + 2);
+      CK(cudaMemcpyAsync(out, w.vad_out + 3, sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CKL();
+      return 0;
+    }
     vad_kernel<float><<<lc.vad_grid, RED_THREADS, 0, st>>>(w.feat, side, side, D, S, nullptr, w.partials);
     mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(w.partials, lc.vad_grid,
                                                     2.0 * side * (side - 1) * (double)D, w.scalars);
