@@ -205,7 +205,10 @@ size_t plas_grid_distance_workspace_bytes(int64_t n);
 int plas_grid_distance(const double* a, const double* b, const double* weights, int64_t n, int dim,
                        double* out_dev, void* ws, size_t ws_bytes, void* stream);
 
-/* vad (metrics.py:25-40) of an (H, W, C) grid; result to *out_dev. */
+/* vad (metrics.py:25-40) of an (H, W, C) grid (PLAS_F32 or PLAS_F64) in
+ * NumPy's summation order: the reference's float; result to *out_dev; ws of
+ * plas_vad_workspace_bytes(H, W, C) bytes. */
+size_t plas_vad_workspace_bytes(int H, int W, int C);
 int plas_vad(const void* grid, int dtype, int H, int W, int C, double* out_dev, void* ws,
              size_t ws_bytes, void* stream);
 

@@ -89,6 +89,7 @@ SIGNATURES = {
     "plas_blur_target_tiers": (i32, [P, P, i32, i32, i32, P, i32, i32, P, P, sz, P]),
     "plas_grid_distance_workspace_bytes": (sz, [i64]),
     "plas_grid_distance": (i32, [P, P, P, i64, i32, P, P, sz, P]),
+    "plas_vad_workspace_bytes": (sz, [i32, i32, i32]),
     "plas_vad": (i32, [P, i32, i32, i32, i32, P, P, sz, P]),
     "plas_smoothness_plane": (i32, [P, P, i32, i32, i32, f64, f64, i32, P, i32, P, P, sz, P]),
     "plas_prune_workspace_bytes": (sz, [i64]),

@@ -185,14 +185,15 @@ __global__ void __launch_bounds__(1024) np_tree_kernel(double* __restrict__ vals
 // var = pairwise((d - mean)^2) / M with mean = pairwise(d) / M (numpy _var:
 // sum, true_divide, subtract, multiply, sum, true_divide).  Element e of the
 // pooled array is formed on the fly from the fp32 grid (row stride S).
+template <typename T = float>
 struct VadElems {
-  const float* g;
+  const T* g;
   unsigned H, W, C, S;
   unsigned long long m0;  // (H - 1) W C axis-0 differences first
   __device__ __forceinline__ double operator()(unsigned long long e) const {
     unsigned long long y, x, c;
-    const float* a;
-    const float* b;
+    const T* a;
+    const T* b;
     if (e < m0) {
       const unsigned long long wc = (unsigned long long)W * C;
       y = e / wc;
@@ -216,8 +217,8 @@ struct VadElems {
 };
 // leaf sums of the pooled differences (PASS 0) or of their squared deviations
 // from mean[1] (PASS 1)
-template <int PASS>
-__global__ void __launch_bounds__(256) np_leaf_vad_kernel(VadElems el, const double* __restrict__ mean,
+template <int PASS, typename T = float>
+__global__ void __launch_bounds__(256) np_leaf_vad_kernel(VadElems<T> el, const double* __restrict__ mean,
                                                           const long long* __restrict__ leaf_start,
                                                           const int* __restrict__ leaf_len, int nleaves,
                                                           double* __restrict__ vals) {

@@ -1014,7 +1014,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   }
   auto vad_launch = [&](double* out) -> int {
     if (np_vad) {
-      const VadElems el{w.feat, (unsigned)side, (unsigned)side, (unsigned)D, (unsigned)S,
+      const VadElems<float> el{w.feat, (unsigned)side, (unsigned)side, (unsigned)D, (unsigned)S,
                         (unsigned long long)(side - 1) * side * D};
       const int nl = (int)vtree.leaf_start.size(), lg = std::max(1, (nl + 255) / 256);
       const long long M = 2LL * side * (side - 1) * D;
@@ -1886,10 +1886,10 @@ int plas_blur(const void* in, void* out, int dtype, int H, int W, int C, const d
 
 // workspace of plas_grid_distance: per-cell values + the NumPy tree
 static size_t carve_np(char* base, long long n, double** v, double** vals, long long** lstart, int** llen,
-                       int** left, int** right, int** order, int** hoff, double** out) {
+                       int** left, int** right, int** order, int** hoff, double** out, bool with_v = true) {
   Carver c{base};
   const size_t nleaf = (size_t)(n / 64 + 4);
-  *v = c.take<double>((size_t)n);
+  *v = c.take<double>(with_v ? (size_t)n : 1);
   *vals = c.take<double>(2 * nleaf);
   *lstart = c.take<long long>(nleaf);
   *llen = c.take<int>(nleaf);
@@ -1938,25 +1938,54 @@ int plas_grid_distance(const double* a, const double* b, const double* weights, 
   return PLAS_OK;
 }
 
+size_t plas_vad_workspace_bytes(int H, int W, int C) {
+  const long long m = std::max<long long>(1, (long long)(H - 1) * W * C + (long long)H * (W - 1) * C);
+  double *v, *vals, *out;
+  long long* ls;
+  int *ll, *l, *r, *o, *h;
+  return carve_np(nullptr, m, &v, &vals, &ls, &ll, &l, &r, &o, &h, &out, false) + sizeof(double) * 8;
+}
+
+// vad (metrics.py:25-40) in NumPy's order (np_sum.cuh VadElems): the
+// reference's float for fp32 and fp64 grids
 int plas_vad(const void* grid, int dtype, int H, int W, int C, double* out_dev, void* ws,
              size_t ws_bytes, void* stream) {
   if (H < 2 || W < 2 || C < 1) return fail(PLAS_ERR_INVALID, "vad needs H, W >= 2");
-  if (!ws || ws_bytes < sizeof(double) * (MAX_PARTS + 8)) return fail(PLAS_ERR_WORKSPACE, "aux workspace");
+  if (!ws || ws_bytes < plas_vad_workspace_bytes(H, W, C)) return fail(PLAS_ERR_WORKSPACE, "vad workspace");
   cudaStream_t st = (cudaStream_t)stream;
-  double* partials = (double*)ws;
-  double* mean = partials + MAX_PARTS;
-  const double count = ((double)(H - 1) * W + (double)H * (W - 1)) * C;
-  int g = grid_for((long long)H * W * C, RED_THREADS, 4);
-  if (dtype == PLAS_F32) {
-    vad_kernel<float><<<g, RED_THREADS, 0, st>>>((const float*)grid, H, W, C, C, nullptr, partials);
-    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, g, count, mean);
-    vad_kernel<float><<<g, RED_THREADS, 0, st>>>((const float*)grid, H, W, C, C, mean, partials);
-  } else {
-    vad_kernel<double><<<g, RED_THREADS, 0, st>>>((const double*)grid, H, W, C, C, nullptr, partials);
-    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, g, count, mean);
-    vad_kernel<double><<<g, RED_THREADS, 0, st>>>((const double*)grid, H, W, C, C, mean, partials);
+  const long long M = (long long)(H - 1) * W * C + (long long)H * (W - 1) * C;
+  double *v, *vals, *out;
+  long long* ls;
+  int *ll, *l, *r, *o, *h;
+  carve_np((char*)ws, M, &v, &vals, &ls, &ll, &l, &r, &o, &h, &out, false);  // values formed on the fly
+  double* out4 = (double*)((char*)ws + plas_vad_workspace_bytes(H, W, C) - sizeof(double) * 8);
+  NpTree t;
+  np_tree_make(&t, M);
+  const size_t nl = t.leaf_start.size(), ni = t.left.size();
+  CK(cudaMemcpyAsync(ls, t.leaf_start.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ll, t.leaf_len.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st));
+  if (ni) {
+    CK(cudaMemcpyAsync(l, t.left.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(r, t.right.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(o, t.order.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
   }
-  mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(partials, g, count, out_dev);
+  CK(cudaMemcpyAsync(h, t.hoff.data(), sizeof(int) * t.hoff.size(), cudaMemcpyHostToDevice, st));
+  const int lg = std::max(1, (int)((nl + 255) / 256)), nh = (int)t.hoff.size() - 1;
+  const unsigned long long m0 = (unsigned long long)(H - 1) * W * C;
+  if (dtype == PLAS_F32) {
+    const VadElems<float> el{(const float*)grid, (unsigned)H, (unsigned)W, (unsigned)C, (unsigned)C, m0};
+    np_leaf_vad_kernel<0, float><<<lg, 256, 0, st>>>(el, nullptr, ls, ll, (int)nl, vals);
+    np_tree_kernel<<<1, 1024, 0, st>>>(vals, l, r, o, h, nh, (int)nl, t.root, M, out4);
+    np_leaf_vad_kernel<1, float><<<lg, 256, 0, st>>>(el, out4, ls, ll, (int)nl, vals);
+  } else {
+    const VadElems<double> el{(const double*)grid, (unsigned)H, (unsigned)W, (unsigned)C, (unsigned)C, m0};
+    np_leaf_vad_kernel<0, double><<<lg, 256, 0, st>>>(el, nullptr, ls, ll, (int)nl, vals);
+    np_tree_kernel<<<1, 1024, 0, st>>>(vals, l, r, o, h, nh, (int)nl, t.root, M, out4);
+    np_leaf_vad_kernel<1, double><<<lg, 256, 0, st>>>(el, out4, ls, ll, (int)nl, vals);
+  }
+  np_tree_kernel<<<1, 1024, 0, st>>>(vals, l, r, o, h, nh, (int)nl, t.root, M, out4 + 2);
+  CK(cudaMemcpyAsync(out_dev, out4 + 3, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));  // the host tree vectors live on this frame only
   CKL();
   return PLAS_OK;
 }

@@ -145,11 +145,10 @@ def test_blur_semantics():
 def test_vad_and_grid_distance_golden():
     z = golden_npz("metrics.npz")
     for i in range(5):
-        assert plas.vad(z[f"vad_in{i}"]) == pytest.approx(float(z[f"vad_out{i}"]), rel=1e-12)
+        assert plas.vad(z[f"vad_in{i}"]) == float(z[f"vad_out{i}"])  # NumPy order: exact
     for i in range(3):
         assert plas.grid_distance(z[f"gd_a{i}"], z[f"gd_b{i}"]) == float(z[f"gd_out{i}"])  # NumPy order: exact
-        assert plas.grid_distance(z[f"gd_a{i}"], z[f"gd_b{i}"], weights=z[f"gd_w{i}"]) == pytest.approx(
-            float(z[f"gd_outw{i}"]), rel=1e-12)
+        assert plas.grid_distance(z[f"gd_a{i}"], z[f"gd_b{i}"], weights=z[f"gd_w{i}"]) == float(z[f"gd_outw{i}"])
     assert plas.grid_distance(np.array([[0.0, 0.0], [3.0, 4.0]]), np.zeros((2, 2))) == pytest.approx(2.5)
     with pytest.raises(ValueError):
         plas.grid_distance(np.zeros((2, 3)), np.zeros((3, 3)))
@@ -686,3 +685,18 @@ def test_lazy_index_reads_same_sort(mode):
     (p0, r0), (p1, r1) = out
     np.testing.assert_array_equal(p0, p1)
     assert r0.reorders == r1.reorders and r0.radius_trace == r1.radius_trace
+
+
+def test_vad_numpy_order_exact():
+    """vad (metrics.py:25-40) in NumPy's order on the GPU: the reference's float
+    (np.concatenate of |diff| along both axes, then .var()) for fp32 and fp64
+    grids of odd and block-boundary sizes, 1 to 14 channels."""
+    rng = np.random.default_rng(43)
+    for H, W, C in ((2, 2, 1), (3, 5, 1), (7, 9, 3), (16, 16, 14), (33, 65, 6), (256, 255, 3), (1024, 1024, 14)):
+        for dt in (np.float64, np.float32):
+            g = (rng.normal(0, 1, (H, W, C)) * rng.uniform(0.1, 5.0, (1, 1, C))).astype(dt)
+            g64 = np.asarray(g, dtype=np.float64)
+            want = float(np.concatenate([np.abs(np.diff(g64, axis=0)).reshape(-1),
+                                         np.abs(np.diff(g64, axis=1)).reshape(-1)]).var())
+            got = plas.vad(g if C > 1 else g[..., 0])
+            assert got == want, (H, W, C, dt)
