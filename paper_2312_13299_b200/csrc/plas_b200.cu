@@ -1663,22 +1663,50 @@ int plas_assign_groups_f64t(float* feat, int64_t* point_idx, const double* targe
   return PLAS_OK;
 }
 
-size_t plas_aux_workspace_bytes(int H, int W, int C) {
-  size_t cells = (size_t)H * W, tot = cells * C;
-  size_t b = 0;
-  b += align_up(sizeof(double) * tot) * 4;  // tmp, centered/blurred, u, back
-  b += align_up(sizeof(double) * cells);    // den64
-  b += align_up(sizeof(float) * cells);     // den32
-  b += align_up(sizeof(double) * H);        // row weights
-  b += align_up(sizeof(double) * (H > W ? H : W) + 4096 * 8);  // weights
-  b += align_up(sizeof(double) * MAX_PARTS);
-  b += align_up(sizeof(double) * 8);
-  return b;
+static size_t carve_np(char* base, long long n, double** v, double** vals, long long** lstart, int** llen,
+                       int** left, int** right, int** order, int** hoff, double** out, bool with_v = true) {
+  Carver c{base};
+  const size_t nleaf = (size_t)(n / 64 + 4);
+  *v = c.take<double>(with_v ? (size_t)n : 1);
+  *vals = c.take<double>(2 * nleaf);
+  *lstart = c.take<long long>(nleaf);
+  *llen = c.take<int>(nleaf);
+  *left = c.take<int>(nleaf);
+  *right = c.take<int>(nleaf);
+  *order = c.take<int>(nleaf);
+  *hoff = c.take<int>(72);
+  *out = c.take<double>(2);
+  return align_up(c.off);
+}
+
+// NumPy-order sum of v[0..n) (np_sum.cuh): out2[0] = sum, out2[1] = sum / n.
+// The tree tables go up from pageable host memory; cudaMemcpyAsync has staged
+// such a copy by the time it returns, so the host vectors may die here.
+static int np_sum_device(const double* v, long long n, char* npws, double* out2, cudaStream_t st) {
+  double *vv, *vals, *out;
+  long long* ls;
+  int *ll, *l, *r, *o, *h;
+  carve_np(npws, n, &vv, &vals, &ls, &ll, &l, &r, &o, &h, &out, false);
+  NpTree t;
+  np_tree_make(&t, n);
+  const size_t nl = t.leaf_start.size(), ni = t.left.size();
+  CK(cudaMemcpyAsync(ls, t.leaf_start.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ll, t.leaf_len.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st));
+  if (ni) {
+    CK(cudaMemcpyAsync(l, t.left.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(r, t.right.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(o, t.order.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemcpyAsync(h, t.hoff.data(), sizeof(int) * t.hoff.size(), cudaMemcpyHostToDevice, st));
+  np_leaf_kernel<<<std::max<int>(1, (int)((nl + 255) / 256)), 256, 0, st>>>(v, ls, ll, (int)nl, vals);
+  np_tree_kernel<<<1, 1024, 0, st>>>(vals, l, r, o, h, (int)t.hoff.size() - 1, (int)nl, t.root, n, out2);
+  return PLAS_OK;
 }
 
 struct AuxWs {
   double *t0, *t1, *t2, *t3, *den64, *rows, *w, *partials, *scalars;
   float* den32;
+  char* np;  // NumPy-order sum tables over H W C values (smoothness mean)
 };
 
 static size_t carve_aux(char* base, int H, int W, int C, AuxWs* a) {
@@ -1694,7 +1722,16 @@ static size_t carve_aux(char* base, int H, int W, int C, AuxWs* a) {
   a->w = c.take<double>((H > W ? H : W) + 4096);
   a->partials = c.take<double>(MAX_PARTS);
   a->scalars = c.take<double>(8);
+  double *v, *vals, *out;
+  long long* ls;
+  int *ll, *l, *r, *o, *h;
+  a->np = c.take<char>(carve_np(nullptr, std::max<size_t>(tot, 1), &v, &vals, &ls, &ll, &l, &r, &o, &h, &out, false));
   return align_up(c.off);
+}
+
+size_t plas_aux_workspace_bytes(int H, int W, int C) {
+  AuxWs a;
+  return carve_aux(nullptr, H, W, C, &a);
 }
 
 static int launch_blur(const void* in, void* out, int dtype, int H, int W, int C, int S, int h,
@@ -1885,22 +1922,6 @@ int plas_blur(const void* in, void* out, int dtype, int H, int W, int C, const d
 }
 
 // workspace of plas_grid_distance: per-cell values + the NumPy tree
-static size_t carve_np(char* base, long long n, double** v, double** vals, long long** lstart, int** llen,
-                       int** left, int** right, int** order, int** hoff, double** out, bool with_v = true) {
-  Carver c{base};
-  const size_t nleaf = (size_t)(n / 64 + 4);
-  *v = c.take<double>(with_v ? (size_t)n : 1);
-  *vals = c.take<double>(2 * nleaf);
-  *lstart = c.take<long long>(nleaf);
-  *llen = c.take<int>(nleaf);
-  *left = c.take<int>(nleaf);
-  *right = c.take<int>(nleaf);
-  *order = c.take<int>(nleaf);
-  *hoff = c.take<int>(72);
-  *out = c.take<double>(2);
-  return align_up(c.off);
-}
-
 size_t plas_grid_distance_workspace_bytes(int64_t n) {
   double *v, *vals, *out;
   long long* ls;
@@ -1919,20 +1940,8 @@ int plas_grid_distance(const double* a, const double* b, const double* weights, 
   long long* ls;
   int *ll, *l, *r, *o, *h;
   carve_np((char*)ws, n, &v, &vals, &ls, &ll, &l, &r, &o, &h, &out);
-  NpTree t;
-  np_tree_make(&t, n);
-  const size_t nl = t.leaf_start.size(), ni = t.left.size();
-  CK(cudaMemcpyAsync(ls, t.leaf_start.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ll, t.leaf_len.data(), sizeof(int) * nl, cudaMemcpyHostToDevice, st));
-  if (ni) {
-    CK(cudaMemcpyAsync(l, t.left.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(r, t.right.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(o, t.order.data(), sizeof(int) * ni, cudaMemcpyHostToDevice, st));
-  }
-  CK(cudaMemcpyAsync(h, t.hoff.data(), sizeof(int) * t.hoff.size(), cudaMemcpyHostToDevice, st));
   np_cell_f64_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(a, b, weights, n, dim, v);
-  np_leaf_kernel<<<std::max<int>(1, (int)((nl + 255) / 256)), 256, 0, st>>>(v, ls, ll, (int)nl, vals);
-  np_tree_kernel<<<1, 1024, 0, st>>>(vals, l, r, o, h, (int)t.hoff.size() - 1, (int)nl, t.root, n, out);
+  if (int e = np_sum_device(v, n, (char*)vals, out, st)) return e;
   CK(cudaMemcpyAsync(out_dev, out + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
   CKL();
   return PLAS_OK;
@@ -2009,7 +2018,6 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
     CK(cudaMemcpyAsync(a.w, half_width > 0 ? weights : &one, sizeof(double) * (half_width + 1),
                        cudaMemcpyHostToDevice, st));
     const dim3 grid((W + SM_TS - 1) / SM_TS, (H + SM_TS - 1) / SM_TS);
-    const int nparts = (int)(grid.x * grid.y);
     void* fn = nullptr;
     size_t smem = 0;
     switch (half_width) {
@@ -2025,10 +2033,11 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
     const double* wd = a.w;
     int Hh = H, Ww = W, Cc = C, det = detach_target;
     double dl = huber_delta, sc = scale;
-    double* parts = a.t0;
-    void* args[] = {&pl, &gr, &Hh, &Ww, &Cc, &wd, &dl, &sc, &det, &parts};
+    double* hv = a.t0;
+    void* args[] = {&pl, &gr, &Hh, &Ww, &Cc, &wd, &dl, &sc, &det, &hv};
     CK(cudaLaunchKernel(fn, grid, dim3(256), args, smem, st));
-    mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(a.t0, nparts, (double)tot, loss_dev);
+    if (int e = np_sum_device(a.t0, tot, a.np, a.scalars, st)) return e;
+    CK(cudaMemcpyAsync(loss_dev, a.scalars + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
     CKL();
     return PLAS_OK;
   }
@@ -2038,9 +2047,9 @@ int plas_smoothness_plane(const double* plane, double* grad, int H, int W, int C
     anchor_center_kernel<<<eg, 256, 0, st>>>(plane, a.t1, cells, C);
     if (int e = launch_blur(a.t1, a.t2, PLAS_F64, H, W, C, C, half_width, a, true, st)) return e;
   }
-  huber_kernel<<<eg, 256, 0, st>>>(a.t1, a.t2, a.t3, tot, huber_delta, scale, half_width == 0,
-                                   a.partials);
-  mean_finalize_kernel<<<1, RED_THREADS, 0, st>>>(a.partials, eg, (double)tot, loss_dev);
+  huber_kernel<<<eg, 256, 0, st>>>(a.t1, a.t2, a.t3, tot, huber_delta, scale, half_width == 0, a.t0);
+  if (int e = np_sum_device(a.t0, tot, a.np, a.scalars, st)) return e;
+  CK(cudaMemcpyAsync(loss_dev, a.scalars + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
   if (detach_target || half_width == 0) {
     CK(cudaMemcpyAsync(grad, a.t3, sizeof(double) * tot, cudaMemcpyDeviceToDevice, st));
   } else {

@@ -18,27 +18,23 @@ __global__ void anchor_center_kernel(const double* __restrict__ plane, double* _
 }
 
 // residual = centered - blurred/den (blurred/den already divided by the blur
-// epilogue); partial Huber sums; upstream u = scale * clip(residual, +-delta)
+// epilogue); per-element Huber values (summed in NumPy's order); upstream u = scale * clip(residual, +-delta)
 // (smoothness.py:87-89, huber 41-47, huber_grad 50-54)
 __global__ void __launch_bounds__(256) huber_kernel(const double* __restrict__ centered,
                                                    const double* __restrict__ blurred,
                                                    double* __restrict__ u, long long total,
                                                    double delta, double scale, int zero_residual,
-                                                   double* __restrict__ partials) {
-  __shared__ double sh[32];
-  double sum = 0.0;
+                                                   double* __restrict__ hval) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     double r = zero_residual ? 0.0 : __dsub_rn(centered[t], blurred[t]);
     double a = fabs(r);
     double hub = a <= delta ? __dmul_rn(__dmul_rn(0.5, r), r)
                             : __dmul_rn(delta, __dsub_rn(a, __dmul_rn(0.5, delta)));
-    sum += hub;
+    hval[t] = hub;
     double cl = r < -delta ? -delta : (r > delta ? delta : r);
     u[t] = __dmul_rn(scale, cl);
   }
-  double tot = block_sum<256>(sum, sh);
-  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
 
 // v = u / den[cell]  (the transpose of the renormalized blur, smoothness.py:95)
@@ -68,7 +64,7 @@ namespace plas {
 //   c    = plane - plane[0, 0]                on the tile + 2R halo (0 outside)
 //   B    = axis1(axis0(c))                    on the tile + R halo
 //   Rsd  = c - B / den                        (den = border weight, exact fold)
-//   loss += huber(Rsd) over the tile          (CTA partial, fixed order)
+//   hval = huber(Rsd) on the tile            (summed after in NumPy's order)
 //   u    = scale * clip(Rsd), v = u / den     on the tile + R halo (v = 0 outside)
 //   grad = u - axis1(axis0(v))                on the tile (grad = u if detached)
 // with the same SciPy fold (acc = x0 w0; acc += (x-j + x+j) w_j, j = R..1,
@@ -99,7 +95,7 @@ template <int R>
 __global__ void __launch_bounds__(256) smooth_fused_kernel(const double* __restrict__ plane, double* __restrict__ grad,
                                                            int H, int W, int C, const double* __restrict__ wts,
                                                            double delta, double scale, int detach,
-                                                           double* __restrict__ partials) {
+                                                           double* __restrict__ hval) {
   using T = SmoothTile<R>;
   constexpr int NC = T::NC, NB = T::NB;
   extern __shared__ double sm[];
@@ -108,7 +104,6 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const double* __restr
   double* vbuf = a0 + (size_t)NB * NC * SM_CG;        // [NB][NB][CG] u (later v)
   double* den = vbuf + (size_t)NB * NB * SM_CG;       // [NB][NB]
   __shared__ double w[R + 1];
-  __shared__ double sh[32];
   const int tid = threadIdx.x;
   if (tid <= R) w[tid] = wts[tid];
   const int y0 = blockIdx.y * SM_TS, x0 = blockIdx.x * SM_TS;
@@ -131,7 +126,6 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const double* __restr
     }
     den[e] = d;
   }
-  double hsum = 0.0;
   for (int c0 = 0; c0 < C; c0 += SM_CG) {
     const int cg = min(SM_CG, C - c0);  // loops cover cg channels; buffers keep the SM_CG stride
     // c on the NC x NC region
@@ -163,7 +157,8 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const double* __restr
         const double r = R > 0 ? __dsub_rn(cbuf[((size_t)(by + R) * NC + bx + R) * SM_CG + ch], blurred) : 0.0;
         if (by >= R && by < R + SM_TS && bx >= R && bx < R + SM_TS) {
           const double a = fabs(r);
-          hsum += a <= delta ? __dmul_rn(__dmul_rn(0.5, r), r) : __dmul_rn(delta, __dsub_rn(a, __dmul_rn(0.5, delta)));
+          hval[((long long)y * W + x) * C + c0 + ch] =
+              a <= delta ? __dmul_rn(__dmul_rn(0.5, r), r) : __dmul_rn(delta, __dsub_rn(a, __dmul_rn(0.5, delta)));
         }
         const double cl = r < -delta ? -delta : (r > delta ? delta : r);
         u = __dmul_rn(scale, cl);
@@ -209,8 +204,6 @@ __global__ void __launch_bounds__(256) smooth_fused_kernel(const double* __restr
     }
     __syncthreads();
   }
-  const double tot = block_sum<256>(hsum, sh);
-  if (tid == 0) partials[blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
 }  // namespace plas

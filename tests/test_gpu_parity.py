@@ -166,9 +166,11 @@ def test_smoothness_golden():
         planes = {n: z[f"{m['i']}_in_{n}"] for n in m["names"]}
         params = plas.SmoothnessParams(**m["params"])
         loss, grads = plas.smoothness_loss(plas.GridStack(plas.GridLayout(m["side"]), planes), params)
-        assert loss == pytest.approx(m["loss"], rel=1e-12)
+        # the reference's floats: same fp64 roundings per element, the Huber
+        # mean summed in NumPy's pairwise order (np_sum.cuh)
+        assert loss == m["loss"], (m["i"], loss, m["loss"])
         for n in m["names"]:
-            np.testing.assert_allclose(grads[n], z[f"{m['i']}_grad_{n}"], rtol=1e-12, atol=1e-300)
+            np.testing.assert_array_equal(grads[n], z[f"{m['i']}_grad_{n}"])
 
 
 def test_smoothness_properties():
