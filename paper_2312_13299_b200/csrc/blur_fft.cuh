@@ -136,14 +136,18 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
   }
 }
 
+// threads per CTA for L > 4096; 0 = L / 8 (640 at 5120, 768 at 6144: one
+// radix-8 butterfly per thread and pass, so no pass runs a second partial
+// round while most warps wait at its barrier; 96 / 80 registers, no spills).
+// Measured at C4: FFT blur 1127 -> 1038 ms per sort vs 512 threads.
 #ifndef FFT_LONG_T
-#define FFT_LONG_T 512  // threads per CTA for L > 4096
+#define FFT_LONG_T 0
 #endif
 #ifndef FFT_LONG_MINB
 #define FFT_LONG_MINB 1
 #endif
 __host__ __device__ constexpr int fft_threads_len(int L) {
-  return L > 4096 ? FFT_LONG_T : (L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8));
+  return L > 4096 ? (FFT_LONG_T > 0 ? FFT_LONG_T : L / 8) : (L / 8 < 32 ? 32 : (L / 8 > 512 ? 512 : L / 8));
 }
 template <int L> __host__ __device__ constexpr int fft_threads_for() { return fft_threads_len(L); }
 // resident CTAs per SM the register budget must allow (~85 registers at 256 threads)
@@ -230,15 +234,6 @@ struct FftPass {
   static constexpr int T = fft_threads_for<L>();
   static constexpr int NB = (L / R + T - 1) / T;  // butterflies per thread
 
-  // twiddles W_{Ns R}^{r k}, r = 1..R-1 (all R-1 loads issued together)
-  __device__ __forceinline__ static void load_twiddles(double2 (&wv)[R], int j, const double2* __restrict__ tw) {
-    if (Ns > 1) {
-      const int k = jmod(j);
-      const double2* pt = tw + L + fft_pass_twiddle_offset(LOG2L, P) + k;
-#pragma unroll
-      for (int r = 1; r < R; r++) wv[r] = __ldg(pt + r * Ns);
-    }
-  }
   __device__ __forceinline__ static void twiddle(double2 (&v)[R], const double2 (&wv)[R]) {
     if (Ns > 1) {
 #pragma unroll
@@ -250,78 +245,6 @@ struct FftPass {
     const int k = jmod(j);
     return (j - k) * R + k + r * Ns;
   }
-  // smem -> smem (SPEC: multiply by the real spectrum and conjugate)
-  template <bool SPEC>
-  __device__ __forceinline__ static void run(const double2* src, double2* dst, int tid_, const double2* tw,
-                                             const double* spec) {
-    if constexpr (fft_inplace<LOG2L>()) {
-      run_inplace<SPEC>(dst, tw, spec);
-      return;
-    }
-    // the thread index is re-read per pass so no pass's (thread-only) twiddle
-    // loads and addresses are hoisted into an earlier pass
-    unsigned tid;
-    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-#pragma unroll
-    for (int t = 0; t < NB; t++) {
-      const int j = (int)tid + t * T;
-      if (j < L / R) {
-        double2 v[R], wv[R];
-        load_twiddles(wv, j, tw);
-#pragma unroll
-        for (int r = 0; r < R; r++) v[r] = src[fft_pad(j + r * (L / R))];
-        twiddle(v, wv);
-        dft_small<R>(v);
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          const int d = dest(j, r);
-          double2 o = v[r];
-          if (SPEC) {
-            const double sp = ld_ordered(spec + d);
-            o = make_double2(o.x * sp, -(o.y * sp));
-          }
-          dst[fft_pad(d)] = o;
-        }
-      }
-    }
-  }
-  // in place (src == dst): every thread reads, the CTA syncs, every thread writes
-  template <bool SPEC>
-  __device__ __forceinline__ static void run_inplace(double2* buf, const double2* tw, const double* spec) {
-    unsigned tid;
-    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-    double2 v[NB][R];
-#pragma unroll
-    for (int t = 0; t < NB; t++) {
-      const int j = (int)tid + t * T;
-      if (j < L / R) {
-        double2 wv[R];
-        load_twiddles(wv, j, tw);
-#pragma unroll
-        for (int r = 0; r < R; r++) v[t][r] = buf[fft_pad(j + r * (L / R))];
-        twiddle(v[t], wv);
-        dft_small<R>(v[t]);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < NB; t++) {
-      const int j = (int)tid + t * T;
-      if (j < L / R) {
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          const int d = dest(j, r);
-          double2 o = v[t][r];
-          if (SPEC) {
-            const double sp = ld_ordered(spec + d);
-            o = make_double2(o.x * sp, -(o.y * sp));
-          }
-          buf[fft_pad(d)] = o;
-        }
-      }
-    }
-  }
-
   // this thread's twiddles of the pass, loaded BEFORE the barrier that precedes
   // the pass (their latency overlaps the barrier wait instead of the pass)
   struct Tw {
@@ -374,19 +297,6 @@ struct FftPass {
           buf[fft_pad(d)] = o;
         }
       }
-    }
-  }
-};
-
-template <int LOG2L, int P, int LAST>
-struct FftChain {
-  // passes P .. LAST-1 of one FFT (a == b: in place, fft_inplace)
-  template <bool SPEC_LAST>
-  __device__ __forceinline__ static void run(double2* a, double2* b, int tid, const double2* tw, const double* spec) {
-    if constexpr (P < LAST) {
-      FftPass<LOG2L, P>::template run<SPEC_LAST && P == fft_npasses(LOG2L) - 1>(a, b, tid, tw, spec);
-      __syncthreads();
-      FftChain<LOG2L, P + 1, LAST>::template run<SPEC_LAST>(b, a, tid, tw, spec);
     }
   }
 };
