@@ -478,6 +478,20 @@ def test_blur_fft_tier_long_lines(width, radii):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("height,radii", [(4096, (150.0, 900.0, 1500.0)), (2048, (700.0,))])
+def test_blur_fft_tier_long_columns(height, radii):
+    """The axis-0 FFT pass (columns) at the long lengths: 4096-row columns take
+    L = 5120 (h <= 1024) and 6144 (radix-16 passes with a composite 20 / 24
+    last pass), 2048-row columns 3072; an odd channel count leaves one
+    single-channel pair."""
+    rng = np.random.default_rng(37 + height)
+    g = rng.normal(0, 1, (height, 3, 3)).astype(np.float32)
+    for r in radii:
+        got, fb = gblur.blur_target_tiers(g, r, 1)
+        np.testing.assert_array_equal(got, O.blur_target(g, r), err_msg=f"height={height} r={r} fb={fb}")
+
+
+@pytest.mark.gpu
 def test_smoothness_autograd_matches_loss_and_gradients():
     """SURVEY 8(f) #3: the loss as a torch.autograd.Function for a trainer."""
     import torch
