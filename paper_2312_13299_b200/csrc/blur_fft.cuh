@@ -136,6 +136,83 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
   }
 }
 
+// Composite radices R = R1 R2 (R1 odd or 4, R2 a power of two) in registers,
+// Cooley-Tukey: DFT_R1 over n1 for each n2 (inputs x[R2 n1 + n2]), internal
+// twiddles W_R^(n2 k1), DFT_R2 over n2 for each k1, output X[k1 + R1 k2].  The
+// internal twiddles are correctly rounded constants (exact for multiples of a
+// quarter turn).  Error accounting (fft_error_constant): the odd DFT with the
+// pass's outer twiddle is charged as for a separate odd pass, and each
+// internal twiddle rides on the first radix-2 stage of the power-of-two DFT
+// after it, so a composite pass costs exactly the radix-2 stages of its factors.
+template <int R>
+__device__ __forceinline__ double2 fft_wconst(int m) {  // W_R^m = e^{-2 pi i m / R}, R = 16, 20 or 24
+  constexpr double c16[5] = {1.0, 0.9238795325112867, 0.7071067811865476, 0.3826834323650898, 0.0};
+  constexpr double c24[7] = {1.0, 0.9659258262890683, 0.8660254037844386, 0.7071067811865476, 0.5,
+                             0.25881904510252074, 0.0};
+  constexpr double c20[6] = {1.0, 0.9510565162951535, 0.8090169943749475, 0.5877852522924731, 0.30901699437494745,
+                             0.0};
+  constexpr int Q = R / 4;  // cos over the first quarter turn in Q steps
+  const double* cq = Q == 4 ? c16 : (Q == 6 ? c24 : c20);
+  m %= R;
+  const int quad = m / Q, r = m - quad * Q;
+  const double2 b = make_double2(cq[r], -cq[Q - r]);  // (cos, -sin) of 2 pi r / R
+  // e^{-i (quad pi/2 + t)} = (-i)^quad e^{-i t}
+  return quad == 0 ? b : (quad == 1 ? make_double2(b.y, -b.x) : (quad == 2 ? make_double2(-b.x, -b.y)
+                                                                           : make_double2(-b.y, b.x)));
+}
+template <int R1, int R2>
+__device__ __forceinline__ void dft_comp(double2 (&v)[R1 * R2]);
+template <int R>
+__device__ __forceinline__ void dft_any(double2 (&v)[R]) {
+  if constexpr (R == 2 || R == 3 || R == 4 || R == 5 || R == 8) {
+    dft_small<R>(v);
+  } else if constexpr (R == 6 || R == 12 || R == 24) {
+    dft_comp<3, R / 3>(v);
+  } else {
+    static_assert(R == 10 || R == 20 || R == 40, "unsupported radix");
+    dft_comp<5, R / 5>(v);
+  }
+}
+template <int R1, int R2>
+__device__ __forceinline__ void dft_comp(double2 (&v)[R1 * R2]) {
+  constexpr int R = R1 * R2;
+  constexpr int RT = (R == 10 || R == 20) ? 20 : 24;  // constant tables: 6, 12 | 24 and 10 | 20
+  constexpr int SC = RT / R;
+#pragma unroll
+  for (int n2 = 0; n2 < R2; n2++) {
+    double2 t[R1];
+#pragma unroll
+    for (int n1 = 0; n1 < R1; n1++) t[n1] = v[R2 * n1 + n2];
+    dft_any<R1>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; k1++) {
+      const int m = (n2 * k1) % R;
+      if (m != 0) {
+        if ((4 * m) % R == 0) {  // a quarter turn: exact
+          const int quad = 4 * m / R;
+          const double2 b = t[k1];
+          t[k1] = quad == 1 ? make_double2(b.y, -b.x) : (quad == 2 ? make_double2(-b.x, -b.y) : make_double2(-b.y, b.x));
+        } else {
+          t[k1] = cmul(t[k1], fft_wconst<RT>(m * SC));
+        }
+      }
+      v[R2 * k1 + n2] = t[k1];
+    }
+  }
+  double2 o[R];
+#pragma unroll
+  for (int k1 = 0; k1 < R1; k1++) {
+    double2 t[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; n2++) t[n2] = v[R2 * k1 + n2];
+    dft_any<R2>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < R2; k2++) o[k1 + R1 * k2] = t[k2];
+  }
+#pragma unroll
+  for (int k = 0; k < R; k++) v[k] = o[k];
+}
+
 // threads per CTA for L > 4096; 0 = L / 8 (640 at 5120, 768 at 6144: one
 // radix-8 butterfly per thread and pass, so no pass runs a second partial
 // round while most warps wait at its barrier; 96 / 80 registers, no spills).
@@ -172,6 +249,13 @@ template <int L> __host__ __device__ constexpr int fft_min_blocks() {
                                : (L == 2560 ? FFT_MINB_2560 : (FFT_MINB * 256) / fft_threads_for<L>()));
 }
 
+// With FFT_MERGE_ODD, the power-of-two remainder (2 or 4) and an odd factor 3
+// or 5 share one composite pass (6, 10, 12 or 20) instead of two passes:
+// 3072 = 8 8 8 6, 5120 = 8 8 8 10, 6144 = 8 8 8 12 (one barrier pair and
+// shared-memory round trip fewer per FFT).
+#ifndef FFT_MERGE_ODD
+#define FFT_MERGE_ODD 1
+#endif
 // FFT length code lc = p2 + 32 m: L = M 2^p2 with M = 1, 3, 5, 9 for m = 0..3
 // (the odd factors cut the padded length: at side 1024 a level with h <= 128
 // uses 1152, h <= 256 1280, h <= 511 1536, instead of 2048).  Pass schedule:
@@ -184,12 +268,19 @@ __host__ __device__ constexpr int fft_p2(int lc) { return lc & 31; }
 __host__ __device__ constexpr int fft_len(int lc) { return fft_mult(lc) << fft_p2(lc); }
 __host__ __device__ constexpr int fft_np2(int lc) { return fft_p2(lc) / 3 + (fft_p2(lc) % 3 ? 1 : 0); }
 __host__ __device__ constexpr int fft_nodd(int lc) { return fft_mult(lc) == 1 ? 0 : (fft_mult(lc) == 9 ? 2 : 1); }
-__host__ __device__ constexpr int fft_npasses(int lc) { return fft_np2(lc) + fft_nodd(lc); }
+__host__ __device__ constexpr bool fft_merged(int lc) {
+  return FFT_MERGE_ODD && fft_p2(lc) % 3 != 0 && (fft_mult(lc) == 3 || fft_mult(lc) == 5);
+}
+__host__ __device__ constexpr int fft_npasses(int lc) { return fft_np2(lc) + fft_nodd(lc) - (fft_merged(lc) ? 1 : 0); }
 __host__ __device__ constexpr int fft_radix(int lc, int p) {
-  return p < fft_np2(lc) ? (p < fft_p2(lc) / 3 ? 8 : (fft_p2(lc) % 3 == 2 ? 4 : 2)) : (fft_mult(lc) == 5 ? 5 : 3);
+  return fft_merged(lc) && p == fft_p2(lc) / 3
+             ? (1 << (fft_p2(lc) % 3)) * fft_mult(lc)
+             : (p < fft_np2(lc) ? (p < fft_p2(lc) / 3 ? 8 : (fft_p2(lc) % 3 == 2 ? 4 : 2)) : (fft_mult(lc) == 5 ? 5 : 3));
 }
 __host__ __device__ constexpr int fft_ns(int lc, int p) {
-  return p < fft_np2(lc) ? (1 << (3 * p)) : (p == fft_np2(lc) ? (1 << fft_p2(lc)) : (3 << fft_p2(lc)));
+  int ns = 1;
+  for (int q = 0; q < p; q++) ns *= fft_radix(lc, q);
+  return ns;
 }
 // lines of up to fft_out_max(lc) samples fit (n + h <= L checked by the caller):
 // L / 2 for powers of two, else the largest power of two below L; the two raw
@@ -278,7 +369,7 @@ struct FftPass {
 #pragma unroll
         for (int r = 0; r < R; r++) v[t][r] = buf[fft_pad(j + r * (L / R))];
         twiddle(v[t], twv.w[t]);
-        dft_small<R>(v[t]);
+        dft_any<R>(v[t]);
       }
     }
     __syncthreads();
@@ -472,7 +563,7 @@ __global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blo
             mx = fmax(mx, fmax(fabs(v[r].x), fabs(v[r].y)));
           }
         }
-        dft_small<P0::R>(v);
+        dft_any<P0::R>(v);
 #pragma unroll
         for (int r = 0; r < P0::R; r++) bufA[fft_pad(P0::dest(j, r))] = v[r];
       }
@@ -524,7 +615,7 @@ __global__ void __launch_bounds__(fft_threads_for<fft_len(LOG2L)>(), fft_min_blo
 #pragma unroll
       for (int r = 0; r < PL::R; r++) v[r] = jv ? last_src[fft_pad(j + r * (L / PL::R))] : make_double2(0.0, 0.0);
       PL::twiddle(v, wv);
-      dft_small<PL::R>(v);
+      dft_any<PL::R>(v);
 #pragma unroll
       for (int r = 0; r < PL::R; r++) {
         const int i = PL::dest(j, r);
