@@ -466,6 +466,22 @@ def test_sort_wide_rows_parity_vs_oracle(side, dim):
                                   [v for _, t in wrep["radius_trace"] for v in t])
 
 
+@pytest.mark.parametrize("dim", [1, 2, 3, 4, 5, 8, 9, 12, 13, 16, 17, 24, 33, 64])
+def test_sort_row_width_sweep_parity_vs_oracle(dim):
+    """Every row-stride family of the kernels (S = 4, 8, 12, 16 and the wide
+    rows up to 64 floats, padded channels included) on a non-power-of-two
+    side: PARITY sort bit-exact with the C oracle -- permutation, pass count,
+    trace."""
+    side = 37
+    f = np.random.default_rng(100 + dim).uniform(-2, 2, (side * side, dim))
+    perm, rep = plas.sort_grid_report(f, plas.SortConfig(rng_seed=dim))
+    want, wrep = O.sort_grid_report(f, rng_seed=dim)
+    np.testing.assert_array_equal(perm, want)
+    assert rep.reorders == wrep["reorders"]
+    np.testing.assert_array_equal([v for _, t in rep.radius_trace for v in t],
+                                  [v for _, t in wrep["radius_trace"] for v in t])
+
+
 @pytest.mark.parametrize("width,radii", [(4096, (300.0, 2047.0)), (2048, (600.0, 1023.0)), (1024, (64.0, 200.0))])
 def test_blur_fft_tier_long_lines(width, radii):
     """Long lines through the FFT tier: 4096 (configs[4]) and 2048 (configs[3]) wide
