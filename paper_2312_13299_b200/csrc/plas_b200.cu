@@ -974,15 +974,29 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
   }
   const int fft_grid = side * ((D + 1) / 2);  // one CTA per line pair
   std::vector<int> hmode(std::max(L, 1));
+  // the zero-padded buffers are read at +-h around every output (direct tier,
+  // fallback folds): h <= pad - BPAD_R, the reference rule's top half-width
+  // plus one; larger start radii are refused (plas.py SortPlan does the same)
+  const int hpad = w.pad - std::max(BLUR_R, BPAD_R);
   for (int lv = 0; lv < L; lv++) {
     const int h = sch.hs[lv];
     int m = level_uses_tile_blur(h, side, hc.fft_min_h, hc.fft_L, hc.tile_blur_hmax) ? NPL : NPL + 1;
     if (m == NPL + 1 && h <= PAD_SMALL_HMAX && pad_small_enabled()) m = NPL + 1 + h;  // direct, compile-time h
     if (NPL && level_uses_fft(h, side, hc.fft_min_h, hc.fft_L)) {
       const int lcode = fft_choose_code(side, h);
-      m = NPL - 1;  // the longest length covers every FFT level
+      int f = -1;
       for (int i = NPL - 1; i >= 0; i--)
-        if (w.fft_codes[i] == lcode) m = i;
+        if (w.fft_codes[i] == lcode) f = i;
+      // otherwise the longest planned length, if it holds the line and h
+      // without wrapping (n + h <= L), else the padded direct tier
+      if (f < 0 && side + (long long)h <= fft_len(w.fft_codes[NPL - 1]) && side <= fft_out_max(w.fft_codes[NPL - 1]))
+        f = NPL - 1;
+      if (f >= 0) m = f;
+    }
+    if (h > hpad) {  // (the FFT tier's overflow list is folded from the padded buffers too)
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      return fail(PLAS_ERR_INVALID, "start radius too large for this grid (ceil(r) must be <= ceil(side/2 - 1) + 1)");
     }
     hmode[lv] = m;
   }

@@ -202,6 +202,12 @@ def _validate(features):
 
 
 @functools.lru_cache(maxsize=64)
+def max_start_half_width(side):
+    """Largest level half-width ceil(r) a sort of this side supports: the
+    reference rule's ceil(max(side/2 - 1, 2)) plus one (csrc blur_pad)."""
+    return int(math.ceil(max(side / 2.0 - 1.0, 2.0))) + 1
+
+
 def _schedule(side, radius_decay, min_block_size, start):
     """Schedules are pure functions of these four values (read-only after
     construction), so repeated sorts of one shape reuse the host tables."""
@@ -217,6 +223,15 @@ class SortPlan:
         self.side = math.isqrt(n)
         self.config = config
         self.mode = RNG_MODES[config.rng_mode]
+        if config.initial_radius is not None:
+            # the sort's zero-padded blur buffers cover half-widths up to the
+            # reference rule's ceil(side/2 - 1) plus one (BASELINE configs[0]
+            # starts at 32 on a 64-cell side); larger start radii are rejected
+            # here (the C ABI returns PLAS_ERR_INVALID for them)
+            hmax = max_start_half_width(self.side)
+            if math.ceil(config.initial_radius) > hmax:
+                raise ValueError(f"initial_radius {config.initial_radius} exceeds the largest start radius "
+                                 f"for a {self.side}-cell side (ceil(r) <= {hmax})")
         self.schedule = _schedule(self.side, config.radius_decay, config.min_block_size,
                                  config.initial_radius)
         self.trace_capacity = max(64 * max(self.schedule.num_levels, 1), 4096)

@@ -482,6 +482,56 @@ def test_sort_row_width_sweep_parity_vs_oracle(dim):
                                   [v for _, t in wrep["radius_trace"] for v in t])
 
 
+@pytest.mark.parametrize("kw", [dict(min_block_size=2), dict(min_block_size=5), dict(min_block_size=40),
+                                dict(radius_decay=0.7, improvement_threshold=1e-3),
+                                dict(radius_decay=0.99, improvement_threshold=1e-2),
+                                dict(initial_radius=7.5), dict(initial_radius=22.0)])
+def test_sort_config_variants_parity_vs_oracle(kw):
+    """SortConfig away from the defaults (plas.py:37-61): tiny and large minimum
+    blocks (leftover groups of 2 and 3 everywhere, blocks wider than the grid),
+    fast and slow decay, strict and loose thresholds, start-radius overrides
+    below and above the reference rule.  PARITY bit-exact with the oracle."""
+    side = 44
+    f = np.random.default_rng(7).normal(0, 1, (side * side, 6))
+    okw = {k: v for k, v in kw.items() if k != "initial_radius"}
+    if "initial_radius" in kw:
+        okw["initial_radius_override"] = kw["initial_radius"]
+    perm, rep = plas.sort_grid_report(f, plas.SortConfig(rng_seed=4, **kw))
+    want, wrep = O.sort_grid_report(f, rng_seed=4, **okw)
+    np.testing.assert_array_equal(perm, want)
+    assert rep.reorders == wrep["reorders"]
+    np.testing.assert_array_equal([v for _, t in rep.radius_trace for v in t],
+                                  [v for _, t in wrep["radius_trace"] for v in t])
+
+
+def test_sort_start_radius_above_the_supported_maximum_raises():
+    """SortConfig.initial_radius (not in the reference) is accepted up to the
+    reference rule's top half-width plus one (ceil(r) <= ceil(side/2 - 1) + 1,
+    BASELINE configs[0] starts at 32 on a 64-cell side); above it the sort
+    raises ValueError instead of reading past its zero-padded buffers, and the
+    C ABI refuses the schedule on its own."""
+    from paper_2312_13299_b200 import _lib
+    from paper_2312_13299_b200.plas import SortPlan
+    f = np.random.default_rng(8).normal(0, 1, (44 * 44, 6))
+    for r in (22.5, 60.0):
+        with pytest.raises(ValueError):
+            plas.sort_grid(f, plas.SortConfig(initial_radius=r))
+    # bypass the Python check: the library itself returns PLAS_ERR_INVALID
+    import torch
+    plan = SortPlan.__new__(SortPlan)
+    cfg = plas.SortConfig(initial_radius=60.0)
+    plan.n, plan.dim, plan.side, plan.config = 44 * 44, 6, 44, cfg
+    from paper_2312_13299_b200.plas import RNG_MODES
+    plan.mode = RNG_MODES["parity"]
+    from paper_2312_13299_b200.plas import _schedule
+    plan.schedule = _schedule(44, cfg.radius_decay, cfg.min_block_size, 60.0)
+    plan.trace_capacity = 4096
+    dev = torch.from_numpy(f).cuda()
+    perm = torch.empty(44 * 44, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        plan.run(dev, perm)
+
+
 @pytest.mark.parametrize("width,radii", [(4096, (300.0, 2047.0)), (2048, (600.0, 1023.0)), (1024, (64.0, 200.0))])
 def test_blur_fft_tier_long_lines(width, radii):
     """Long lines through the FFT tier: 4096 (configs[4]) and 2048 (configs[3]) wide
