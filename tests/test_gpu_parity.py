@@ -504,6 +504,30 @@ def test_sort_config_variants_parity_vs_oracle(kw):
                                   [v for _, t in wrep["radius_trace"] for v in t])
 
 
+@pytest.mark.parametrize("kind", ["constant", "two_values", "small_ints", "one_hot"])
+def test_sort_tie_heavy_inputs_parity_vs_oracle(kind):
+    """Inputs whose 4x4 costs tie exactly (constant rows, two distinct rows,
+    small integers, one-hot rows): the fast tier cannot certify a gap, the
+    exact tier and the first-strict-minimum rule (plas.py:138-146) decide.
+    PARITY bit-exact with the oracle in permutation, passes and trace."""
+    side, D = 30, 5
+    g = np.random.default_rng(21)
+    if kind == "constant":
+        f = np.full((side * side, D), 0.25)
+    elif kind == "two_values":
+        f = np.where(g.random((side * side, 1)) < 0.5, 0.0, 1.0) * np.ones((1, D))
+    elif kind == "small_ints":
+        f = g.integers(0, 3, (side * side, D)).astype(np.float64)
+    else:
+        f = np.eye(D)[g.integers(0, D, side * side)]
+    perm, rep = plas.sort_grid_report(f, plas.SortConfig(rng_seed=3))
+    want, wrep = O.sort_grid_report(f, rng_seed=3)
+    np.testing.assert_array_equal(perm, want)
+    assert rep.reorders == wrep["reorders"]
+    np.testing.assert_array_equal([v for _, t in rep.radius_trace for v in t],
+                                  [v for _, t in wrep["radius_trace"] for v in t])
+
+
 def test_sort_start_radius_above_the_supported_maximum_raises():
     """SortConfig.initial_radius (not in the reference) is accepted up to the
     reference rule's top half-width plus one (ceil(r) <= ceil(side/2 - 1) + 1,
