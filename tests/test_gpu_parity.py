@@ -607,7 +607,7 @@ def test_smoothness_autograd_matches_loss_and_gradients():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("side,dim", [(256, 6), (128, 14), (96, 21)])
+@pytest.mark.parametrize("side,dim", [(256, 6), (128, 14), (96, 21), (300, 14), (75, 3)])
 def test_device_graph_matches_stepped(side, dim):
     """DEVICE mode runs as one CUDA graph (per-level regime IF, pass loop unrolled
     x3 with early-exit slots, level set-up node); the profiled run launches the
