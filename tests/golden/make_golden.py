@@ -216,7 +216,8 @@ def part_smooth():
                             (33, tuple(channels), {"weights": {k: 0.3 for k in channels}}),
                             (16, ("rotation",), {"kernel_size": 7, "sigma": 1.5}),
                             (9, ("opacity",), {"kernel_size": 1}),
-                            (20, ("rotation", "opacity"), {"kernel_size": 13, "sigma": 3.0})):
+                            (20, ("rotation", "opacity"), {"kernel_size": 13, "sigma": 3.0}),
+                            (12, ("opacity", "sh_dc"), {"kernel_size": 41, "sigma": 10.0})):
         planes = {n: rng.normal(0, 1.5, (side, side, channels[n])) for n in names}
         params = ref_smooth.SmoothnessParams(**kw)
         loss, grads = ref_smooth.smoothness_loss(GridStack(layout=GridLayout(side), planes=planes), params)
