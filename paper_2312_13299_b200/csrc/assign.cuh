@@ -171,12 +171,14 @@ __device__ __forceinline__ void lane_best_fast_cols(float c0, const float (&x)[4
   const float INF = __int_as_float(0x7f800000);
   float v1 = INF, v2 = INF;
   int q1 = 0x7fffffff;
+  bool ovf = false;  // an arrangement sum overflowed (see below)
   if (s < k) {
     if (k == 4) {
       const int A[6] = {0, 0, 1, 1, 2, 2}, B[6] = {1, 2, 0, 2, 0, 1}, E[6] = {2, 1, 2, 0, 1, 0};
 #pragma unroll
       for (int l = 0; l < 6; l++) {
         const float c = ((c0 + x[1][A[l]]) + x[2][B[l]]) + x[3][E[l]];
+        ovf |= c == INF;
         if (c < v1) {
           v2 = v1;
           v1 = c;
@@ -188,6 +190,7 @@ __device__ __forceinline__ void lane_best_fast_cols(float c0, const float (&x)[4
     } else if (k == 3) {  // the other targets of {0, 1, 2} are o_0 < o_1
       const float ca = (c0 + x[1][0]) + x[2][1];
       const float cb = (c0 + x[1][1]) + x[2][0];
+      ovf = ca == INF || cb == INF;
       if (cb < ca) {
         v1 = cb;
         q1 = 2 * s + 1;
@@ -200,11 +203,17 @@ __device__ __forceinline__ void lane_best_fast_cols(float c0, const float (&x)[4
     } else if (k == 2) {
       v1 = c0 + x[1][0];
       q1 = s;
+      ovf = v1 == INF;
     }
   }
+  // The fast costs sum fp32 squares in fp32: a sum can overflow to +inf where
+  // the reference's fp64 sum of the same squares stays finite (plas.py:129-137),
+  // so an infinite arrangement says nothing about the reference's order.  A
+  // lane that saw one reports b2 = -inf, which fails the certificate for the
+  // whole group after the min-reduction (decide_from_acc).
   *b1 = v1;
   *p1 = q1;
-  *b2 = v2;
+  *b2 = ovf ? -INF : v2;
 }
 
 // Decide one group (all 32 lanes call together; k may differ between the 8
@@ -386,9 +395,14 @@ __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4
       bp = op;
     }
   }
-  const float margin = 2.0f * (float)(D + 24) * 5.9604645e-08f;  // 2 (D+24) 2^-24
+  // relative: 2 (D+24) 2^-24 for the fp32 roundings; absolute: a cost whose
+  // sum of squares lies below the normal fp32 range (2^-126) carries an error
+  // up to its own size, < 1.1e-19, in both the fast and the reference
+  // arithmetic -- 4e-18 covers four of them on each side.  b2 = -inf: an
+  // overflowed fast sum (lane_best_fast_cols).
+  const float margin = 2.0f * (float)(D + 24) * 5.9604645e-08f;
   const bool certain =
-      k < 2 || (b2 < __int_as_float(0x7f800000) && b2 > 1e-30f && (b2 - b1) > margin * b2);
+      k < 2 || (b2 < __int_as_float(0x7f800000) && b2 > 1e-30f && (b2 - b1) > margin * b2 + 4e-18f);
   if (__any_sync(PLAS_FULL_MASK, !certain)) {
     bp = OOL ? decide_exact_call(Fb, Tb, rowj, D, S, k) : decide_exact_body(Fb, Tb, rowj, D, S, k);
     if (s == 0 && k >= 2 && !certain) *exact += 1;

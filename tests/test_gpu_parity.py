@@ -528,6 +528,52 @@ def test_sort_tie_heavy_inputs_parity_vs_oracle(kind):
                                   [v for _, t in wrep["radius_trace"] for v in t])
 
 
+def _fuzz_case(seed, case):
+    """The input of case `case` of tools/fuzz_parity.py's generator (seed `seed`)."""
+    g = np.random.default_rng(seed)
+    for c in range(case + 1):
+        side = int(g.integers(2, 49))
+        D = int(g.integers(1, 25))
+        dist = g.integers(0, 4)
+        n = side * side
+        if dist == 0:
+            f = g.normal(0, 1, (n, D))
+        elif dist == 1:
+            f = g.uniform(0, 1, (n, D))
+        elif dist == 2:
+            f = g.integers(-2, 3, (n, D)).astype(np.float64)
+        else:
+            f = g.normal(0, 1, (n, D)) * 10.0 ** g.uniform(-20, 20, (1, D))
+        kw = dict(rng_seed=int(g.integers(0, 1000)))
+        if g.random() < 0.5:
+            kw["radius_decay"] = float(g.uniform(0.5, 0.98))
+        if g.random() < 0.5:
+            kw["improvement_threshold"] = float(10 ** g.uniform(-6, -1))
+        if g.random() < 0.4:
+            kw["min_block_size"] = int(g.integers(2, 40))
+        if g.random() < 0.3:
+            kw["initial_radius"] = float(g.uniform(0.5, int(math.ceil(max(side / 2.0 - 1.0, 2.0))) + 1))
+    return f, kw
+
+
+@pytest.mark.parametrize("case", [54, 209, 271])
+def test_sort_extreme_channel_scales_parity_vs_oracle(case):
+    """Channels scaled by 10^-20 .. 10^20 (cases found by tools/fuzz_parity.py,
+    seed 1; the oracle matched the reference on them, the GPU did not): the
+    fast tier sums fp32 squares in fp32 and can overflow to +inf where the
+    reference's fp64 sum of the same squares stays finite, so an infinite fast
+    arrangement must send the group to the exact tier.  PARITY bit-exact."""
+    f, kw = _fuzz_case(1, case)
+    assert "initial_radius" not in kw
+    okw = dict(kw)
+    perm, rep = plas.sort_grid_report(f, plas.SortConfig(**kw))
+    want, wrep = O.sort_grid_report(f, **okw)
+    np.testing.assert_array_equal(perm, want)
+    assert rep.reorders == wrep["reorders"]
+    np.testing.assert_array_equal([v for _, t in rep.radius_trace for v in t],
+                                  [v for _, t in wrep["radius_trace"] for v in t])
+
+
 def test_sort_start_radius_above_the_supported_maximum_raises():
     """SortConfig.initial_radius (not in the reference) is accepted up to the
     reference rule's top half-width plus one (ceil(r) <= ceil(side/2 - 1) + 1,
