@@ -1,0 +1,107 @@
+"""Randomised sweep of the non-sort entry points against their checkers:
+blur_target (API, f32 and f64) and the sort's blur tiers vs the C oracle's
+SciPy fold; grid_distance and vad vs NumPy's own expressions of the reference
+(plas.py:71-84, metrics.py:25-40); reassign_block vs the oracle.  Shapes,
+radii (past the grid too), and value ranges (1e-20 .. 1e20 scales, zeros,
+constants, signed zeros) are drawn at random.  Prints every mismatch; exit 1
+if any.   usage: python tools/fuzz_api.py [cases] [seed]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2312_13299_b200 as plas  # noqa: E402
+from paper_2312_13299_b200 import blur as gblur  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+g = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+
+
+def values(shape):
+    kind = int(g.integers(0, 6))
+    if kind == 0:
+        return g.normal(0, 1, shape)
+    if kind == 1:
+        return g.uniform(0, 1, shape)
+    if kind == 2:
+        return g.normal(0, 1, shape) * 10.0 ** g.uniform(-20, 20, (1,) * (len(shape) - 1) + (shape[-1],))
+    if kind == 3:
+        return np.full(shape, float(g.normal()))
+    if kind == 4:
+        v = g.normal(0, 1, shape)
+        v[g.random(shape) < 0.5] = 0.0
+        v[g.random(shape) < 0.1] = -0.0
+        return v
+    return g.integers(-3, 4, shape).astype(np.float64)
+
+
+def np_grid_distance(a, b):  # plas.py:71-84, NumPy's own evaluation
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.sqrt(((a - b) ** 2).sum(axis=1)).mean())
+
+
+def np_vad(grid):  # metrics.py:25-40
+    gr = np.asarray(grid, dtype=np.float64)
+    if gr.ndim == 2:
+        gr = gr[..., None]
+    d = np.concatenate([np.abs(np.diff(gr, axis=0)).ravel(), np.abs(np.diff(gr, axis=1)).ravel()])
+    return float(d.var())
+
+
+bad = 0
+for c in range(cases):
+    what = int(g.integers(0, 5))
+    try:
+        if what == 0:  # API blur, dtype preserving
+            H, W, C = int(g.integers(1, 60)), int(g.integers(1, 60)), int(g.integers(1, 6))
+            r = float(g.uniform(0.3, 1.5 * max(H, W)))
+            dt = np.float32 if g.random() < 0.6 else np.float64
+            x = values((H, W, C)).astype(dt)
+            got, want = plas.blur_target(x, r), O.blur_target(x, r)
+            ok = got.dtype == want.dtype and np.array_equal(got, want)
+            tag = f"blur {H}x{W}x{C} {dt.__name__} r={r:.3f}"
+        elif what == 1:  # the sort's tiers (direct / FFT) on a square grid
+            side, C = int(g.integers(8, 200)), int(g.integers(1, 8))
+            r = float(g.uniform(1.0, max(side / 2.0 - 1.0, 2.0)))
+            tier = int(g.integers(0, 2))
+            x = values((side, side, C)).astype(np.float32)
+            got, _ = gblur.blur_target_tiers(x, r, tier)
+            ok = np.array_equal(got, O.blur_target(x, r))
+            tag = f"tiers {side}^2x{C} r={r:.3f} tier={tier}"
+        elif what == 2:
+            n, D = int(g.integers(1, 3000)), int(g.integers(1, 40))
+            a, b = values((n, D)), values((n, D))
+            got, want = plas.grid_distance(a, b), np_grid_distance(a, b)
+            ok = got == want or (np.isnan(got) and np.isnan(want))
+            tag = f"grid_distance n={n} D={D} {got!r} {want!r}"
+        elif what == 3:
+            H, W, C = int(g.integers(2, 80)), int(g.integers(2, 80)), int(g.integers(1, 6))
+            x = values((H, W, C)).astype(np.float32 if g.random() < 0.6 else np.float64)
+            got, want = plas.vad(x), np_vad(x)
+            ok = got == want or (np.isnan(got) and np.isnan(want))
+            tag = f"vad {H}x{W}x{C} {x.dtype} {got!r} {want!r}"
+        else:
+            m, D = int(g.integers(1, 40)), int(g.integers(1, 20))
+            n = m + int(g.integers(0, 10))
+            feat = values((n, D)).astype(np.float32)
+            target = values((n, D)).astype(np.float32)
+            idx = np.arange(n, dtype=np.int64)
+            positions = g.permutation(n)[:m]
+            grouping = g.permutation(m + int(g.integers(0, 5)))
+            f1, i1 = feat.copy(), idx.copy()
+            f2, i2 = feat.copy(), idx.copy()
+            plas.reassign_block(f1, i1, target, positions, grouping)
+            O.reassign_block(f2, i2, target, positions, grouping)
+            ok = np.array_equal(f1, f2) and np.array_equal(i1, i2)
+            tag = f"reassign m={m} n={n} D={D}"
+    except Exception as e:  # noqa: BLE001
+        ok = False
+        tag = f"case kind {what}: {e!r}"[:300]
+    if not ok:
+        bad += 1
+        print("MISMATCH", c, tag)
+print(f"{cases} cases, {bad} mismatches")
+sys.exit(1 if bad else 0)
