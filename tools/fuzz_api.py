@@ -1,7 +1,8 @@
 """Randomised sweep of the non-sort entry points against their checkers:
 blur_target (API, f32 and f64) and the sort's blur tiers vs the C oracle's
 SciPy fold; grid_distance and vad vs NumPy's own expressions of the reference
-(plas.py:71-84, metrics.py:25-40); reassign_block vs the oracle.  Shapes,
+(plas.py:71-84, metrics.py:25-40); reassign_block, quantize_planes and
+prune_indices vs the oracle.  Shapes,
 radii (past the grid too), and value ranges (1e-20 .. 1e20 scales, zeros,
 constants, signed zeros) are drawn at random.  Prints every mismatch; exit 1
 if any.   usage: python tools/fuzz_api.py [cases] [seed]"""
@@ -53,7 +54,7 @@ def np_vad(grid):  # metrics.py:25-40
 
 bad = 0
 for c in range(cases):
-    what = int(g.integers(0, 5))
+    what = int(g.integers(0, 7))
     try:
         if what == 0:  # API blur, dtype preserving
             H, W, C = int(g.integers(1, 60)), int(g.integers(1, 60)), int(g.integers(1, 6))
@@ -83,6 +84,32 @@ for c in range(cases):
             got, want = plas.vad(x), np_vad(x)
             ok = got == want or (np.isnan(got) and np.isnan(want))
             tag = f"vad {H}x{W}x{C} {x.dtype} {got!r} {want!r}"
+        elif what == 5:  # quantize / contract / plane packing vs the oracle
+            import torch
+            from paper_2312_13299_b200 import quantization as q
+            from oracle import prep as oprep
+            name = ["position", "sh_dc", "sh_rest", "rotation", "scale", "opacity"][int(g.integers(0, 6))]
+            C = {"position": 3, "sh_dc": 3, "sh_rest": 45, "rotation": 4, "scale": 3, "opacity": 1}[name]
+            n = int(g.integers(1, 3000))
+            v = values((n, C))
+            spec = q.default_quant_spec()[name]
+            SPEC = {"position": (2 ** 14, None), "sh_dc": (2 ** 8, (-2.0, 4.0)), "sh_rest": (2 ** 5, (-1.0, 1.0)),
+                    "opacity": (2 ** 6, (-6.0, 12.0)), "scale": (2 ** 6, None), "rotation": (2 ** 6, (-1.0, 2.0))}
+            # (tests/test_quant.py SPEC: the oracle's levels / clip of default_quant_spec)
+            levels, clip = SPEC[name]
+            planes, lo, hi = oprep.quantize_attribute_planes(name, v, levels, clip)
+            images, glo, ghi = q.quantize_planes(name, torch.from_numpy(v).cuda(), spec)
+            ok = (np.array_equal(images.cpu().numpy().astype(np.int64), planes)
+                  and np.array_equal(np.array(glo), lo) and np.array_equal(np.array(ghi), hi))
+            tag = f"quantize {name} n={n}"
+        elif what == 6:  # prune survivors vs the oracle
+            from paper_2312_13299_b200.splats import prune_indices
+            from oracle import prep as oprep
+            n = int(g.integers(1, 5000))
+            x = values((n, 1))[:, 0]
+            keep = int(g.integers(1, n + 1))
+            ok = np.array_equal(prune_indices(x, keep).cpu().numpy(), oprep.prune_survivors(x, keep))
+            tag = f"prune n={n} keep={keep}"
         else:
             m, D = int(g.integers(1, 40)), int(g.integers(1, 20))
             n = m + int(g.integers(0, 10))
