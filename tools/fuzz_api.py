@@ -1,8 +1,8 @@
 """Randomised sweep of the non-sort entry points against their checkers:
 blur_target (API, f32 and f64) and the sort's blur tiers vs the C oracle's
 SciPy fold; grid_distance and vad vs NumPy's own expressions of the reference
-(plas.py:71-84, metrics.py:25-40); reassign_block, quantize_planes and
-prune_indices vs the oracle.  Shapes,
+(plas.py:71-84, metrics.py:25-40); reassign_block, quantize_planes,
+prune_indices and normalize_for_sorting vs the oracle.  Shapes,
 radii (past the grid too), and value ranges (1e-20 .. 1e20 scales, zeros,
 constants, signed zeros) are drawn at random.  Prints every mismatch; exit 1
 if any.   usage: python tools/fuzz_api.py [cases] [seed]"""
@@ -54,7 +54,7 @@ def np_vad(grid):  # metrics.py:25-40
 
 bad = 0
 for c in range(cases):
-    what = int(g.integers(0, 7))
+    what = int(g.integers(0, 8))
     try:
         if what == 0:  # API blur, dtype preserving
             H, W, C = int(g.integers(1, 60)), int(g.integers(1, 60)), int(g.integers(1, 6))
@@ -110,6 +110,56 @@ for c in range(cases):
             keep = int(g.integers(1, n + 1))
             ok = np.array_equal(prune_indices(x, keep).cpu().numpy(), oprep.prune_survivors(x, keep))
             tag = f"prune n={n} keep={keep}"
+        elif what == 7:  # normalize_for_sorting vs the oracle (activations: <= 4 ulp)
+            from paper_2312_13299_b200.splats import normalize_features
+            from oracle import prep as oprep
+            n = int(g.integers(1, 3000))
+            chans = {"position": 3, "sh_dc": 3, "sh_rest": 45 if g.random() < 0.3 else 0, "opacity": 1,
+                     "scale": 3, "rotation": 4}
+            attrs = {}
+            for a, C in chans.items():
+                v = values((n, C)) if C else np.zeros((n, 0))
+                if a in ("opacity", "scale"):
+                    v = np.clip(v, -50.0, 50.0)  # finite activations
+                attrs[a] = v
+            wts = {a: float(g.choice([0.0, 0.5, 1.0, 2.0])) for a in chans}
+            feats, mins, maxs = normalize_features(attrs, wts)
+            ofe, omi, oma = oprep.normalize_columns(attrs, wts)
+            feats = feats.cpu().numpy()
+
+            def ulp(a, b):
+                a = np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+                b = np.ascontiguousarray(b, dtype=np.float64).view(np.int64)
+                return int(np.abs(a - b).max(initial=0))
+            ok = feats.shape == ofe.shape
+            why = ""
+            for a in chans:
+                tol = 4 if a in ("opacity", "scale") else 0
+                um, uM = ulp(mins[a].cpu().numpy(), omi[a]), ulp(maxs[a].cpu().numpy(), oma[a])
+                if um > tol or uM > tol:
+                    ok = False
+                    why += f" {a}: min/max ulp {um}/{uM}"
+            if ok:
+                col = 0
+                for a in ("position", "sh_dc", "sh_rest", "opacity", "scale", "rotation"):
+                    C = chans[a]
+                    if wts[a] == 0.0 or C == 0:
+                        continue
+                    got, exp = feats[:, col:col + C], ofe[:, col:col + C]
+                    if a in ("opacity", "scale"):
+                        # a last-bit difference of the activation (NumPy's SIMD exp is not
+                        # correctly rounded) is amplified by the affine map to ~ulp(max|v|) / span
+                        act = oprep.activate(a, attrs[a]).reshape(n, -1)
+                        span = np.maximum(oma[a] - omi[a], 1e-300)
+                        amp = 8 * np.spacing(np.abs(act).max(axis=0)) / span * wts[a]
+                        good = bool(np.all(np.abs(got - exp) <= amp + 1e-15 * wts[a]))
+                    else:
+                        good = bool(np.array_equal(got, exp))
+                    if not good:
+                        ok = False
+                        why += f" {a}: features"
+                    col += C
+            tag = f"normalize n={n} weights={wts}{why}"
         else:
             m, D = int(g.integers(1, 40)), int(g.integers(1, 20))
             n = m + int(g.integers(0, 10))
