@@ -625,12 +625,15 @@ double oracle_smoothness_plane(const double *plane, int H, int W, int C, double 
         free(cen);
         free(bl);
     }
-    double hsum = 0.0;
+    /* huber(residual).mean() (smoothness.py:88): elementwise values, then
+     * NumPy's pairwise sum over the contiguous array and one division */
+    double *hub = (double *)malloc(sizeof(double) * n);
     for (size_t i = 0; i < n; i++) {
         double a = fabs(res[i]);
-        hsum += a <= delta ? 0.5 * res[i] * res[i] : delta * (a - 0.5 * delta);
+        hub[i] = a <= delta ? 0.5 * res[i] * res[i] : delta * (a - 0.5 * delta);
     }
-    double loss = coeff * (hsum / (double)n);
+    double loss = coeff * (np_pairwise(hub, (int64_t)n) / (double)n);
+    free(hub);
     double scale = coeff / (double)n;
     for (size_t i = 0; i < n; i++) {
         double r = res[i];

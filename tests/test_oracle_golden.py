@@ -136,5 +136,5 @@ def test_smoothness_golden():
                                             p.get("detach_target", False), p.get("sigma", 3.0),
                                             p.get("kernel_size", 5))
             total += loss
-            np.testing.assert_allclose(grad, z[f"{m['i']}_grad_{name}"], rtol=1e-12, atol=1e-300)
-        assert total == pytest.approx(m["loss"], rel=1e-12)
+            np.testing.assert_array_equal(grad, z[f"{m['i']}_grad_{name}"])
+        assert total == m["loss"]  # the mean in NumPy's pairwise order: the reference's float

@@ -2,7 +2,7 @@
 blur_target (API, f32 and f64) and the sort's blur tiers vs the C oracle's
 SciPy fold; grid_distance and vad vs NumPy's own expressions of the reference
 (plas.py:71-84, metrics.py:25-40); reassign_block, quantize_planes,
-prune_indices and normalize_for_sorting vs the oracle.  Shapes,
+prune_indices, normalize_for_sorting and smoothness_loss vs the oracle.  Shapes,
 radii (past the grid too), and value ranges (1e-20 .. 1e20 scales, zeros,
 constants, signed zeros) are drawn at random.  Prints every mismatch; exit 1
 if any.   usage: python tools/fuzz_api.py [cases] [seed]"""
@@ -54,7 +54,7 @@ def np_vad(grid):  # metrics.py:25-40
 
 bad = 0
 for c in range(cases):
-    what = int(g.integers(0, 8))
+    what = int(g.integers(0, 9))
     try:
         if what == 0:  # API blur, dtype preserving
             H, W, C = int(g.integers(1, 60)), int(g.integers(1, 60)), int(g.integers(1, 6))
@@ -160,6 +160,30 @@ for c in range(cases):
                         why += f" {a}: features"
                     col += C
             tag = f"normalize n={n} weights={wts}{why}"
+        elif what == 8:  # smoothness_loss vs the oracle (loss and gradients exact)
+            side = int(g.integers(2, 40))
+            names = [nm for nm in ("position", "sh_dc", "scale", "rotation", "opacity") if g.random() < 0.6] or ["opacity"]
+            chans = {"position": 3, "sh_dc": 3, "scale": 3, "rotation": 4, "opacity": 1}
+            planes = {nm: values((side, side, chans[nm])) for nm in names}
+            ks = int(g.choice([1, 3, 5, 7, 9, 11, 13, 21, 41]))
+            params = plas.SmoothnessParams(kernel_size=ks, sigma=float(g.uniform(0.3, 8.0)),
+                                           overall_multiplier=float(g.uniform(0.1, 3.0)),
+                                           huber_delta=float(10 ** g.uniform(-3, 2)),
+                                           weights={nm: float(g.choice([0.0, 0.3, 1.0])) for nm in names},
+                                           detach_target=bool(g.random() < 0.3))
+            loss, grads = plas.smoothness_loss(plas.GridStack(plas.GridLayout(side), planes), params)
+            total, ok = 0.0, True
+            for nm in names:
+                coeff = params.overall_multiplier * params.weights.get(nm, 0.0)
+                if coeff == 0.0:
+                    ok &= bool(np.all(grads[nm] == 0.0))
+                    continue
+                l1, g1 = O.smoothness_plane(planes[nm], coeff, params.huber_delta, params.detach_target,
+                                            params.sigma, params.kernel_size)
+                total += l1
+                ok &= bool(np.array_equal(grads[nm], g1))
+            ok &= loss == total
+            tag = f"smoothness side={side} k={ks} planes={names} {loss!r} {total!r}"
         else:
             m, D = int(g.integers(1, 40)), int(g.integers(1, 20))
             n = m + int(g.integers(0, 10))
