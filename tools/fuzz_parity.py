@@ -1,7 +1,7 @@
 """Randomised PARITY-vs-oracle sweep over small shapes and SortConfig values
 (side 2..48, D 1..24, decay, threshold, min block, start radius, value
 distributions).  Prints every mismatch; exit status 1 if any.
-usage: python tools/fuzz_parity.py [cases] [seed]"""
+usage: python tools/fuzz_parity.py [cases] [seed] [side_min] [side_max]"""
 import math
 import os
 import sys
@@ -14,9 +14,11 @@ from oracle import oracle as O  # noqa: E402
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 g = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+SMIN = int(sys.argv[3]) if len(sys.argv) > 3 else 2    # side range (defaults: 2 .. 48)
+SMAX = int(sys.argv[4]) if len(sys.argv) > 4 else 48
 bad = 0
 for c in range(cases):
-    side = int(g.integers(2, 49))
+    side = int(g.integers(SMIN, SMAX + 1))
     D = int(g.integers(1, 25))
     dist = g.integers(0, 4)
     n = side * side
