@@ -1,7 +1,7 @@
 """Randomised DEVICE-mode checks (no reference value exists for the device
 draws): valid permutation, run-to-run determinism, and the CUDA-graph run equal
 to the host-stepped run of the same kernels, over random shapes / configs /
-value ranges.  usage: python tools/fuzz_device.py [cases] [seed]"""
+value ranges.  usage: python tools/fuzz_device.py [cases] [seed] [side_min] [side_max]"""
 import os
 import sys
 
@@ -16,8 +16,10 @@ from tools.fuzz_dump import cases as gen  # noqa: E402
 
 ncases = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+smin = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+smax = int(sys.argv[4]) if len(sys.argv) > 4 else 48
 bad = 0
-for c, f, kw in gen(seed, ncases - 1):
+for c, f, kw in gen(seed, ncases - 1, smin, smax):
     kw["rng_mode"] = "device"
     n, D = f.shape
     cfg = plas.SortConfig(**kw)

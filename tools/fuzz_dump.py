@@ -8,10 +8,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 
-def cases(seed, upto):
+def cases(seed, upto, smin=2, smax=48):
     g = np.random.default_rng(seed)
     for c in range(upto + 1):
-        side = int(g.integers(2, 49)); D = int(g.integers(1, 25)); dist = g.integers(0, 4); n = side * side
+        side = int(g.integers(smin, smax + 1)); D = int(g.integers(1, 25)); dist = g.integers(0, 4); n = side * side
         if dist == 0: f = g.normal(0, 1, (n, D))
         elif dist == 1: f = g.uniform(0, 1, (n, D))
         elif dist == 2: f = g.integers(-2, 3, (n, D)).astype(np.float64)
