@@ -262,7 +262,7 @@ __device__ __forceinline__ void load_chunks(const float* Fb, const float* Tb, co
 template <bool OOL>  // exact tier out of line (wide rows)
 __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4][4], const float* Fb,
                                                const float* Tb, const int (&rowj)[4], int D, int S, int k,
-                                               int* exact);
+                                               int* exact, float (&col)[4]);
 
 // Exact tier for the whole warp (same decision wherever the fast one was
 // certain): lane s recomputes row s of the cost matrix with the reference
@@ -325,7 +325,8 @@ __device__ __noinline__ int decide_exact_call(const float* Fb, const float* Tb, 
 
 template <bool WIDE, bool TNC>
 __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const int (&rowj)[4],
-                                       const int (&rowt)[4], int D, int S, int k, float4 (&Fc)[4], int* exact) {
+                                       const int (&rowt)[4], int D, int S, int k, float4 (&Fc)[4], int* exact,
+                                       float (&col)[4]) {
   const int s = threadIdx.x & 3;
   const int nch = S >> 2;
   // fast-tier partial squared distances: acc[i][jj] holds the (even, odd)
@@ -343,13 +344,15 @@ __device__ __forceinline__ int decide4(const float* Fb, const float* Tb, const i
     load_chunks<TNC>(Fb, Tb, rowj, rowt, S, c, c < nch, Fc, Tc);
     accum_chunks(acc, Fc, Tc);
   }
-  return decide_from_acc<WIDE>(acc, Fb, Tb, rowj, D, S, k, exact);
+  return decide_from_acc<WIDE>(acc, Fb, Tb, rowj, D, S, k, exact, col);
 }
 
+// col[i] = the fast cost C[i][s] of slot i's element in target s (lane s of
+// the group), returned for the DEVICE-mode pass statistic (k3_delta_acc).
 template <bool OOL>  // exact tier out of line (wide rows)
 __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4][4], const float* Fb,
                                                const float* Tb, const int (&rowj)[4], int D, int S, int k,
-                                               int* exact) {
+                                               int* exact, float (&col)[4]) {
   const int lane = threadIdx.x & 31;
   const int s = lane & 3;
   const int gbase = lane & ~3;
@@ -363,7 +366,6 @@ __device__ __forceinline__ int decide_from_acc(const unsigned long long (&acc)[4
     }
   // reduce-scatter over the 4 lanes by column (rotated order, no selects):
   // lane s ends with column s of the cost matrix, col[i] = C[i][s]
-  float col[4];
 #pragma unroll
   for (int i = 0; i < 4; i++) {
     const float h0 = part[i][0] + __shfl_xor_sync(PLAS_FULL_MASK, part[i][2], 2);
@@ -440,7 +442,8 @@ __device__ __forceinline__ void move_index(int* __restrict__ idx, bool my_mv, in
 // memory and append them to list[] with one reservation on *count per flush.
 struct MoveOut {
   int* list;
-  int* count;
+  int* count;                // moved cells of the pass (the list length when the list is staged)
+  unsigned long long* acc;   // DEVICE mode: the pass's 128-bit fixed-point distance change
 };
 
 constexpr int WARP_LIST = 512;  // shared staging entries per warp
@@ -485,6 +488,66 @@ __device__ __forceinline__ void flush_moves(const MoveOut& mo, int* s_list, int 
   int off = *s_base;
   for (int w = 0; w < wid; w++) off += s_wcnt[w];
   for (int i = lane; i < wcnt; i += 32) mo.list[off + i] = s_list[wid * CAP + i];
+}
+
+// DEVICE-mode pass statistic, formed in K3 (no moved-cell list, no per-cell
+// distance recomputation).  Lane s of a group holds column s of the fast cost
+// matrix (col[i] = C[i][s], decide_from_acc); when the decision brings slot
+// src's element into target s, that cell's distance changes by
+// C[src][s] - C[s][s].  Each change is rounded to a multiple of 2^-64 (fx64)
+// and summed as a 128-bit integer, so the pass total does not depend on which
+// lane, CTA or rank handled the group: DEVICE sorts repeat bit for bit and a
+// sharded sort sums to the 1-GPU total.  The fast costs are within
+// (D/2 + 7) 2^-24 (relative) of the reference's, so the running mean drifts
+// from grid_distance by < 1e-6 of the moved cells' distance per pass and is
+// re-anchored exactly at every level start (level_stats_kernel); changes that
+// are not finite or beyond fx64's range (|change| >= 2^86: fp32 costs that
+// overflowed) are dropped.  PARITY mode keeps the exact per-cell fp64 changes
+// (pass_stats_kernel over the moved-cell list): its strike decisions must be
+// the reference's.
+__device__ __forceinline__ void k3_delta_acc(const float (&col)[4], unsigned code, int s, __int128* q) {
+  int src = s;
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+    if (((code >> (2 * i)) & 3u) == (unsigned)s) src = i;
+  if (src != s) {
+    const double dd = (double)pick4(col, src) - (double)pick4(col, s);
+    if (fabs(dd) < 7.7371252455336267e25) *q += fx64(dd);  // 2^86
+  }
+}
+
+// End of a pass kernel: the CTA's moved-cell count and (DEVICE) its 128-bit
+// distance change, one atomic each per CTA.  Called by every thread.
+template <bool KD>
+__device__ __forceinline__ void k3_cta_epilogue(const MoveOut& mo, int nmv, __int128 q) {
+  __shared__ __int128 sq[32];
+  __shared__ int sn[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  nmv = __reduce_add_sync(PLAS_FULL_MASK, nmv);
+  if (KD) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += shfl_xor_i128(q, o);
+  }
+  if (lane == 0) {
+    sn[wid] = nmv;
+    if (KD) sq[wid] = q;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    __int128 b = 0;
+    for (int w = 0; w < nw; w++) {
+      t += sn[w];
+      if (KD) b += sq[w];
+    }
+    if (t) atomicAdd(mo.count, t);
+    if (KD && b != 0) {
+      const unsigned long long lo = (unsigned long long)b;
+      const unsigned long long old = atomicAdd(mo.acc, lo);
+      const unsigned long long carry = old + lo < old ? 1ull : 0ull;
+      atomicAdd(mo.acc + 1, (unsigned long long)((unsigned __int128)b >> 64) + carry);
+    }
+  }
 }
 
 // per-pass class tables in shared memory
@@ -535,6 +598,12 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
   const int nch = S >> 2;
   const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
   int exact = 0;
+  // the moved-cell list: PARITY (the statistics kernel recomputes the moved
+  // cells' exact distances) and sharded sorts (the exchange); DEVICE mode on
+  // one GPU only counts the moves
+  const bool stage = PARITY || ctrl->world > 1;
+  int nmv = 0;
+  __int128 dq = 0;  // DEVICE: this lane's fixed-point distance change (k3_delta_acc)
   // geometry of group g for lane slot s; the table entry load is issued here
   // and consumed one iteration later (prefetch)
   struct Geo {
@@ -577,8 +646,10 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
       rowt[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + (j ^ s));
     }
     float4 Fc[4];
-    const int bp = decide4<WIDE, true>(feat, target, rowj, rowt, D, S, k, Fc, &exact);
+    float col[4];
+    const int bp = decide4<WIDE, true>(feat, target, rowj, rowt, D, S, k, Fc, &exact, col);
     const unsigned code = perm_dest_code(k, bp);
+    if (!PARITY) k3_delta_acc(col, code, s, &dq);
     int dst[4], dcl[4];
     bool mv[4];
 #pragma unroll
@@ -613,9 +684,13 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
     }
     const int dcell = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + my_dst);
     move_index(idx, my_mv, cell, dcell, my_idx, lazy);
-    stage_move(my_mv, dcell, wlist, &wcnt, mo);
+    if (stage)
+      stage_move(my_mv, dcell, wlist, &wcnt, mo);
+    else
+      nmv += my_mv;
   }
-  flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  if (stage) flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  k3_cta_epilogue<!PARITY>(mo, nmv, dq);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
   gtrace_mark(ctrl, 1);
@@ -660,6 +735,9 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
   const int lane = threadIdx.x & 31, s = lane & 3, gl = threadIdx.x >> 2;
   const bool cvalid = s < nch;
   int exact = 0;
+  const bool stage = PARITY || ctrl->world > 1;  // moved-cell list (see pass_kernel)
+  int nmv = 0;
+  __int128 dq = 0;
   // (slot count, this lane's cell) of group g; cell 0 for absent slots
   auto group_cell = [&](unsigned g, int* k) {
     *k = 0;
@@ -716,8 +794,10 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
 #pragma unroll
       for (int j = 0; j < 4; j++) acc[i][j] = 0ull;
     accum_chunks(acc, Fc, Tc);
-    const int bp = decide_from_acc<false>(acc, feat, target, rowj, D, S, k, &exact);
+    float col[4];
+    const int bp = decide_from_acc<false>(acc, feat, target, rowj, D, S, k, &exact, col);
     const unsigned code = perm_dest_code(k, bp);
+    if (!PARITY) k3_delta_acc(col, code, s, &dq);
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       const int dst = (int)((code >> (2 * i)) & 3u);
@@ -728,7 +808,10 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
     const bool my_mv = my_dst != s;
     const int dcell = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + my_dst);
     move_index(idx, my_mv, cell, dcell, my_idx, lazy);
-    stage_move(my_mv, dcell, wlist, &wcnt, mo);
+    if (stage)
+      stage_move(my_mv, dcell, wlist, &wcnt, mo);
+    else
+      nmv += my_mv;
     // ---- rotate
     k = nk;
     cell = ncell;
@@ -740,7 +823,8 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
     }
     my_idx = nidx;
   }
-  flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  if (stage) flush_moves(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  k3_cta_epilogue<!PARITY>(mo, nmv, dq);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
   gtrace_mark(ctrl, 1);
@@ -861,6 +945,9 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
   const int G = gridDim.x;
 
   int exact = 0;
+  const bool stage = PARITY || ctrl->world > 1;  // moved-cell list (see pass_kernel)
+  int nmv = 0;
+  __int128 dq = 0;
   if (threadIdx.x >= TILE_THREADS) {
     // ---- producer warp: block it of this CTA into stage it % TILE_NST once
     // the consumers released that stage's previous block (bulk copies are
@@ -923,8 +1010,10 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
         rowt[j] = __shfl_sync(PLAS_FULL_MASK, myrow, (lane & ~3) + (j ^ s));
       }
       float4 Fc[4];
-      const int bp = decide4<WIDE, false>(sF, sT, rowj, rowt, D, S, k, Fc, &exact);
+      float col[4];
+      const int bp = decide4<WIDE, false>(sF, sT, rowj, rowt, D, S, k, Fc, &exact, col);
       const unsigned code = perm_dest_code(k, bp);
+      if (!PARITY) k3_delta_acc(col, code, s, &dq);
       int dst[4];
       bool mv[4];
 #pragma unroll
@@ -952,12 +1041,16 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
       const bool my_mv = my_dst != s;
       const int dcell = __shfl_sync(PLAS_FULL_MASK, mycell, (lane & ~3) + my_dst);
       move_index(idx, my_mv, mycell, dcell, my_idx, lazy);
-      stage_move<TILE_WARP_LIST>(my_mv, dcell, wlist, &wcnt, mo);
+      if (stage)
+        stage_move<TILE_WARP_LIST>(my_mv, dcell, wlist, &wcnt, mo);
+      else
+        nmv += my_mv;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[st]);  // this warp is done with stage st
   }
-  flush_moves<TILE_WARP_LIST>(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  if (stage) flush_moves<TILE_WARP_LIST>(mo, s_list, wcnt, ps.wcnt, &ps.base);
+  k3_cta_epilogue<!PARITY>(mo, nmv, dq);
   const int ex = __reduce_add_sync(PLAS_FULL_MASK, exact);
   if (lane == 0 && ex) atomicAdd(counters + 1, ex);
   gtrace_mark(ctrl, 1);
@@ -1024,7 +1117,8 @@ __global__ void __launch_bounds__(256) groups_kernel(float* __restrict__ feat,
       rowt[j] = __shfl_sync(PLAS_FULL_MASK, cell, (lane & ~3) + (j ^ s));
     }
     float4 Fc[4];
-    const int bp = decide4<WIDE, true>(feat, target, rowj, rowt, D, S, k, Fc, &exact);
+    float col[4];
+    const int bp = decide4<WIDE, true>(feat, target, rowj, rowt, D, S, k, Fc, &exact, col);
     int dst[4];
     bool mv[4];
 #pragma unroll

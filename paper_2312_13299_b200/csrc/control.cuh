@@ -314,15 +314,19 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
       __shared__ int rec[PREC_INTS];
       for (int i = threadIdx.x; i < PREC_INTS; i += blockDim.x) rec[i] = prec[(long long)pass * PREC_INTS + i];
       __syncthreads();
-      const long long per = (long long)blockDim.x * nworkers;
+      int start = 0;  // chunks of the earlier classes: the work is spread over (class, chunk) pairs
       for (int cls = 0; cls < 9; cls++) {
         const unsigned m = (unsigned)rec[cls];
         if (!m) continue;
         Feistel fe;
         fe.init_keys(reinterpret_cast<const unsigned*>(rec + 27 + 6 * cls), rec[9 + cls], rec[18 + cls], m);
         const unsigned ww = (unsigned)rec[PREC_WW + cls];
-        for (long long l = worker * (long long)blockDim.x + threadIdx.x; l < m; l += per)
-          tab[cls * stride + l] = pack_local(fe((unsigned)l), ww);
+        const int nch = (int)((m + blockDim.x - 1) / blockDim.x);
+        for (int ch = ((worker - start) % nworkers + nworkers) % nworkers; ch < nch; ch += nworkers) {
+          const unsigned l = (unsigned)ch * blockDim.x + threadIdx.x;
+          if (l < m) tab[cls * stride + l] = pack_local(fe(l), ww);
+        }
+        start += nch;
       }
       return;
     }
@@ -346,15 +350,19 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
     mcls[threadIdx.x] = (exists(ty, nx.nby) && exists(tx, nx.nbx)) ? nx.seg_h[ty] * nx.seg_w[tx] : 0;
   }
   __syncthreads();
-  const long long per = (long long)blockDim.x * nworkers;
+  int start = 0;
   for (int cls = 0; cls < 9; cls++) {
     const unsigned m = (unsigned)mcls[cls];
     if (!m) continue;
     Feistel fe;
     fe.init_keys(nx.fe_keys[cls], nx.fe_lbits[cls], nx.fe_rbits[cls], m);
     const unsigned ww = (unsigned)nx.seg_w[cls % 3];
-    for (long long l = worker * (long long)blockDim.x + threadIdx.x; l < m; l += per)
-      tab[cls * stride + l] = pack_local(fe((unsigned)l), ww);
+    const int nch = (int)((m + blockDim.x - 1) / blockDim.x);
+    for (int ch = ((worker - start) % nworkers + nworkers) % nworkers; ch < nch; ch += nworkers) {
+      const unsigned l = (unsigned)ch * blockDim.x + threadIdx.x;
+      if (l < m) tab[cls * stride + l] = pack_local(fe(l), ww);
+    }
+    start += nch;
   }
 }
 
@@ -598,6 +606,58 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   __shared__ unsigned long long s_gkey;
   if (c->level_done) return;  // an unrolled pass slot after the level ended (no CTA takes a ticket)
   gtrace_mark(c, 2);
+  if (c->rng_mode == 1) {
+    // DEVICE mode: K3 already summed the pass's distance change (k3_delta_acc,
+    // 128-bit fixed point in partials[0..1]) and counted the moves, so no CTA
+    // waits for another: CTA 0 runs the controller at once while the others
+    // build the next pass's grouping tables.
+    const bool gen = tab != nullptr;
+    if (blockIdx.x != 0) {
+      if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, blockIdx.x - 1, gridDim.x - 1);
+      if (c->gtrace) {
+        __syncthreads();
+        gtrace_mark(c, 5);
+      }
+      return;
+    }
+    __shared__ int s_count;
+    __shared__ __int128 s_raw;
+    if (threadIdx.x == 0) {
+      volatile unsigned long long* va = reinterpret_cast<unsigned long long*>(partials);
+      const unsigned long long lo = va[0], hi = va[1];
+      va[0] = 0ull;
+      va[1] = 0ull;
+      s_raw = (__int128)(((unsigned __int128)hi << 64) | (unsigned __int128)lo);
+      s_tot = fx64_to_double(s_raw);
+      s_count = counters[2];
+    }
+    __syncthreads();
+    gtrace_mark(c, 4);
+    if (c->world > 1) {  // sharded: publish this rank's exact partial; shard_control_kernel decides
+      if (threadIdx.x == 0) {
+        store_i128(xpart, s_raw);
+        xpart[2] = (double)s_count;
+        xpart[3] = 0.0;
+      }
+      return;
+    }
+    __shared__ Ctrl sc;
+    Ctrl* const cg = c;
+    ctrl_to_smem(&sc, cg);
+    bool more = false;
+    if (threadIdx.x == 0) {
+      counters[0] += s_count;
+      counters[2] = 0;
+      more = controller_step(&sc, s, s_tot, n, inner);
+    }
+    more = __syncthreads_or(more);
+    if (more) prepare_device_pass_cta(&sc, &s_gkey);
+    if (!more && outer && threadIdx.x == 0) level_end_work(&sc, s, outer);
+    if (cg->gtrace && threadIdx.x == 0) atomicMax(&cg->gtrace[6 * (sc.reorders - 1) + 3], gtimer());
+    ctrl_from_smem(cg, &sc);
+    if (gen && gridDim.x == 1) gen_class_tables(&sc, sc.pass, tab, tab_stride, 0, 1);
+    return;
+  }
   const int count = counters[2];
   __int128 sum = 0;  // fixed point (fx64): order-free
   const int stride = gridDim.x * blockDim.x;

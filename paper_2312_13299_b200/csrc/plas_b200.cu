@@ -1055,7 +1055,7 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
 
   const int sgrid = stats_grid_size();
   int* counters = w.flags + 2;  // [0] moved cells, [1] exact decisions, [2] moved-list length
-  MoveOut ml{w.list, counters + 2};
+  MoveOut ml{w.list, counters + 2, reinterpret_cast<unsigned long long*>(w.spart + MAX_PARTS)};
   int* done = w.flags + 6;      // last-CTA ticket of the statistic kernels
   if (htrace) fprintf(stderr, "host: graph/loop start at %.3f ms\n", hms());
   long long banded_levels = 0;
