@@ -420,6 +420,11 @@ __device__ __forceinline__ unsigned group_entry(const int* __restrict__ sel, lon
                                                 unsigned q, int s) {
   return (unsigned)__ldg(sel + (long long)cls * sel_stride + 4 * q + s);
 }
+#ifdef PLAS_DEBUG_BOUNDS
+#define PLAS_DBG_E(e) e_
+#else
+#define PLAS_DBG_E(e) e
+#endif
 __device__ __forceinline__ int entry_cell_off(unsigned e, int side) { return (int)(e >> 16) * side + (int)(e & 0xffffu); }
 __device__ __forceinline__ int entry_row(unsigned e, int ww) { return (int)(e >> 16) * ww + (int)(e & 0xffffu); }
 
@@ -583,7 +588,10 @@ __global__ void __launch_bounds__(256, WIDE ? 2 : K3_MINB) pass_kernel(float* __
   load_pass_shared(ps, ctrl);
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
-  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) {
+    const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+    const_cast<Ctrl*>(ctrl)->gen_level = ctrl->level;
+  }
   int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
   int wcnt = 0;
   const int side = ctrl->side;
@@ -719,7 +727,10 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
   gtrace_mark(ctrl, 0);
   load_pass_shared(ps, ctrl);
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
-  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) {
+    const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+    const_cast<Ctrl*>(ctrl)->gen_level = ctrl->level;
+  }
   int* wlist = s_list + (threadIdx.x >> 5) * WARP_LIST;
   int wcnt = 0;
   const int side = ctrl->side;
@@ -755,7 +766,18 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
         *k = rem >= 4 ? 4 : rem;
         const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
         const int x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
-        if (s < *k) cell = y0 * side + x0 + entry_cell_off(group_entry(selp, sel_stride, ty * 3 + tx, q, s), side);
+        if (s < *k) {
+          const unsigned e = group_entry(selp, sel_stride, ty * 3 + tx, q, s);
+          cell = y0 * side + x0 + entry_cell_off(e, side);
+#ifdef PLAS_DEBUG_BOUNDS
+          if ((int)(e >> 16) >= hh || (int)(e & 0xffffu) >= ww || cell < 0 || cell >= side * side)
+          {
+            printf("K3pipe bad entry: lvl %d pass %d cls %d q %u s %d e %08x hh %d ww %d cell %d\n", ctrl->level,
+                   ctrl->pass, ty * 3 + tx, q, s, e, hh, ww, cell);
+            cell = y0 * side + x0;
+          }
+#endif
+        }
       }
     }
     return cell;
@@ -925,7 +947,10 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
   load_pass_shared(ps, ctrl);  // (its __syncthreads also publishes the barriers)
   // DEVICE: the grouping tables of this pass's parity (gen_class_tables)
   const int* selp = PARITY ? sel : sel + (long long)(ctrl->pass & 1) * 9 * sel_stride;
-  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+  if (!PARITY && blockIdx.x == 0 && threadIdx.x == 0) {
+    const_cast<Ctrl*>(ctrl)->gen_pass = ctrl->pass + 1;
+    const_cast<Ctrl*>(ctrl)->gen_level = ctrl->level;
+  }
   int* wlist = s_list + (threadIdx.x >> 5) * TILE_WARP_LIST;
   int wcnt = 0;
   const int side = ctrl->side;
@@ -1000,9 +1025,19 @@ __global__ void __launch_bounds__(TILE_CTA_THREADS, WIDE ? 2 : TILE_MINB) tile_p
       const int k = knext;
       const unsigned e = enext;
       group_at(q0 + TILE_THREADS / 4 + gl, &knext, &enext);
+#ifdef PLAS_DEBUG_BOUNDS
+      unsigned e_ = e;
+      if (s < k && ((int)(e >> 16) >= g.hh || (int)(e & 0xffffu) >= g.ww)) {
+        printf("K3tile bad entry: lvl %d pass %d cls %d q %d s %d e %08x hh %d ww %d\n", ctrl->level, ctrl->pass,
+               g.cls, q0 + gl, s, e, g.hh, g.ww);
+        e_ = 0u;
+      }
+      const int mycell = origin + entry_cell_off(e_, side);
+#else
       const int mycell = origin + entry_cell_off(e, side);
+#endif
       const int my_idx = (!lazy && s < k) ? __ldg(idx + mycell) : 0;  // consumed after the decision
-      const int myrow = entry_row(e, g.ww);
+      const int myrow = entry_row(PLAS_DBG_E(e), g.ww);
       int rowj[4], rowt[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) {

@@ -73,6 +73,7 @@ struct Ctrl {
   unsigned lv_cap_m, lv_seg_m[2];
   int lv_cap_l, lv_seg_l[2], lv_seg_base, lv_cap;
   int gen_pass;                    // pass whose grouping tables gen_tables_kernel builds
+  int gen_level;                   // its level (written with gen_pass by K3; the controller never touches it)
   // multi-GPU, per level (set_level_shard_kernel): banded = this level's
   // passes split by block rows whose first row lies in [own_lo, own_hi) (the
   // rank's share of rows); the rank keeps target / distance cache valid on

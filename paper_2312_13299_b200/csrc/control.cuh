@@ -299,17 +299,24 @@ __device__ __forceinline__ void ctrl_from_smem(Ctrl* dst, const Ctrl* src) {
 // CTA derives the pass's geometry and keys itself and fills its slice of the
 // tables; the pass kernel then looks groupings up instead of evaluating the
 // Feistel network (and its cycle walk) per lane.  Called by all threads.
+// `level`: the level whose pass `pass` the tables are for (-1: cg->level).
+// Callers running beside a controller CTA that may rewrite Ctrl (the
+// statistics kernels' other CTAs) pass a value that CTA never changes while
+// they run (Ctrl.gen_level written by K3, or Ctrl.level read before the
+// ticket): the fast/slow path choice below must be CTA-uniform, and the slow
+// path must not mix two levels' state.
 __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* __restrict__ tab0, long long stride,
-                                                 int worker = -1, int nworkers = 0) {
+                                                 int worker = -1, int nworkers = 0, int level = -1, bool spread = true) {
   if (worker < 0) {
     worker = blockIdx.x;
     nworkers = gridDim.x;
   }
+  if (level < 0) level = cg->level;
   int* __restrict__ tab = tab0 + (long long)(pass & 1) * 9 * stride;  // double-buffered by pass parity
   {
     // fast path: the pass's record precomputed at level start (pass_draws_kernel)
     const int* prec = cg->prec;
-    const bool ok = prec && cg->pdraw_level == cg->level && pass < PDRAW_MAX;
+    const bool ok = prec && cg->pdraw_level == level && pass < PDRAW_MAX;
     if (ok) {
       __shared__ int rec[PREC_INTS];
       for (int i = threadIdx.x; i < PREC_INTS; i += blockDim.x) rec[i] = prec[(long long)pass * PREC_INTS + i];
@@ -322,7 +329,7 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
         fe.init_keys(reinterpret_cast<const unsigned*>(rec + 27 + 6 * cls), rec[9 + cls], rec[18 + cls], m);
         const unsigned ww = (unsigned)rec[PREC_WW + cls];
         const int nch = (int)((m + blockDim.x - 1) / blockDim.x);
-        for (int ch = ((worker - start) % nworkers + nworkers) % nworkers; ch < nch; ch += nworkers) {
+        for (int ch = spread ? ((worker - start) % nworkers + nworkers) % nworkers : worker; ch < nch; ch += nworkers) {
           const unsigned l = (unsigned)ch * blockDim.x + threadIdx.x;
           if (l < m) tab[cls * stride + l] = pack_local(fe(l), ww);
         }
@@ -336,6 +343,7 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
   __shared__ int mcls[10];
   ctrl_to_smem(&nx, cg);
   if (threadIdx.x == 0) {
+    nx.level = level;
     nx.pass = pass;
     int dy, dx;
     device_pass_draws(&nx, &dy, &dx, &gk);
@@ -371,7 +379,7 @@ __device__ __forceinline__ void gen_class_tables(const Ctrl* cg, int pass, int* 
 // gen_pass was set by the pass kernel, so the controller's update of pass
 // does not race with it).
 __global__ void __launch_bounds__(256) gen_tables_kernel(const Ctrl* c, int* tab, long long stride) {
-  gen_class_tables(c, c->gen_pass, tab, stride);
+  gen_class_tables(c, c->gen_pass, tab, stride, -1, 0, c->gen_level);
 }
 
 // Last-CTA-done protocol: every CTA writes its partial, fences and takes a
@@ -515,14 +523,18 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
   __shared__ double s_tot;
   __shared__ unsigned long long s_gkey;
   const int side = c->side;
+  const int lev0 = c->level;  // read before the ticket: the last CTA may rewrite Ctrl after it
   const long long i0 = (long long)c->band_lo * side, i1 = (long long)c->band_hi * side;
   const long long o0 = (long long)c->own_lo * side, o1 = (long long)c->own_hi * side;
   __int128 sum = 0;
+  // the per-cell cache feeds PARITY mode's moved-cell statistic only (DEVICE
+  // mode forms its pass changes in K3, k3_delta_acc)
+  const bool keep = c->rng_mode != 1;
   for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < i1;
        i += (long long)gridDim.x * blockDim.x) {
     const double d = sqrt(S == 16 ? cell_dist2_s16(feat + i * 16, target + i * 16, D)
                                    : cell_dist2(feat + i * S, target + i * S, D, S));
-    dcache[i] = d;
+    if (keep) dcache[i] = d;
     if (i >= o0 && i < o1) sum += fx64(d);
   }
   const bool gen = tab && c->rng_mode == 1;
@@ -530,7 +542,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) level_stats_kernel(
   __int128 raw = 0;
   if (!last_cta_reduce_fx(sum, reinterpret_cast<unsigned long long*>(acc), done, &s_tot, &ticket, &raw)) {
     // pass 0's tables, built by the other CTAs (ticket order) while the last one finishes
-    if (gen) gen_class_tables(c, 0, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
+    if (gen) gen_class_tables(c, 0, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1, lev0);
     return;
   }
   if (c->world > 1) {
@@ -613,7 +625,10 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
     // build the next pass's grouping tables.
     const bool gen = tab != nullptr;
     if (blockIdx.x != 0) {
-      if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, blockIdx.x - 1, gridDim.x - 1);
+      // (per-class slices here, not spread over (class, chunk) pairs as at level
+      // start: the spread form made concurrent sorts from several host threads
+      // fail with illegal addresses now and then -- not understood, so not used)
+      if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, blockIdx.x - 1, gridDim.x - 1, c->gen_level, false);
       if (c->gtrace) {
         __syncthreads();
         gtrace_mark(c, 5);
@@ -762,7 +777,7 @@ __global__ void __launch_bounds__(RED_THREADS, STATS_MINB) pass_stats_kernel(
   int ticket = 0;
   __int128 raw = 0;
   if (!last_cta_reduce_fx(sum, reinterpret_cast<unsigned long long*>(partials), done, &s_tot, &ticket, &raw)) {
-    if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1);
+    if (gen) gen_class_tables(c, c->gen_pass, tab, tab_stride, ticket, gridDim.x > 1 ? gridDim.x - 1 : 1, c->gen_level);
     if (c->gtrace) {
       __syncthreads();
       gtrace_mark(c, 5);  // this CTA's table slice is done
@@ -837,7 +852,8 @@ __global__ void shard_apply_kernel(const int2* __restrict__ recv, long long stri
       for (int c = 0; c < nch; c++)
         reinterpret_cast<float4*>(feat + cell * S)[c] = reinterpret_cast<const float4*>(orig32 + el * S)[c];
       idx[cell] = (int)el;
-      if (cell >= c0 && cell < c1) dcache[cell] = sqrt(cell_dist2(feat + cell * S, target + cell * S, D, S));
+      if (ctrl->rng_mode != 1 && cell >= c0 && cell < c1)  // PARITY's distance cache (see level_stats_kernel)
+        dcache[cell] = sqrt(cell_dist2(feat + cell * S, target + cell * S, D, S));
     }
   }
 }

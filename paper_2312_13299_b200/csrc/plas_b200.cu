@@ -1093,8 +1093,14 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                     lc.sched, (unsigned long long)blur_h, (unsigned long long)tile_h, w.pdraw, w.prec, w.rowweight,
                     lc.lvl, (const int*)w.lvl_mode, (const FftPlan*)w.fft_plans, NPL, ndraw, nrow));
     }
-    CK(add_kernel(&nd[2], obody, &nd[1], 1, border_weight32_kernel, dim3(lc.den_grid), dim3(256),
-                  (const double*)w.rowweight, (const double*)w.rowweight, w.den32, side, side, lc.lvl));
+    // the certified border weight (den32) is needed by the blur's axis-1 pass
+    // only: each blur body runs it beside the axis-0 pass (a node of its own
+    // body, joined before axis 1), off the level's critical path
+    auto add_border = [&](cudaGraphNode_t* bw, cudaGraph_t body) {
+      return add_kernel(bw, body, nullptr, 0, border_weight32_kernel, dim3(lc.den_grid), dim3(256),
+                        (const double*)w.rowweight, (const double*)w.rowweight, w.den32, side, side, lc.lvl);
+    };
+    nd[2] = nd[1];
     // SWITCH (blur mode of the level) { FFT at length 0 | ... | FFT at length
     // NPL - 1 | one tile kernel | direct fold + fallbacks }
     cudaGraphNode_t blur_if;
@@ -1135,7 +1141,11 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       void* a1[] = {&in1, &out1, &pg, &lv, &pl, &den, &fb1, &cap, &fb0};
       kp.func = fft1s[i];
       kp.kernelParams = a1;
-      CK(cudaGraphAddKernelNode(&fn[3], bbody[i], &fn[2], 1, &kp));
+      CK(add_border(&fn[0], bbody[i]));
+      {
+        cudaGraphNode_t deps[2] = {fn[2], fn[0]};
+        CK(cudaGraphAddKernelNode(&fn[3], bbody[i], deps, 2, &kp));
+      }
       CK(add_kernel(&fn[4], bbody[i], &fn[3], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
     }
@@ -1152,8 +1162,9 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
       kp.blockDim = dim3(TB_THREADS);
       kp.sharedMemBytes = (unsigned)tile_blur_smem_bytes(std::max(hc.tile_blur_hmax, 1));
       kp.kernelParams = ta;
-      cudaGraphNode_t tn;
-      CK(cudaGraphAddKernelNode(&tn, bbody[NPL], nullptr, 0, &kp));
+      cudaGraphNode_t tn, bw;
+      CK(add_border(&bw, bbody[NPL]));
+      CK(cudaGraphAddKernelNode(&tn, bbody[NPL], &bw, 1, &kp));
     }
     // direct fold: the runtime-h kernels (case NPL + 1) and the compile-time-h
     // kernels of h = 1 .. PAD_SMALL_HMAX (case NPL + 1 + h)
@@ -1166,7 +1177,10 @@ int plas_sort(const plas_sort_args* a, plas_sort_result* res, void* wsp, size_t 
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap, w.fb1));
       CK(add_kernel(&bn[1], db, &bn[0], 1, blur_pad_fallback_kernel<0, 0>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.feat, w.tmp, lc.pg, lc.lvl, (const float*)nullptr, w.fb0, w.fb_cap));
-      CK(add_kernel(&bn[2], db, &bn[1], 1, p1, dim3(lc.blur_grid), dim3(256),
+      cudaGraphNode_t bw;
+      CK(add_border(&bw, db));
+      const cudaGraphNode_t d2[2] = {bn[1], bw};
+      CK(add_kernel(&bn[2], db, d2, 2, p1, dim3(lc.blur_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap, w.fb0));
       CK(add_kernel(&bn[3], db, &bn[2], 1, blur_pad_fallback_kernel<1, 1>, dim3(lc.fb_grid), dim3(256),
                     (const float*)w.tmp, w.target, lc.pg, lc.lvl, (const float*)w.den32, w.fb1, w.fb_cap));
