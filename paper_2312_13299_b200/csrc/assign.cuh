@@ -749,10 +749,21 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
   const bool stage = PARITY || ctrl->world > 1;  // moved-cell list (see pass_kernel)
   int nmv = 0;
   __int128 dq = 0;
-  // (slot count, this lane's cell) of group g; cell 0 for absent slots
-  auto group_cell = [&](unsigned g, int* k) {
-    *k = 0;
-    int cell = 0;
+  // Group g's slot count, block origin and this lane's table entry.  The
+  // entry load is issued two groups ahead (pre), so its L2 latency is not
+  // exposed between the geometry and the row gathers that depend on it.
+  struct Pre {
+    int k, base;
+    unsigned e;
+#ifdef PLAS_DEBUG_BOUNDS
+    int hh, ww;
+#endif
+  };
+  auto group_pre = [&](unsigned g) {
+    Pre o;
+    o.k = 0;
+    o.base = 0;
+    o.e = 0u;
     if (g < total) {
       const unsigned b = fastdiv(g, cap_m, cap_l);
       const unsigned q = g - b * cap;
@@ -763,29 +774,37 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
       const int hh = ps.seg[ty], ww = ps.seg[3 + tx];
       const int rem = hh * ww - 4 * (int)q;
       if (rem >= 2) {  // a single leftover cell never moves
-        *k = rem >= 4 ? 4 : rem;
+        o.k = rem >= 4 ? 4 : rem;
         const int y0 = by == 0 ? 0 : fy + ((int)by - 1) * beta;
         const int x0 = bx == 0 ? 0 : fx + ((int)bx - 1) * beta;
-        if (s < *k) {
-          const unsigned e = group_entry(selp, sel_stride, ty * 3 + tx, q, s);
-          cell = y0 * side + x0 + entry_cell_off(e, side);
+        o.base = y0 * side + x0;
+        if (s < o.k) o.e = group_entry(selp, sel_stride, ty * 3 + tx, q, s);
 #ifdef PLAS_DEBUG_BOUNDS
-          if ((int)(e >> 16) >= hh || (int)(e & 0xffffu) >= ww || cell < 0 || cell >= side * side)
-          {
-            printf("K3pipe bad entry: lvl %d pass %d cls %d q %u s %d e %08x hh %d ww %d cell %d\n", ctrl->level,
-                   ctrl->pass, ty * 3 + tx, q, s, e, hh, ww, cell);
-            cell = y0 * side + x0;
-          }
+        o.hh = hh;
+        o.ww = ww;
 #endif
-        }
       }
     }
+    return o;
+  };
+  // (slot count, this lane's cell); cell 0 for absent slots
+  auto group_cell = [&](const Pre& o, int* k) {
+    *k = o.k;
+    int cell = s < o.k ? o.base + entry_cell_off(o.e, side) : 0;
+#ifdef PLAS_DEBUG_BOUNDS
+    if (s < o.k && ((int)(o.e >> 16) >= o.hh || (int)(o.e & 0xffffu) >= o.ww || cell < 0 || cell >= side * side)) {
+      printf("K3pipe bad entry: lvl %d pass %d s %d e %08x hh %d ww %d cell %d\n", ctrl->level, ctrl->pass, s, o.e,
+             o.hh, o.ww, cell);
+      cell = o.base;
+    }
+#endif
     return cell;
   };
   const unsigned stride = gridDim.x * 64u;
   unsigned g = g_lo + blockIdx.x * 64u + gl;
   int k;
-  int cell = group_cell(g, &k);
+  int cell = group_cell(group_pre(g), &k);
+  Pre pre = group_pre(g + stride);  // the next group's entry, in flight
   int rowj[4], rowt[4];
 #pragma unroll
   for (int j = 0; j < 4; j++) {
@@ -799,7 +818,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
     // ---- the next group's gathers go out first
     g += stride;
     int nk;
-    const int ncell = group_cell(g, &nk);
+    const int ncell = group_cell(pre, &nk);
     int nrowj[4], nrowt[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -808,6 +827,7 @@ __global__ void __launch_bounds__(256, K3P_MINB) pass_kernel_pipe(float* __restr
     }
     float4 nFc[4], nTc[4];
     load_chunks<true>(feat, target, nrowj, nrowt, S, s, cvalid, nFc, nTc);
+    pre = group_pre(g + stride);  // the entry of the group after next
     const int nidx = (!lazy && s < nk) ? idx[ncell] : 0;
     // ---- decide and apply the current group
     unsigned long long acc[4][4];
