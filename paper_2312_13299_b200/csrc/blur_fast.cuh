@@ -43,6 +43,21 @@ __device__ __forceinline__ void fb_append(bool need, int entry, int* __restrict_
   }
 }
 
+// fb_append for a converged warp (every lane calls it)
+__device__ __forceinline__ void fb_append_full(bool need, int entry, int* __restrict__ fb, int fb_cap) {
+  const unsigned bal = __ballot_sync(PLAS_FULL_MASK, need);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(bal) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(fb, __popc(bal));
+  base = __shfl_sync(PLAS_FULL_MASK, base, leader);
+  if (need) {
+    const int slot = base + __popc(bal & ((1u << lane) - 1u));
+    if (slot < fb_cap) fb[FB_HEADER + slot] = entry;
+  }
+}
+
 struct PadGeom {
   int H, W, C, S;
   int pad;        // zero elements before/after every line (>= hmax + BPAD_R)
@@ -101,9 +116,19 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
   make_fastdiv(nstrips, &ns_m, &ns_l);
   make_fastdiv((unsigned)S, &s_m, &s_l);
   make_fastdiv((unsigned)nchunks, &nc_m, &nc_l);
-  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  // Every lane of a warp runs the whole body (lanes past the work, on pad
+  // channels or past the line end compute on valid padded addresses and store
+  // nothing), so the fallback-list ballot below is a plain full-warp ballot:
+  // with lanes dropping out early, the compiler emulated it with
+  // match/collective sequences and local-memory spills (C2, h = 6: 48 M
+  // instructions per axis pass).
+  const unsigned total_w = (total + 31u) & ~31u;
+  for (unsigned tt = blockIdx.x * blockDim.x + threadIdx.x; tt < total_w; tt += gridDim.x * blockDim.x) {
+    const bool live = tt < total;
+    const unsigned t = live ? tt : total - 1u;
     long long in_base, out_base, cellbase = 0;
     int chunk, c;
+    bool valid = live;
     if (AXIS == 0) {
       // a CTA takes one 32-float column strip and 8 consecutive chunks, so its
       // warps share input rows in L1
@@ -112,8 +137,12 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
       const unsigned q = fastdiv(item, ns_m, ns_l);
       const unsigned strip = item - q * nstrips;
       chunk = (int)(q * 8 + (lt >> 5));
-      const unsigned f = strip * 32 + (lt & 31);
-      if ((long long)f >= WS || chunk >= nchunks) continue;
+      unsigned f = strip * 32 + (lt & 31);
+      if (chunk >= nchunks) continue;  // warp-uniform (one chunk per warp)
+      if ((long long)f >= WS) {
+        valid = false;
+        f = (unsigned)(WS - 1);
+      }
       chunk += chunk0;
       const unsigned cell = fastdiv(f, s_m, s_l);
       c = (int)(f - cell * (unsigned)S);
@@ -130,7 +159,7 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
       out_base = (long long)y * WS + c;
       cellbase = (long long)y * W;
     }
-    if (c >= C) continue;
+    valid = valid && c < C;  // pad channels: zero in, zero out (computed, not stored)
     const int i0 = chunk * R;
     const float* line = in + in_base;
     // lo ring: in[i0+k-h+t] at slot (k+t)%R ; hi ring: in[i0+k+h-t] at slot (k-t)%R
@@ -180,17 +209,28 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
       }
     }
     const double B = bscale * (double)mx;
+    unsigned unsure = 0u;
 #pragma unroll
     for (int k = 0; k < R; k++) {
       const int i = i0 + k;
-      if (i < n) {
-        const float a = __double2float_rn(__dsub_rn(acc[k], B));
-        const float bb = __double2float_rn(__dadd_rn(acc[k], B));
-        float r = __double2float_rn(acc[k]);
+      const bool ok = valid && i < n;
+      const float a = __double2float_rn(__dsub_rn(acc[k], B));
+      const float bb = __double2float_rn(__dadd_rn(acc[k], B));
+      float r = __double2float_rn(acc[k]);
+      if (ok && a != bb) unsure |= 1u << k;
+      if (ok) {
         const long long o = out_base + (long long)i * out_stride;
-        fb_append(a != bb, (int)(AXIS == 0 ? (long long)i * WS + in_base : o), fb, fb_cap);
         if (EPI == 1) r = __fdiv_rn(r, den32[cellbase + i]);
         out[o] = r;
+      }
+    }
+    // rare: uncertain outputs go to the fallback list (full-warp ballots)
+    if (__any_sync(PLAS_FULL_MASK, unsure != 0u)) {
+#pragma unroll
+      for (int k = 0; k < R; k++) {
+        const int i = i0 + k;
+        const long long o = out_base + (long long)i * out_stride;
+        fb_append_full((unsure >> k) & 1u, (int)(AXIS == 0 ? (long long)i * WS + in_base : o), fb, fb_cap);
       }
     }
   }
