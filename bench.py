@@ -636,8 +636,9 @@ def run_ours(args):
     # DEVICE (one graph) per level: set-up, border weight, blur (FFT: 2 + 2
     # fallback kernels for h >= 48 (side <= 1024) or 64; tile: 1 for h <= 4 and D <= 16;
     # direct: 2 + 2), level
-    # statistics, and the pass loop in iterations of 3 passes (K3 + statistics
-    # each; the slots after the level's last pass launch and return at once).
+    # statistics, and the pass loop in iterations of PLAS_PASS_UNROLL (default 6)
+    # passes (K3 + statistics each; the slots after the level's last pass
+    # launch and return at once).
     # PARITY (host-stepped) per level: begin, 2 border, blur (FFT adds the
     # spectrum kernel), level statistics, level end; per pass: set-pass, class
     # select, K3, statistics.
@@ -650,10 +651,11 @@ def run_ours(args):
             return 4 if device else 5
         return 1 if h <= 4 and D <= 16 else 4  # tile blur only for rows of <= 16 floats
     per_level = []
+    unroll = max(1, min(8, int(os.environ.get("PLAS_PASS_UNROLL", "6"))))  # plas_b200.cu pass_unroll()
     for r, tr in rep["radius_trace"]:
         h, p = math.ceil(r), len(tr) - 1
         if args.mode == "device":
-            per_level.append(2 + blur_launches(h, True) + 1 + 6 * (-(-p // 3)))
+            per_level.append(2 + blur_launches(h, True) + 1 + 2 * unroll * (-(-p // unroll)))
         else:
             per_level.append(3 + blur_launches(h, False) + 2 + 4 * p)
     launches = args.steps * (11 + sum(per_level))  # every timed step runs the same (deterministic) sort

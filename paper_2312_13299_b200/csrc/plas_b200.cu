@@ -648,12 +648,14 @@ void graph_cache_put(const GraphKey& k, const GraphExecRef& ge) {
   g_graphs.push_back({k, ge});
 }
 
-// passes per iteration of the graph's pass loop (PLAS_PASS_UNROLL, default 3: measured 1 -> 122.1, 2 -> 120.2, 3 -> 119.6, 4 -> 120.0 ms at C2)
+// passes per iteration of the graph's pass loop (PLAS_PASS_UNROLL; round 1: 1 -> 122.1, 2 -> 120.2, 3 -> 119.6,
+// 4 -> 120.0 ms at C2; round 2 with the lighter statistics node: 3 -> 105.2, 5 -> 104.8, 6 -> 104.6, 8 -> 104.9 ms,
+// C3 / C4 unchanged)
 int pass_unroll() {
   static std::atomic<int> v{0};
   if (!v) {
     const char* e = getenv("PLAS_PASS_UNROLL");
-    v = e ? std::max(1, std::min(8, atoi(e))) : 3;
+    v = e ? std::max(1, std::min(8, atoi(e))) : 6;
   }
   return v;
 }
