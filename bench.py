@@ -634,7 +634,7 @@ def run_ours(args):
 
     # kernels launched per sort by our library (plas_b200.cu): 6 init + 5 final;
     # DEVICE (one graph) per level: set-up, border weight, blur (FFT: 2 + 2
-    # fallback kernels for h >= 48 (side <= 1024) or 64; tile: 1 for h <= 4 and D <= 16;
+    # fallback kernels for h >= 48 (side <= 1024) or 64; tile: 1 for h <= PLAS_TILE_BLUR_HMAX (default 0: off);
     # direct: 2 + 2), level
     # statistics, and the pass loop in iterations of PLAS_PASS_UNROLL (default 6)
     # passes (K3 + statistics each; the slots after the level's last pass
@@ -649,7 +649,8 @@ def run_ours(args):
     def blur_launches(h, device):
         if h >= fft_min_h:
             return 4 if device else 5
-        return 1 if h <= 4 and D <= 16 else 4  # tile blur only for rows of <= 16 floats
+        hmax = int(os.environ.get("PLAS_TILE_BLUR_HMAX", "0"))  # plas_b200.cu tile_blur_hmax(): off by default
+        return 1 if h <= hmax and D <= 16 else 4
     per_level = []
     unroll = max(1, min(8, int(os.environ.get("PLAS_PASS_UNROLL", "6"))))  # plas_b200.cu pass_unroll()
     for r, tr in rep["radius_trace"]:

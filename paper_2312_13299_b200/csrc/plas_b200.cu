@@ -367,7 +367,12 @@ int tile_blur_hmax(int S) {
     v = e ? std::min(std::max(atoi(e), 0), TB_HMAX) : -1;
   }
   if (v >= 0) return v;
-  return S <= 16 ? 4 : 0;
+  // round 2: the direct fold with compile-time half-widths (converged warps)
+  // beats the one-kernel tile tier at every h <= 4 (C2: hmax 4 -> 104.6 ms,
+  // 2 -> 104.3, 0 -> 104.05; the tier stays available: PLAS_TILE_BLUR_HMAX,
+  // plas_blur_target_tiers tier 2)
+  (void)S;
+  return 0;
 }
 
 // relative error constant of the FFT convolution (blur_fft.cuh), x2 safety
