@@ -82,13 +82,21 @@ __host__ __device__ inline PadGeom make_pad_geom(int H, int W, int C, int S, int
 // the tap loop is fully static -- no partial tap block whose R unrolled steps
 // are all issued under predicates -- which halves the instructions per output
 // at h <= 8 (the direct tier's fixed cost dominated below h ~ 16).
+// Two adjacent channels per thread (float2 loads, 16 independent
+// accumulator chains).  Measured (same box, three runs each): C2 104.0 ->
+// 102.4 ms, C3 1.59 -> 1.58 s, C4 2.00 -> 1.96 s against one channel per
+// thread; the runtime-h kernel (h > 16) has a few spilled registers at the
+// 128-register cap and still wins.
+#ifndef BPAD_V
+#define BPAD_V 2
+#endif
+template <int HC> __host__ __device__ constexpr int bpad_v() { return BPAD_V; }
 template <int AXIS, int EPI, int HC = 0>
-__global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                       PadGeom pg, BlurLevelRef lvl,
-                                                       const float* __restrict__ den32,
-                                                       int* __restrict__ fb, int fb_cap,
-                                                       int* __restrict__ fb_other) {
+__global__ void __launch_bounds__(256, bpad_v<HC>() == 2 ? 2 : BPAD_MINB) blur_pad_kernel(
+    const float* __restrict__ in, float* __restrict__ out, PadGeom pg, BlurLevelRef lvl,
+    const float* __restrict__ den32, int* __restrict__ fb, int fb_cap, int* __restrict__ fb_other) {
   constexpr int R = BPAD_R;
+  constexpr int V = bpad_v<HC>();  // adjacent channels per thread (S is a multiple of 4)
   // the other axis' fallback list has been consumed by now: clear its counter
   if (blockIdx.x == 0 && threadIdx.x == 0 && fb_other) fb_other[0] = 0;
   int hrt;
@@ -108,14 +116,16 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
   const double w0 = __ldg(w);
   const double bscale = (2.0 * h + 4.0) * 2.0 * 1.1102230246251565e-16 * 1.0001;
   // 32-bit index math with multiply-shift division (every count < 2^31)
-  const unsigned nstrips = (unsigned)((WS + 31) / 32);
+  const unsigned SV = (unsigned)(S / V);  // channel groups per cell
+  const unsigned nstrips = (unsigned)((WS + 32 * V - 1) / (32 * V));
   const unsigned ncg = (unsigned)((nchunks + 7) / 8);
-  const unsigned total = AXIS == 0 ? nstrips * ncg * 256u : (unsigned)S * (unsigned)nchunks * (unsigned)nlines;
-  unsigned ns_m, s_m, nc_m;
-  int ns_l, s_l, nc_l;
+  const unsigned total = AXIS == 0 ? nstrips * ncg * 256u : SV * (unsigned)nchunks * (unsigned)nlines;
+  unsigned ns_m, s_m, nc_m, sv_m;
+  int ns_l, s_l, nc_l, sv_l;
   make_fastdiv(nstrips, &ns_m, &ns_l);
   make_fastdiv((unsigned)S, &s_m, &s_l);
   make_fastdiv((unsigned)nchunks, &nc_m, &nc_l);
+  make_fastdiv(SV, &sv_m, &sv_l);
   // Every lane of a warp runs the whole body (lanes past the work, on pad
   // channels or past the line end compute on valid padded addresses and store
   // nothing), so the fallback-list ballot below is a plain full-warp ballot:
@@ -130,18 +140,18 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
     int chunk, c;
     bool valid = live;
     if (AXIS == 0) {
-      // a CTA takes one 32-float column strip and 8 consecutive chunks, so its
-      // warps share input rows in L1
+      // a CTA takes one 32V-float column strip and 8 consecutive chunks, so
+      // its warps share input rows in L1
       const unsigned item = t >> 8;
       const int lt = (int)(t & 255);
       const unsigned q = fastdiv(item, ns_m, ns_l);
       const unsigned strip = item - q * nstrips;
       chunk = (int)(q * 8 + (lt >> 5));
-      unsigned f = strip * 32 + (lt & 31);
+      unsigned f = (strip * 32 + (lt & 31)) * V;
       if (chunk >= nchunks) continue;  // warp-uniform (one chunk per warp)
       if ((long long)f >= WS) {
         valid = false;
-        f = (unsigned)(WS - 1);
+        f = (unsigned)(WS - V);
       }
       chunk += chunk0;
       const unsigned cell = fastdiv(f, s_m, s_l);
@@ -150,8 +160,8 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
       out_base = f;  // same column of the tmp interior (row offset added per i)
       cellbase = cell;
     } else {
-      const unsigned rest = fastdiv(t, s_m, s_l);
-      c = (int)(t - rest * (unsigned)S);
+      const unsigned rest = fastdiv(t, sv_m, sv_l);
+      c = (int)(t - rest * SV) * V;
       const unsigned yl = fastdiv(rest, nc_m, nc_l);
       chunk = (int)(rest - yl * (unsigned)nchunks);
       const unsigned y = yl + (unsigned)pg.r0;
@@ -159,79 +169,106 @@ __global__ void __launch_bounds__(256, BPAD_MINB) blur_pad_kernel(const float* _
       out_base = (long long)y * WS + c;
       cellbase = (long long)y * W;
     }
-    valid = valid && c < C;  // pad channels: zero in, zero out (computed, not stored)
+    bool vch[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) vch[v] = valid && c + v < C;  // pad channels: zero in, zero out (not stored)
     const int i0 = chunk * R;
     const float* line = in + in_base;
+    auto ldv = [&](const float* p, float (&o)[V]) {
+      if (V == 2) {
+        const float2 q2 = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = q2.x;
+        o[V - 1] = q2.y;
+      } else {
+        o[0] = __ldg(p);
+      }
+    };
     // lo ring: in[i0+k-h+t] at slot (k+t)%R ; hi ring: in[i0+k+h-t] at slot (k-t)%R
-    double acc[R], lo[R], hi[R];
+    double acc[R][V], lo[R][V], hi[R][V];
     float mx = 0.f;
 #pragma unroll
     for (int k = 0; k < R; k++) {
-      const float xc = __ldg(line + (long long)(i0 + k) * in_stride);
-      const float xl = __ldg(line + (long long)(i0 + k - h) * in_stride);
-      const float xh = __ldg(line + (long long)(i0 + k + h) * in_stride);
-      mx = fmaxf(mx, fmaxf(fabsf(xc), fmaxf(fabsf(xl), fabsf(xh))));
-      acc[k] = __dmul_rn((double)xc, w0);
-      lo[k] = (double)xl;
-      hi[k] = (double)xh;
+      float xc[V], xl[V], xh[V];
+      ldv(line + (long long)(i0 + k) * in_stride, xc);
+      ldv(line + (long long)(i0 + k - h) * in_stride, xl);
+      ldv(line + (long long)(i0 + k + h) * in_stride, xh);
+#pragma unroll
+      for (int v = 0; v < V; v++) {
+        mx = fmaxf(mx, fmaxf(fabsf(xc[v]), fmaxf(fabsf(xl[v]), fabsf(xh[v]))));
+        acc[k][v] = __dmul_rn((double)xc[v], w0);
+        lo[k][v] = (double)xl[v];
+        hi[k][v] = (double)xh[v];
+      }
     }
     const float* plo = line + (long long)(i0 + R - h) * in_stride;  // next lo value
     const float* phi = line + (long long)(i0 + h - 1) * in_stride;  // next hi value
     const double* pw = w + h;
     const int nblk = h / R, rem = h % R;
+    auto tap = [&](int u) {
+      const double wj = __ldg(pw - u);
+#pragma unroll
+      for (int k = 0; k < R; k++)
+#pragma unroll
+        for (int v = 0; v < V; v++)
+          acc[k][v] = fma(__dadd_rn(lo[(k + u) % R][v], hi[(k - u + R) % R][v]), wj, acc[k][v]);
+      float xl[V], xh[V];
+      ldv(plo, xl);
+      ldv(phi, xh);
+#pragma unroll
+      for (int v = 0; v < V; v++) {
+        mx = fmaxf(mx, fmaxf(fabsf(xl[v]), fabsf(xh[v])));
+        lo[u % R][v] = (double)xl[v];
+        hi[(R - 1 - u) % R][v] = (double)xh[v];
+      }
+      plo += in_stride;
+      phi -= in_stride;
+    };
     for (int b = 0; b < nblk; b++) {
 #pragma unroll
-      for (int u = 0; u < R; u++) {
-        const double wj = __ldg(pw - u);
-#pragma unroll
-        for (int k = 0; k < R; k++) acc[k] = fma(__dadd_rn(lo[(k + u) % R], hi[(k - u + R) % R]), wj, acc[k]);
-        const float xl = __ldg(plo), xh = __ldg(phi);
-        mx = fmaxf(mx, fmaxf(fabsf(xl), fabsf(xh)));
-        lo[u % R] = (double)xl;
-        hi[(R - 1 - u) % R] = (double)xh;
-        plo += in_stride;
-        phi -= in_stride;
-      }
+      for (int u = 0; u < R; u++) tap(u);
       pw -= R;
     }
 #pragma unroll
-    for (int u = 0; u < R; u++) {
-      if (u < rem) {
-        const double wj = __ldg(pw - u);
-#pragma unroll
-        for (int k = 0; k < R; k++) acc[k] = fma(__dadd_rn(lo[(k + u) % R], hi[(k - u + R) % R]), wj, acc[k]);
-        const float xl = __ldg(plo), xh = __ldg(phi);
-        mx = fmaxf(mx, fmaxf(fabsf(xl), fabsf(xh)));
-        lo[u % R] = (double)xl;
-        hi[(R - 1 - u) % R] = (double)xh;
-        plo += in_stride;
-        phi -= in_stride;
-      }
-    }
+    for (int u = 0; u < R; u++)
+      if (u < rem) tap(u);
     const double B = bscale * (double)mx;
     unsigned unsure = 0u;
 #pragma unroll
     for (int k = 0; k < R; k++) {
       const int i = i0 + k;
-      const bool ok = valid && i < n;
-      const float a = __double2float_rn(__dsub_rn(acc[k], B));
-      const float bb = __double2float_rn(__dadd_rn(acc[k], B));
-      float r = __double2float_rn(acc[k]);
-      if (ok && a != bb) unsure |= 1u << k;
-      if (ok) {
+      float r[V];
+#pragma unroll
+      for (int v = 0; v < V; v++) {
+        const bool ok = vch[v] && i < n;
+        const float a = __double2float_rn(__dsub_rn(acc[k][v], B));
+        const float bb = __double2float_rn(__dadd_rn(acc[k][v], B));
+        r[v] = __double2float_rn(acc[k][v]);
+        if (ok && a != bb) unsure |= 1u << (k * V + v);
+      }
+      if (i < n && vch[0]) {
         const long long o = out_base + (long long)i * out_stride;
-        if (EPI == 1) r = __fdiv_rn(r, den32[cellbase + i]);
-        out[o] = r;
+        if (EPI == 1) {
+          const float dn = den32[cellbase + i];
+#pragma unroll
+          for (int v = 0; v < V; v++) r[v] = __fdiv_rn(r[v], dn);
+        }
+        if (V == 2 && vch[V - 1])
+          *reinterpret_cast<float2*>(out + o) = make_float2(r[0], r[V - 1]);
+        else
+          out[o] = r[0];
       }
     }
     // rare: uncertain outputs go to the fallback list (full-warp ballots)
     if (__any_sync(PLAS_FULL_MASK, unsure != 0u)) {
 #pragma unroll
-      for (int k = 0; k < R; k++) {
-        const int i = i0 + k;
-        const long long o = out_base + (long long)i * out_stride;
-        fb_append_full((unsure >> k) & 1u, (int)(AXIS == 0 ? (long long)i * WS + in_base : o), fb, fb_cap);
-      }
+      for (int k = 0; k < R; k++)
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+          const int i = i0 + k;
+          const long long o = out_base + (long long)i * out_stride + v;
+          fb_append_full((unsure >> (k * V + v)) & 1u,
+                         (int)(AXIS == 0 ? (long long)i * WS + in_base + v : o), fb, fb_cap);
+        }
     }
   }
 }
